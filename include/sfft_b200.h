@@ -1,0 +1,167 @@
+/*
+ * sfft_b200.h — C ABI of the B200 multiple-rank-1-lattice (MR1L) hot path.
+ *
+ * The reference (arXiv 1711.05152 package `sfft`, /root/reference/pkg/src/sfft)
+ * is pure Python; it has no native boundary.  These entry points replace the
+ * internal seams of its MR1L reconstruction step one-for-one, and
+ * are bound from Python with ctypes by paper_1711_05152_b200/_native.py.
+ *
+ * Conventions
+ *   - d_* arguments are DEVICE pointers owned by the caller; h_* are HOST
+ *     pointers to small metadata (copied into kernel parameters, never
+ *     retained).  No call allocates device memory; scratch is caller-provided.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and returns 0 on success, a cudaError_t value (> 0) on a
+ *     CUDA error, or a negative errno-style code on an argument error.
+ *     sfft_error_string() names the code.
+ *   - Frequency sets are component-major int32: freqs[c * n + i] is component c
+ *     of candidate i (|k_c| <= 2^31 - 1, lattice.py:36-38).  Candidate sets are
+ *     kept lexicographically sorted (lattice.py:63-77).
+ *   - Complex arrays are interleaved complex128 (double re, im).
+ *   - Lattice metadata: h_m[l] = M_l (1 <= M_l <= 2^31 - 1), h_z[l * t1 + c]
+ *     = z_l[c] in [0, M_l) (lattice.py:284-294).  One "unit" is one
+ *     (iteration i, lattice l) pair, numbered u = i * L + l; unit u owns the
+ *     transform buffer d_buf + 2 * u * P doubles.
+ *   - Thread-safe across distinct streams / devices; one host thread per GPU.
+ */
+#ifndef SFFT_B200_H
+#define SFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFFT_B200_ABI_VERSION 1
+
+int sfft_abi_version(void);
+const char* sfft_error_string(int code);
+/* number of SMs and compute capability of the current device */
+int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);
+
+/* ---- K3: alias histogram, masks, coverage --------------------------------
+ * Replaces construct.py:139-143 (_alias_free_mask) evaluated for every prime
+ * of one attempt of build_multiple_lattice (construct.py:146-182), with
+ * residues as lattice.py:511-517.  masks[i] bit l = candidate i is alias-free
+ * on lattice l.  stats[0] = max_i (index of the lowest set bit + 1) (the
+ * early-exit lattice count when every mask is nonzero), stats[1] = number of
+ * candidates with an empty mask.  kmax bounds |k_c| (selects exact fast
+ * arithmetic when d*kmax*M < 2^52).  L <= 64, L * t1 <= 4096, t1 <= 64. */
+int64_t sfft_alias_scratch_words(const int64_t* h_m, int L);
+int sfft_alias_masks(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax,
+                     const int64_t* h_m, const int32_t* h_z, int L,
+                     uint32_t* d_scratch, int64_t scratch_words,
+                     uint64_t* d_masks, int32_t* d_stats, void* stream);
+
+/* ---- per-lattice tables ----------------------------------------------------
+ * tw[off_l + n] = e^{+2 pi i n / M_l}, chirp[off_l + n] = e^{-pi i (n^2 mod 2M_l)/M_l},
+ * off_l = sum_{l' < l} M_l' (both arrays hold sum_l M_l complex values). */
+int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp, void* stream);
+
+/* ---- K2: Bluestein prime-length DFT (transform.py:50-64, scipy.fft.fft) -----
+ * P = 2^p >= 2 * max M_l - 1, 4 <= p <= 24.  sfft_fft_tables fills the FFT
+ * twiddle tables (sfft_fft_table_len(p) complex values); sfft_bluestein_bhat
+ * builds the transformed Bluestein kernel of each lattice (L * P complex);
+ * sfft_bluestein transforms `nunits` pre-chirped buffers in place and leaves
+ * the unnormalised DFT X_k (k < M of the unit's lattice) in d_buf. */
+int64_t sfft_fft_table_len(int p);
+int sfft_fft_tables(int p, double* d_ftab, void* stream);
+int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
+                        const double* d_chirp, double* d_bhat, void* stream);
+int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
+                   const double* d_bhat, const double* d_chirp, double* d_buf, void* stream);
+
+/* ---- K1: sampling at lattice nodes ----------------------------------------
+ * Sparse polynomial oracle (testbed.py:116-127) on the nodes of
+ * _invert_candidates (detect.py:290-299): unit u = i*L + l gets
+ * x_n * chirp_l[n] (n < M_l) in its buffer, x_n = p(node n of lattice l with
+ * anchor tail i).  Terms: d_hfreqs component-major (d x s int32), d_hcoef s
+ * complex.  h_anchor: rb x (d - t1) doubles.  Scratch: d_cprime rb*s complex,
+ * d_rres and d_rj L*s int32 each.  apply_chirp = 0 leaves the raw samples. */
+int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                     const int64_t* h_m, const int32_t* h_z, int L,
+                     const double* h_anchor, int rb,
+                     double* d_cprime, int32_t* d_rres, int32_t* d_rj,
+                     const double* d_tw, const double* d_chirp,
+                     double* d_buf, int64_t P, int apply_chirp, void* stream);
+/* B-spline oracle (testbed.py:198-244): ngroups tensor-product terms; group g
+ * has spline order h_order[g] (<= 8), scale h_scale[g] = C_m * m, and the
+ * component slots h_comps[h_start[g] .. h_start[g+1]). */
+int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_start,
+                        const int32_t* h_comps, const double* h_scale, int d, int t1,
+                        const int64_t* h_m, const int32_t* h_z, int L,
+                        const double* h_anchor, int rb, const double* d_chirp,
+                        double* d_buf, int64_t P, int apply_chirp, void* stream);
+/* Host-callback / noisy oracles: d_buf holds raw samples; adds
+ * d_sigma[u] * d_noise[u * nstride + n] when d_noise != NULL (NoisyOracle,
+ * testbed.py:100-106), then applies the pre-chirp. */
+int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp,
+                        double* d_buf, int64_t P, const double* d_noise, int64_t nstride,
+                        const double* d_sigma, void* stream);
+/* sum_n |x_n|^2 per unit over n < M (relative-SNR noise calibration). */
+int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
+                    double* d_out, void* stream);
+/* Node coordinates of lattice l (lattice.py:505-508 + anchor tail,
+ * detect.py:294-297): d_pts is M_l x d row-major float64. */
+int sfft_lattice_nodes(const int64_t* h_m, const int32_t* h_z, int L, int t1, int l, int d,
+                       const double* h_anchor_tail, double* d_pts, void* stream);
+
+/* ---- K4: gather + average + threshold (transform.py:99-127, detect.py:197-204)
+ * For iterations it0 .. it0+rb-1 (rb <= 8) of the step: coef[(it0+i)*n + k] =
+ * average over lattices l < L with mask bit l of X_{i,l}[k.z_l mod M_l] / M_l;
+ * keep = |coef| >= delta (0 for uncovered k); counts[it0+i] += #kept. */
+int sfft_gather_select(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax,
+                       const int64_t* h_m, const int32_t* h_z, int L,
+                       const uint64_t* d_masks, const double* d_buf, int64_t P,
+                       int rb, int it0, double delta,
+                       double* d_coef, uint8_t* d_keep, int32_t* d_counts, void* stream);
+/* cap selection of one iteration (detect.py:205-211) */
+int64_t sfft_select_scratch_bytes(int64_t n);
+int sfft_select_cap(const double* d_coef, uint8_t* d_keep, int64_t n, int cap,
+                    uint8_t* d_scratch, void* stream);
+
+/* ---- compaction / sets (detect.py:257-260, 367-371, 412; lattice.py:97-109) */
+int64_t sfft_scan_scratch_len(int64_t n);
+/* ascending indices i with OR_r flags[r*n + i] != 0; *d_total = count */
+int sfft_flag_indices(const uint8_t* d_flags, int64_t n, int nrows, int32_t* d_idx,
+                      int32_t* d_total, int32_t* d_scratch, void* stream);
+int sfft_gather_rows(const int32_t* d_in, int64_t n_in, int ncomp, const int32_t* d_idx,
+                     const int32_t* d_count, int64_t cap_rows, int32_t* d_out, int64_t out_stride,
+                     const double* d_cin, double* d_cout, void* stream);
+int sfft_candidate_product(const int32_t* d_prefix, int64_t np, int t, const int32_t* d_comp,
+                           int64_t nc, int32_t* d_out, void* stream);
+
+/* residues k . z_l mod M_l (lattice.py:511-529) of every candidate on every
+ * lattice: d_out[l * n + i], int64. */
+int sfft_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                  const int32_t* h_z, int L, int64_t* d_out, void* stream);
+
+/* ---- line detection (detect.py:175-240) ------------------------------------
+ * r lines of K points of component t (K <= 1024), anchors h_anchors (r x d). */
+int sfft_line_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t,
+                          int K, const double* h_anchors, int r, double* d_values, void* stream);
+int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, double delta,
+                     double* d_coefs, uint8_t* d_keep, void* stream);
+
+/* ---- oracle evaluation at arbitrary points (testbed.py:60-73, 116-127, 232-244)
+ * d_pts: n x d row-major float64 in [0,1)^d; d_out: n complex.  These back the
+ * device oracles' __call__ and the line samples of non-polynomial oracles. */
+int sfft_eval_poly_points(const double* d_pts, int64_t n, int d, const int32_t* d_hfreqs,
+                          const double* d_hcoef, int s, double* d_out, void* stream);
+int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,
+                             const int32_t* h_order, const int32_t* h_start,
+                             const int32_t* h_comps, const double* h_scale, double* d_out,
+                             void* stream);
+/* d_x[i] += scale * d_noise[i] (complex; NoisyOracle update, testbed.py:104-106) */
+int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, void* stream);
+
+/* ---- utilities ---------------------------------------------------------------- */
+int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream);
+/* FP64 roofline probe: blocks x 256 threads x iters x 16 DFMA */
+int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFFT_B200_H */

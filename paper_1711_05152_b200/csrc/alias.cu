@@ -1,0 +1,144 @@
+// K3: alias histogram, alias-free masks and coverage of one randomized MR1L
+// attempt over all L_max pre-drawn lattices at once.
+//
+// Reference: construct.py:139-143 (_alias_free_mask: residues, bincount,
+// counts[res] == 1), construct.py:173-181 (per-prime loop, covered |= mask,
+// early exit when covered.all()), lattice.py:511-517 (residues).
+//
+// Pre-drawing all L_max generating vectors of an attempt is stream-identical
+// to the reference's sequential draw (the attempt's generator is discarded
+// afterwards, SURVEY §7 hard part 1), so the early exit becomes a reduction:
+// candidate k is first covered by lattice ctz(mask_k); the attempt uses
+// L = max_k (ctz(mask_k) + 1) lattices when every mask is nonzero.
+//
+// The histogram only needs "seen once" / "seen at least twice" per bin, so it
+// is kept as two bitmaps per lattice (2 bits per residue bin instead of an
+// int64 count): seen1 |= bit; if the bit was already set, seen2 |= bit.  The
+// result is exact for any multiplicity and the bitmaps (sum_l M_l / 4 bytes)
+// stay L2-resident even at |J| = 6.5e5, d = 20 (29 lattices, ~9 MB).
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace sfft {
+
+// bitmap word offsets: lattice l owns words [bw[l], bw[l+1]) in each bitmap
+__device__ __forceinline__ int64_t bm_words(int64_t m) { return (m + 31) >> 5; }
+
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+                  uint32_t* __restrict__ seen1, uint32_t* __restrict__ seen2, int64_t words_total) {
+  __shared__ int64_t bw[SFFT_LMAX + 1];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int l = 0; l < lt.nlat; ++l) { bw[l] = acc; acc += bm_words(lt.m[l]); }
+    bw[lt.nlat] = acc;
+  }
+  __syncthreads();
+  const int d = lt.d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    for (int l = 0; l < lt.nlat; ++l) {
+      const int64_t r = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+      const int64_t w = bw[l] + (r >> 5);
+      const uint32_t bit = 1u << (r & 31);
+      const uint32_t old = atomicOr(&seen1[w], bit);
+      if (old & bit) atomicOr(&seen2[w], bit);
+    }
+  }
+}
+
+// stats[0] = max_k first-cover index (1-based), stats[1] = #candidates with an empty mask
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+                  const uint32_t* __restrict__ seen2, uint64_t* __restrict__ masks,
+                  int32_t* __restrict__ stats) {
+  __shared__ int64_t bw[SFFT_LMAX + 1];
+  __shared__ int red[32];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int l = 0; l < lt.nlat; ++l) { bw[l] = acc; acc += bm_words(lt.m[l]); }
+    bw[lt.nlat] = acc;
+  }
+  __syncthreads();
+  const int d = lt.d;
+  int first_max = 0, empty = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    uint64_t mask = 0;
+    for (int l = 0; l < lt.nlat; ++l) {
+      const int64_t r = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+      const uint32_t wv = __ldg(&seen2[bw[l] + (r >> 5)]);
+      if (!((wv >> (r & 31)) & 1u)) mask |= (1ull << l);
+    }
+    masks[i] = mask;
+    if (mask) first_max = max(first_max, __ffsll((long long)mask));
+    else empty += 1;
+  }
+  // block reductions
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    first_max = max(first_max, __shfl_down_sync(0xffffffffu, first_max, o));
+    empty += __shfl_down_sync(0xffffffffu, empty, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[wid] = first_max; red[16 + wid] = empty; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int fm = 0, em = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { fm = max(fm, red[w]); em += red[16 + w]; }
+    if (fm) atomicMax(&stats[0], fm);
+    if (em) atomicAdd(&stats[1], em);
+  }
+}
+
+int64_t alias_scratch_words(const LatTable& lt) {
+  int64_t acc = 0;
+  for (int l = 0; l < lt.nlat; ++l) acc += (lt.m[l] + 31) >> 5;
+  return 2 * acc;
+}
+
+template <int DM, bool FAST>
+static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+                           int64_t words, uint64_t* masks, int32_t* stats, int blocks,
+                           cudaStream_t st) {
+  alias_mark_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits, bits + words / 2, words);
+  alias_mask_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits + words / 2, masks, stats);
+}
+
+int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+                 int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
+                 cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st);
+  if (e != cudaSuccess) return (int)e;
+  if (n == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  int blocks = (int)(want < cap ? want : cap);
+  const int d = lt.d;
+#define SFFT_ALIAS_CASE(DMV)                                                                 \
+  if (d <= DMV) {                                                                            \
+    if (fast) launch_alias_t<DMV, true>(freqs, n, lt, bits, words, masks, stats, blocks, st); \
+    else launch_alias_t<DMV, false>(freqs, n, lt, bits, words, masks, stats, blocks, st);     \
+    SFFT_CHECK_LAUNCH();                                                                     \
+    return 0;                                                                                \
+  }
+  SFFT_ALIAS_CASE(4)
+  SFFT_ALIAS_CASE(8)
+  SFFT_ALIAS_CASE(16)
+  SFFT_ALIAS_CASE(32)
+  SFFT_ALIAS_CASE(64)
+#undef SFFT_ALIAS_CASE
+  return -22;  // EINVAL: dimension too large
+}
+
+}  // namespace sfft

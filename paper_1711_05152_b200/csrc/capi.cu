@@ -1,0 +1,436 @@
+// extern "C" boundary (include/sfft_b200.h): validates arguments, builds the
+// by-value launch structs and dispatches to the kernels.
+#include <math.h>
+#include <string.h>
+
+#include "../../include/sfft_b200.h"
+#include "common.cuh"
+#include "gather.cuh"
+#include "lines.cuh"
+#include "plan.cuh"
+#include "sample.cuh"
+
+namespace sfft {
+int launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t st);
+int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* hf,
+                            const double2* coef, int s, double2* out, cudaStream_t st);
+int launch_eval_bspline_points(const double* pts, int64_t n, const BsplineSpec& bs, double2* out,
+                               int num_sms, cudaStream_t st);
+int launch_add_noise(double2* x, const double2* e, int64_t n, double scale, int num_sms,
+                     cudaStream_t st);
+}
+
+using namespace sfft;
+
+namespace {
+
+constexpr int E_INVAL = -22;
+constexpr int E_2BIG = -7;
+
+int num_sms_current() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+int fill_lat(LatTable& lt, const int64_t* h_m, const int32_t* h_z, int L, int t1) {
+  if (L < 0 || L > SFFT_LMAX) return E_2BIG;
+  if (t1 < 0 || t1 > SFFT_DMAX || (int64_t)L * t1 > SFFT_ZMAX) return E_2BIG;
+  memset(&lt, 0, sizeof(LatTable));
+  lt.nlat = L;
+  lt.d = t1;
+  int64_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    const int64_t m = h_m[l];
+    if (m < 1 || m > 2147483647LL) return E_INVAL;
+    lt.m[l] = m;
+    lt.inv_m[l] = 1.0 / (double)m;
+    lt.off[l] = off;
+    off += m;
+    if (h_z)
+      for (int c = 0; c < t1; ++c) {
+        int64_t zc = h_z[l * t1 + c];
+        if (zc < 0 || zc >= m) return E_INVAL;
+        lt.z[l * t1 + c] = (int32_t)zc;
+      }
+  }
+  return 0;
+}
+
+int fill_units(UnitTable& ut, const int64_t* h_m, int L, int rb) {
+  if (L < 1 || L > SFFT_LMAX || rb < 1 || (int64_t)rb * L > SFFT_UMAX) return E_2BIG;
+  memset(&ut, 0, sizeof(UnitTable));
+  ut.nunits = rb * L;
+  ut.nlat = L;
+  int64_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    ut.m[l] = h_m[l];
+    ut.off[l] = off;
+    off += h_m[l];
+  }
+  for (int i = 0; i < rb; ++i)
+    for (int l = 0; l < L; ++l) {
+      ut.lat[i * L + l] = l;
+      ut.it[i * L + l] = i;
+    }
+  return 0;
+}
+
+bool residue_fast(int t1, int64_t kmax, const int64_t* h_m, int L) {
+  int64_t mmax = 1;
+  for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
+  const double bound = (double)t1 * (double)(kmax < 0 ? -kmax : kmax) * (double)mmax;
+  return bound < 4.0e15;  // < 2^52 with margin
+}
+
+bool mulmod_fast(const int64_t* h_m, int L) {
+  int64_t mmax = 1;
+  for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
+  const double b = (double)(mmax + 64) * (double)(mmax + 64);
+  return b < 4.0e15;
+}
+
+int fill_bspline(BsplineSpec& bs, int ngroups, const int32_t* h_order, const int32_t* h_start,
+                 const int32_t* h_comps, const double* h_scale, int d) {
+  if (ngroups < 0 || ngroups > 8 || d < 1 || d > SFFT_DMAX) return E_INVAL;
+  memset(&bs, 0, sizeof(bs));
+  bs.d = d;
+  bs.ngroups = ngroups;
+  if (h_start[0] != 0 || h_start[ngroups] > SFFT_DMAX) return E_2BIG;
+  for (int g = 0; g <= ngroups; ++g) bs.start[g] = h_start[g];
+  for (int g = 0; g < ngroups; ++g) {
+    if (h_order[g] < 1 || h_order[g] > 7 || h_start[g + 1] < h_start[g]) return E_INVAL;
+    bs.order[g] = h_order[g];
+    bs.scale[g] = h_scale[g];
+  }
+  for (int q = 0; q < h_start[ngroups]; ++q) {
+    if (h_comps[q] < 0 || h_comps[q] >= d) return E_INVAL;
+    bs.comps[q] = h_comps[q];
+  }
+  return 0;
+}
+
+// J1 (multiple of 64) minimising the padded tile count J1 * 64 * ceil(J2 / 64)
+void choose_j1(int64_t m, int& j1, int& nt1, int& nt2) {
+  int64_t best = -1;
+  int bj = 64;
+  const int64_t amax = (m + 63) / 64;
+  const int64_t alim = amax < 4096 ? amax : 4096;
+  const double root = sqrt((double)m);
+  for (int64_t a = 1; a <= alim; ++a) {
+    const int64_t J1 = 64 * a;
+    const int64_t J2 = (m + J1 - 1) / J1;
+    const int64_t padded = J1 * 64 * ((J2 + 63) / 64);
+    if (best < 0 || padded < best ||
+        (padded == best && fabs((double)J1 - root) < fabs((double)bj - root))) {
+      best = padded;
+      bj = (int)J1;
+    }
+  }
+  j1 = bj;
+  nt1 = bj / 64;
+  const int64_t J2 = (m + bj - 1) / bj;
+  nt2 = (int)((J2 + 63) / 64);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfft_abi_version(void) { return SFFT_B200_ABI_VERSION; }
+
+const char* sfft_error_string(int code) {
+  if (code == 0) return "ok";
+  if (code == E_INVAL) return "invalid argument";
+  if (code == E_2BIG) return "argument exceeds a device-table limit";
+  if (code > 0) return cudaGetErrorString((cudaError_t)code);
+  return "unknown error";
+}
+
+int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  if (num_sms) *num_sms = num_sms_current();
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return 0;
+}
+
+int64_t sfft_alias_scratch_words(const int64_t* h_m, int L) {
+  int64_t acc = 0;
+  for (int l = 0; l < L; ++l) acc += (h_m[l] + 31) >> 5;
+  return 2 * acc;
+}
+
+int sfft_alias_masks(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                     const int32_t* h_z, int L, uint32_t* d_scratch, int64_t scratch_words,
+                     uint64_t* d_masks, int32_t* d_stats, void* stream) {
+  if (n < 0 || t1 < 1 || L < 1) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  const int64_t need = sfft_alias_scratch_words(h_m, L);
+  if (scratch_words < need) return E_INVAL;
+  return launch_alias(d_freqs, n, lt, d_scratch, need, d_masks, d_stats,
+                      residue_fast(t1, kmax, h_m, L), num_sms_current(), S(stream));
+}
+
+int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp, void* stream) {
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, nullptr, L, 0);
+  if (rc) return rc;
+  if (L == 0) return 0;
+  return launch_lattice_tables(lt, (double2*)d_tw, (double2*)d_chirp, S(stream));
+}
+
+int64_t sfft_fft_table_len(int p) {
+  if (p < 4 || p > 24) return -1;
+  return fft_geom(p).table_len;
+}
+
+int sfft_fft_tables(int p, double* d_ftab, void* stream) {
+  if (p < 4 || p > 24) return E_INVAL;
+  return launch_fft_tables(p, (double2*)d_ftab, S(stream));
+}
+
+int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
+                        const double* d_chirp, double* d_bhat, void* stream) {
+  if (p < 4 || p > 24) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, nullptr, L, 0);
+  if (rc) return rc;
+  for (int l = 0; l < L; ++l)
+    if (2 * h_m[l] - 1 > ((int64_t)1 << p)) return E_INVAL;
+  return launch_bhat(lt, (const double2*)d_chirp, (double2*)d_bhat, p, (const double2*)d_ftab,
+                     S(stream));
+}
+
+int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
+                   const double* d_bhat, const double* d_chirp, double* d_buf, void* stream) {
+  if (p < 4 || p > 24) return E_INVAL;
+  UnitTable ut;
+  int rc = fill_units(ut, h_m, L, rb);
+  if (rc) return rc;
+  for (int l = 0; l < L; ++l)
+    if (2 * h_m[l] - 1 > ((int64_t)1 << p)) return E_INVAL;
+  return launch_bluestein((double2*)d_buf, ut, p, (const double2*)d_ftab, (const double2*)d_bhat,
+                          (const double2*)d_chirp, S(stream));
+}
+
+int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                     const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                     double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                     const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                     void* stream) {
+  if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  if ((int64_t)rb * L > SFFT_UMAX || rb < 1) return E_2BIG;
+  const int tail = d - t1;
+  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  AnchorTable at;
+  at.rb = rb;
+  at.tail = tail;
+  for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
+  PolyPlan* pp = new PolyPlan;
+  memset(pp, 0, sizeof(PolyPlan));
+  pp->nunits = rb * L;
+  pp->s = s;
+  int tiles_l[SFFT_LMAX];
+  for (int l = 0; l < L; ++l) {
+    int j1, nt1, nt2;
+    choose_j1(h_m[l], j1, nt1, nt2);
+    pp->J1[l] = j1;
+    pp->nt1[l] = nt1;
+    tiles_l[l] = nt1 * nt2;
+  }
+  int64_t acc = 0;
+  for (int i = 0; i < rb; ++i)
+    for (int l = 0; l < L; ++l) {
+      const int u = i * L + l;
+      pp->unit_lat[u] = l;
+      pp->unit_it[u] = i;
+      pp->tile_start[u] = (int)acc;
+      acc += tiles_l[l];
+    }
+  pp->tile_start[rb * L] = (int)acc;
+  if (acc > 0x7fffffffLL) { delete pp; return E_2BIG; }
+  cudaStream_t st = S(stream);
+  rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at,
+                           (double2*)d_cprime, d_rres, d_rj, st);
+  if (!rc)
+    rc = launch_sample_poly(*pp, lt, (const double2*)d_cprime, d_rres, d_rj, (const double2*)d_tw,
+                            (const double2*)d_chirp, (double2*)d_buf, P, mulmod_fast(h_m, L),
+                            apply_chirp != 0, st);
+  delete pp;
+  return rc;
+}
+
+int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_start,
+                        const int32_t* h_comps, const double* h_scale, int d, int t1,
+                        const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor,
+                        int rb, const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                        void* stream) {
+  if (ngroups < 0 || ngroups > 8 || d < 1 || d > SFFT_DMAX || t1 < 1 || t1 > d) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb);
+  if (rc) return rc;
+  BsplineSpec bs;
+  rc = fill_bspline(bs, ngroups, h_order, h_start, h_comps, h_scale, d);
+  if (rc) return rc;
+  const int tail = d - t1;
+  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  AnchorTable at;
+  at.rb = rb;
+  at.tail = tail;
+  for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
+  return launch_sample_bspline(ut, lt, bs, at, (const double2*)d_chirp, (double2*)d_buf, P,
+                               mulmod_fast(h_m, L), apply_chirp != 0, num_sms_current(),
+                               S(stream));
+}
+
+int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp, double* d_buf,
+                        int64_t P, const double* d_noise, int64_t nstride, const double* d_sigma,
+                        void* stream) {
+  UnitTable ut;
+  int rc = fill_units(ut, h_m, L, rb);
+  if (rc) return rc;
+  return launch_finish_samples(ut, (const double2*)d_chirp, (double2*)d_buf, P,
+                               (const double2*)d_noise, nstride, d_sigma, num_sms_current(),
+                               S(stream));
+}
+
+int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
+                    double* d_out, void* stream) {
+  UnitTable ut;
+  int rc = fill_units(ut, h_m, L, rb);
+  if (rc) return rc;
+  return launch_unit_norm2(ut, (const double2*)d_buf, P, d_out, num_sms_current(), S(stream));
+}
+
+int sfft_lattice_nodes(const int64_t* h_m, const int32_t* h_z, int L, int t1, int l, int d,
+                       const double* h_anchor_tail, double* d_pts, void* stream) {
+  if (l < 0 || l >= L || t1 < 1 || t1 > d || d > SFFT_DMAX) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  AnchorTable at;
+  at.rb = 1;
+  at.tail = d - t1;
+  for (int i = 0; i < d - t1; ++i) at.a[i] = h_anchor_tail[i];
+  return launch_lattice_nodes(lt, l, d, at, 0, d_pts, mulmod_fast(h_m, L), S(stream));
+}
+
+int sfft_gather_select(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                       const int32_t* h_z, int L, const uint64_t* d_masks, const double* d_buf,
+                       int64_t P, int rb, int it0, double delta, double* d_coef, uint8_t* d_keep,
+                       int32_t* d_counts, void* stream) {
+  if (n < 0 || rb < 1 || rb > 8 || it0 < 0) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  return launch_gather(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, rb, it0, delta,
+                       (double2*)d_coef, d_keep, d_counts, residue_fast(t1, kmax, h_m, L),
+                       num_sms_current(), S(stream));
+}
+
+int64_t sfft_select_scratch_bytes(int64_t n) { return select_scratch_bytes(n); }
+
+int sfft_select_cap(const double* d_coef, uint8_t* d_keep, int64_t n, int cap, uint8_t* d_scratch,
+                    void* stream) {
+  if (n < 0 || cap < 0) return E_INVAL;
+  return launch_select_cap((const double2*)d_coef, d_keep, n, cap, d_scratch, num_sms_current(),
+                           S(stream));
+}
+
+int64_t sfft_scan_scratch_len(int64_t n) { return scan_scratch_len(n); }
+
+int sfft_flag_indices(const uint8_t* d_flags, int64_t n, int nrows, int32_t* d_idx,
+                      int32_t* d_total, int32_t* d_scratch, void* stream) {
+  if (n < 0 || n > 0x7fffffffLL || nrows < 1) return E_INVAL;
+  return launch_flag_indices(d_flags, n, nrows, d_idx, d_total, d_scratch, S(stream));
+}
+
+int sfft_gather_rows(const int32_t* d_in, int64_t n_in, int ncomp, const int32_t* d_idx,
+                     const int32_t* d_count, int64_t cap_rows, int32_t* d_out, int64_t out_stride,
+                     const double* d_cin, double* d_cout, void* stream) {
+  return launch_gather_rows(d_in, n_in, ncomp, d_idx, d_count, cap_rows, d_out, out_stride,
+                            (const double2*)d_cin, (double2*)d_cout, num_sms_current(), S(stream));
+}
+
+int sfft_candidate_product(const int32_t* d_prefix, int64_t np, int t, const int32_t* d_comp,
+                           int64_t nc, int32_t* d_out, void* stream) {
+  if (np < 0 || nc < 0 || t < 0) return E_INVAL;
+  return launch_product(d_prefix, np, t, d_comp, nc, d_out, num_sms_current(), S(stream));
+}
+
+int sfft_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                  const int32_t* h_z, int L, int64_t* d_out, void* stream) {
+  if (n < 0 || t1 < 1) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  return launch_residues(d_freqs, n, lt, d_out, residue_fast(t1, kmax, h_m, L), num_sms_current(),
+                         S(stream));
+}
+
+int sfft_line_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t,
+                          int K, const double* h_anchors, int r, double* d_values, void* stream) {
+  if ((int64_t)r * d > 2048 || t < 0 || t >= d) return E_2BIG;
+  LineAnchors la;
+  for (int i = 0; i < r * d; ++i) la.a[i] = h_anchors[i];
+  return launch_line_sample_poly(d_hfreqs, (const double2*)d_hcoef, s, d, t, K, la, r,
+                                 (double2*)d_values, S(stream));
+}
+
+int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, double delta,
+                     double* d_coefs, uint8_t* d_keep, void* stream) {
+  return launch_line_select((const double2*)d_values, r, K, lo, cap, delta, (double2*)d_coefs,
+                            d_keep, S(stream));
+}
+
+int sfft_eval_poly_points(const double* d_pts, int64_t n, int d, const int32_t* d_hfreqs,
+                          const double* d_hcoef, int s, double* d_out, void* stream) {
+  if (n < 0 || d < 1 || s < 0) return E_INVAL;
+  return launch_eval_poly_points(d_pts, n, d, d_hfreqs, (const double2*)d_hcoef, s,
+                                 (double2*)d_out, S(stream));
+}
+
+int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,
+                             const int32_t* h_order, const int32_t* h_start,
+                             const int32_t* h_comps, const double* h_scale, double* d_out,
+                             void* stream) {
+  BsplineSpec bs;
+  int rc = fill_bspline(bs, ngroups, h_order, h_start, h_comps, h_scale, d);
+  if (rc) return rc;
+  return launch_eval_bspline_points(d_pts, n, bs, (double2*)d_out, num_sms_current(), S(stream));
+}
+
+int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, void* stream) {
+  if (n < 0) return E_INVAL;
+  return launch_add_noise((double2*)d_x, (const double2*)d_noise, n, scale, num_sms_current(),
+                          S(stream));
+}
+
+int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream) {
+  return launch_cscale((double2*)d_x, n, scale, conj, num_sms_current(), S(stream));
+}
+
+int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream) {
+  return launch_fp64_peak(d_out, iters, blocks, S(stream));
+}
+
+}  // extern "C"

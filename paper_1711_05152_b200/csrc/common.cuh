@@ -1,0 +1,102 @@
+// Shared device helpers for the MR1L hot path (sm_100a).
+//
+// Exact residue arithmetic: every lattice size M satisfies 1 <= M <= 2^31-1
+// (reference lattice.py:36-38, 290-294), so a single product of two residues
+// fits in 62 bits.  The fast reduction below needs |x| < 2^52, which the host
+// checks before it selects the FAST template variants; the slow variants use
+// 64-bit integer division and are exact for every admissible input.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SFFT_DMAX 64          // largest dimension handled by the device kernels
+#define SFFT_LMAX 64          // masks are one uint64 word per candidate
+
+namespace sfft {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// x mod m in [0, m) for |x| < 2^52 and 1 <= m < 2^31 (inv_m = 1.0 / m).
+__device__ __forceinline__ int64_t mod_fast(int64_t x, int64_t m, double inv_m) {
+  int64_t q = (int64_t)floor((double)x * inv_m);
+  int64_t r = x - q * m;
+  if (r < 0) r += m;
+  else if (r >= m) r -= m;
+  return r;
+}
+
+// x mod m in [0, m) for any int64 x.
+__device__ __forceinline__ int64_t mod_slow(int64_t x, int64_t m) {
+  int64_t r = x % m;
+  return r < 0 ? r + m : r;
+}
+
+// (a * b) mod m for 0 <= a, b < m < 2^31.
+template <bool FAST>
+__device__ __forceinline__ int64_t mulmod(int64_t a, int64_t b, int64_t m, double inv_m) {
+  if (FAST) return mod_fast(a * b, m, inv_m);
+  return (int64_t)(((uint64_t)a * (uint64_t)b) % (uint64_t)m);
+}
+
+// Residue k . z mod M of one candidate (components in registers).
+// FAST requires sum_c |k_c| * z_c < 2^52 (host-checked).  Matches
+// reference lattice.py:511-517 (componentwise-reduced inner product).
+template <int DM, bool FAST>
+__device__ __forceinline__ int64_t residue(const int32_t (&k)[DM], int d, const int32_t* z,
+                                           int64_t m, double inv_m) {
+  if (FAST) {
+    int64_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+      if (c < d) acc += (int64_t)k[c] * (int64_t)z[c];
+    return mod_fast(acc, m, inv_m);
+  } else {
+    int64_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+      if (c < d) {
+        int64_t km = mod_slow((int64_t)k[c], m);
+        acc = (acc + (int64_t)(((uint64_t)km * (uint64_t)z[c]) % (uint64_t)m)) % m;
+      }
+    return acc;
+  }
+}
+
+// Block-wide inclusive sum over 32-bit values (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ int block_sum(int v, int* smem32) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) smem32[wid] = v;
+  __syncthreads();
+  int tot = 0;
+  if (threadIdx.x < 32) {
+    int x = (threadIdx.x < (blockDim.x >> 5)) ? smem32[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    tot = x;
+  }
+  return tot;  // valid in thread 0
+}
+
+}  // namespace sfft
+
+#define SFFT_CHECK_LAUNCH()                           \
+  do {                                                \
+    cudaError_t _e = cudaGetLastError();              \
+    if (_e != cudaSuccess) return (int)_e;            \
+  } while (0)

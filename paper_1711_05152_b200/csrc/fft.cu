@@ -1,0 +1,308 @@
+// K2: batched prime-length DFT by Bluestein's algorithm on power-of-two
+// four-step Stockham FFTs (replaces reference transform.py:50-64, the
+// scipy.fft.fft call at transform.py:61, used by invert_multiple :121).
+//
+// For a lattice of prime size M, with chirp c_n = e^{-pi i (n^2 mod 2M) / M}:
+//     X_k = c_k * sum_n (x_n c_n) * conj(c_{k-n})            (k < M)
+// i.e. a linear convolution evaluated as a cyclic one of length
+// P = 2^p >= 2M - 1.  The chirp exponent is reduced mod 2M in integers so
+// the phase is exact for every M < 2^31 (SURVEY §7 hard part 3).
+//
+// Layout of one transform buffer (P complex128): natural index n.  The FFT
+// of length P = P1 * P2 (P2 = 2^min(12,p)) runs as
+//   column pass  : P2 columns of length P1 (stride P2) + twiddle e^{-2pi i n2 k1/P}
+//   row pass     : P1 rows of length P2, fused: forward FFT, * Bhat, inverse
+//                  FFT, * e^{+2pi i n2 k1 / P}
+//   column pass  : inverse length-P1 FFTs, then the post-chirp, written only
+//                  for n < M.
+// Bhat = FFT_P(b) / P with b_m = conj(c_m) wrapped cyclically is built once per
+// lattice by the same forward passes (row pass in FWD_ONLY mode), so its
+// layout matches the data after the forward row FFT by construction.
+#include "common.cuh"
+#include "fft.cuh"
+#include "plan.cuh"
+
+namespace sfft {
+
+// ---------------------------------------------------------------------------
+// tables
+
+// twiddle/chirp tables: tw[n] = e^{+2pi i n/M}, chirp[n] = e^{-pi i (n^2 mod 2M)/M}
+__global__ void lattice_tables_kernel(LatTable lt, double2* __restrict__ tw,
+                                      double2* __restrict__ chirp) {
+  const int l = blockIdx.y;
+  const int64_t m = lt.m[l];
+  const int64_t off = lt.off[l];
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < m;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double s, c;
+    // e^{+2 pi i n / M}: argument 2n/M for sincospi
+    sincospi(2.0 * (double)n / (double)m, &s, &c);
+    tw[off + n] = make_double2(c, s);
+    const int64_t m2 = 2 * m;
+    const int64_t nn = (int64_t)(((uint64_t)n * (uint64_t)n) % (uint64_t)m2);
+    sincospi((double)nn / (double)m, &s, &c);
+    chirp[off + n] = make_double2(c, -s);
+  }
+}
+
+// FFT tables for one P: [twP1 | twP2 | Tlo | Thi], all e^{-2 pi i m / N}
+__global__ void fft_tables_kernel(int p, double2* __restrict__ out) {
+  const FftGeom g = fft_geom(p);
+  const int64_t total = g.table_len;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double num, den;
+    if (i < g.P1) { num = (double)i; den = (double)g.P1; }
+    else if (i < g.P1 + g.P2) { num = (double)(i - g.P1); den = (double)g.P2; }
+    else if (i < g.P1 + g.P2 + g.nlo) { num = (double)(i - g.P1 - g.P2); den = (double)g.P; }
+    else { num = (double)((i - g.P1 - g.P2 - g.nlo) << g.qlo); den = (double)g.P; }
+    double s, c;
+    sincospi(2.0 * num / den, &s, &c);
+    out[i] = make_double2(c, -s);
+  }
+}
+
+// e^{-2 pi i m / P} from the two-level table
+__device__ __forceinline__ double2 twP(const FftGeom& g, const double2* __restrict__ tab, int64_t m) {
+  const double2 lo = __ldg(&tab[g.off_lo + (m & (g.nlo - 1))]);
+  const double2 hi = __ldg(&tab[g.off_hi + (m >> g.qlo)]);
+  return cmul(hi, lo);
+}
+
+// Bluestein kernel sequence b: b[m] = e^{+pi i (m^2 mod 2M)/M} for m < M,
+// b[P-m] = b[m] for 0 < m < M, zero elsewhere.  One row of `bhat` per lattice.
+__global__ void bluestein_b_kernel(LatTable lt, const double2* __restrict__ chirp,
+                                   double2* __restrict__ bhat, int64_t P) {
+  const int l = blockIdx.y;
+  const int64_t m = lt.m[l];
+  const double2* ch = chirp + lt.off[l];
+  double2* b = bhat + (int64_t)l * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (i < m) v = cconj(ch[i]);
+    else if (P - i < m) v = cconj(ch[P - i]);
+    b[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// column pass (P1 > 1).  CTA = C = 4096/P1 consecutive columns of one unit.
+// FWD: mask n >= M to zero if MASK, forward FFT, twiddle, store transposed.
+// INV: inverse FFT, post-chirp, store n < M.
+template <bool INV>
+__global__ void __launch_bounds__(FFT_T)
+fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int mask_input,
+               const double2* __restrict__ ftab, const double2* __restrict__ chirp) {
+  extern __shared__ double2 s[];
+  const FftGeom g = fft_geom(p);
+  const int P1 = g.P1, P2 = g.P2;
+  const int C = FFT_E / P1;
+  const int rstride = fft_rstride(P1);
+  const int u = blockIdx.y;
+  const int c0 = blockIdx.x * C;
+  const int lat = ut.lat[u];
+  const int64_t m = ut.m[lat];
+  double2* ub = buf + (int64_t)u * ustride;
+
+  // load (coalesced along columns), transpose into rows of length P1
+  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    const int c = f % C, n1 = f / C;
+    const int64_t n = (int64_t)n1 * P2 + c0 + c;
+    double2 v;
+    if (!INV && mask_input && n >= m) v = make_double2(0.0, 0.0);
+    else v = ub[n];
+    s[c * rstride + fpad(n1)] = v;
+  }
+  __syncthreads();
+  block_fft<INV>(s, C, rstride, g.p1, ftab + g.off_p1);
+  if (!INV) {
+    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+      const int c = f % C, k1 = f / C;
+      const int64_t n2 = c0 + c;
+      double2 v = s[c * rstride + fpad(k1)];
+      v = cmul(v, twP(g, ftab, n2 * (int64_t)k1));
+      ub[(int64_t)k1 * P2 + n2] = v;
+    }
+  } else {
+    const double2* ch = chirp + ut.off[lat];
+    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+      const int c = f % C, n1 = f / C;
+      const int64_t n = (int64_t)n1 * P2 + c0 + c;
+      if (n < m) ub[n] = cmul(s[c * rstride + fpad(n1)], __ldg(&ch[n]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row pass.  CTA = 4096/P2 rows (rows index (unit, k1) flattened).
+// MODE 0 (conv): forward FFT, * bhat, inverse FFT, then twiddle (P1 > 1) or
+//                post-chirp (P1 == 1, whole transform in one row).
+// MODE 1 (fwd only, builds bhat): forward FFT, scale by 1/P.
+template <int MODE>
+__global__ void __launch_bounds__(FFT_T)
+fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int total_rows,
+               const double2* __restrict__ ftab, const double2* __restrict__ bhat,
+               const double2* __restrict__ chirp) {
+  extern __shared__ double2 s[];
+  const FftGeom g = fft_geom(p);
+  const int P1 = g.P1, P2 = g.P2;
+  const int rows = FFT_E / P2;
+  const int rstride = fft_rstride(P2);
+  const int g0 = blockIdx.x * rows;
+  const bool single = (P1 == 1);
+
+  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    const int r = f / P2, i = f - r * P2;
+    const int grow = g0 + r;
+    double2 v = make_double2(0.0, 0.0);
+    if (grow < total_rows) {
+      const int u = grow / P1, k1 = grow - u * P1;
+      const int lat = ut.lat[u];
+      if (!(MODE == 0 && single && i >= ut.m[lat]))
+        v = buf[(int64_t)u * ustride + (int64_t)k1 * P2 + i];
+    }
+    s[r * rstride + fpad(i)] = v;
+  }
+  __syncthreads();
+  block_fft<false>(s, rows, rstride, g.p2, ftab + g.off_p2);
+  if (MODE == 1) {
+    const double scale = 1.0 / (double)g.P;  // exact: P is a power of two
+    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+      const int r = f / P2, i = f - r * P2;
+      const int grow = g0 + r;
+      if (grow < total_rows) {
+        const int u = grow / P1, k1 = grow - u * P1;
+        double2 v = s[r * rstride + fpad(i)];
+        buf[(int64_t)u * ustride + (int64_t)k1 * P2 + i] = make_double2(v.x * scale, v.y * scale);
+      }
+    }
+    return;
+  }
+  // pointwise product with Bhat (same layout)
+  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    const int r = f / P2, i = f - r * P2;
+    const int grow = g0 + r;
+    if (grow < total_rows) {
+      const int u = grow / P1, k1 = grow - u * P1;
+      const int lat = ut.lat[u];
+      const double2 b = __ldg(&bhat[(int64_t)lat * ustride + (int64_t)k1 * P2 + i]);
+      const int si = r * rstride + fpad(i);
+      s[si] = cmul(s[si], b);
+    }
+  }
+  __syncthreads();
+  block_fft<true>(s, rows, rstride, g.p2, ftab + g.off_p2);
+  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    const int r = f / P2, i = f - r * P2;
+    const int grow = g0 + r;
+    if (grow < total_rows) {
+      const int u = grow / P1, k1 = grow - u * P1;
+      const int lat = ut.lat[u];
+      double2 v = s[r * rstride + fpad(i)];
+      double2* ub = buf + (int64_t)u * ustride;
+      if (!single) {
+        v = cmulc(v, twP(g, ftab, (int64_t)i * k1));  // e^{+2 pi i n2 k1 / P}
+        ub[(int64_t)k1 * P2 + i] = v;
+      } else if (i < ut.m[lat]) {
+        ub[i] = cmul(v, __ldg(&chirp[ut.off[lat] + i]));
+      }
+    }
+  }
+}
+
+static size_t fft_smem_bytes(int rows_len) {
+  const int rows = FFT_E / rows_len;
+  return (size_t)rows * fft_rstride(rows_len) * sizeof(double2);
+}
+
+int launch_fft_tables(int p, double2* out, cudaStream_t st) {
+  const FftGeom g = fft_geom(p);
+  int blocks = (int)((g.table_len + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  fft_tables_kernel<<<blocks, 256, 0, st>>>(p, out);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_lattice_tables(const LatTable& lt, double2* tw, double2* chirp, cudaStream_t st) {
+  int64_t mmax = 1;
+  for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
+  int bx = (int)((mmax + 255) / 256);
+  if (bx > 512) bx = 512;
+  lattice_tables_kernel<<<dim3(bx, lt.nlat), 256, 0, st>>>(lt, tw, chirp);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+static int set_smem(const void* fn, size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return (int)e;
+}
+
+// forward passes on `nunits` buffers (column pass if P1 > 1, then row pass in `mode`)
+static int run_forward_cols(double2* buf, int64_t ustride, const UnitTable& ut, int p, int mask,
+                            const double2* ftab, const double2* chirp, cudaStream_t st) {
+  const FftGeom g = fft_geom(p);
+  if (g.P1 == 1) return 0;
+  const size_t sm = fft_smem_bytes(g.P1);
+  int rc = set_smem((const void*)fft_col_kernel<false>, sm);
+  if (rc) return rc;
+  dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
+  fft_col_kernel<false><<<grid, FFT_T, sm, st>>>(buf, ustride, ut, p, mask, ftab, chirp);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
+                const double2* ftab, cudaStream_t st) {
+  const FftGeom g = fft_geom(p);
+  const int64_t P = g.P;
+  int bx = (int)((P + 255) / 256);
+  if (bx > 512) bx = 512;
+  bluestein_b_kernel<<<dim3(bx, lt.nlat), 256, 0, st>>>(lt, chirp, bhat, P);
+  SFFT_CHECK_LAUNCH();
+  UnitTable ut;
+  ut.nunits = lt.nlat;
+  ut.nlat = lt.nlat;
+  for (int l = 0; l < lt.nlat; ++l) { ut.lat[l] = l; ut.m[l] = lt.m[l]; ut.off[l] = lt.off[l]; }
+  int rc = run_forward_cols(bhat, P, ut, p, 0, ftab, chirp, st);
+  if (rc) return rc;
+  const size_t sm = fft_smem_bytes(g.P2);
+  rc = set_smem((const void*)fft_row_kernel<1>, sm);
+  if (rc) return rc;
+  const int total_rows = ut.nunits * g.P1;
+  const int rows = FFT_E / g.P2;
+  fft_row_kernel<1><<<(total_rows + rows - 1) / rows, FFT_T, sm, st>>>(bhat, P, ut, p, total_rows,
+                                                                       ftab, nullptr, chirp);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ftab,
+                     const double2* bhat, const double2* chirp, cudaStream_t st) {
+  const FftGeom g = fft_geom(p);
+  const int64_t P = g.P;
+  int rc = run_forward_cols(buf, P, ut, p, 1, ftab, chirp, st);
+  if (rc) return rc;
+  const size_t sm = fft_smem_bytes(g.P2);
+  rc = set_smem((const void*)fft_row_kernel<0>, sm);
+  if (rc) return rc;
+  const int total_rows = ut.nunits * g.P1;
+  const int rows = FFT_E / g.P2;
+  fft_row_kernel<0><<<(total_rows + rows - 1) / rows, FFT_T, sm, st>>>(buf, P, ut, p, total_rows,
+                                                                       ftab, bhat, chirp);
+  SFFT_CHECK_LAUNCH();
+  if (g.P1 > 1) {
+    const size_t smc = fft_smem_bytes(g.P1);
+    rc = set_smem((const void*)fft_col_kernel<true>, smc);
+    if (rc) return rc;
+    dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
+    fft_col_kernel<true><<<grid, FFT_T, smc, st>>>(buf, P, ut, p, 0, ftab, chirp);
+    SFFT_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+}  // namespace sfft

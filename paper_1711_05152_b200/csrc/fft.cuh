@@ -1,0 +1,151 @@
+// In-shared-memory Stockham FFT building blocks shared by the Bluestein
+// passes (fft.cu) and the line-detection kernel.
+//
+// A CTA of FFT_T = 256 threads owns a tile of FFT_E = 4096 complex128
+// elements (64 KB + padding), organised as `rows` independent transforms of
+// length N = 4096 / rows.  Every radix pass keeps 16 values per thread in
+// registers (one radix-16 butterfly, or 16/R butterflies of radix R).
+#pragma once
+#include "common.cuh"
+
+namespace sfft {
+
+constexpr int FFT_T = 256;
+constexpr int FFT_E = 4096;
+
+// padded shared-memory index of element i inside a row (one gap per 16)
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int fft_rstride(int n) { return n + (n >> 4) + 1; }
+
+// constant twiddles of the 16th roots of unity: e^{-2 pi i m / 16}, m < 8
+__device__ __forceinline__ double2 tw16(int m, bool inv) {
+  const double c1 = 0.92387953251128673848, s1 = 0.38268343236508977173;
+  const double h = 0.70710678118654752440;
+  double cr, ci;
+  switch (m) {
+    case 0: cr = 1.0; ci = 0.0; break;
+    case 1: cr = c1; ci = -s1; break;
+    case 2: cr = h; ci = -h; break;
+    case 3: cr = s1; ci = -c1; break;
+    case 4: cr = 0.0; ci = -1.0; break;
+    case 5: cr = -s1; ci = -c1; break;
+    case 6: cr = -h; ci = -h; break;
+    default: cr = -c1; ci = -s1; break;
+  }
+  return make_double2(cr, inv ? -ci : ci);
+}
+
+template <bool INV>
+__device__ __forceinline__ double2 twmul_const(double2 x, int m) {
+  if (m == 0) return x;
+  if (m == 4) return INV ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+  return cmul(x, tw16(m, INV));
+}
+
+__host__ __device__ constexpr int bitrev_small(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+template <int R>
+struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
+template <>
+struct Log2<1> { static constexpr int v = 0; };
+
+// Radix-R DFT in registers, natural order in and out.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(double2* v) {
+#pragma unroll
+  for (int span = R / 2; span >= 1; span >>= 1) {
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * span) {
+#pragma unroll
+      for (int q = 0; q < span; ++q) {
+        double2 a = v[b + q], c = v[b + q + span];
+        v[b + q] = cadd(a, c);
+        v[b + q + span] = twmul_const<INV>(csub(a, c), q * (16 / (2 * span)));
+      }
+    }
+  }
+  double2 t[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) t[bitrev_small(i, Log2<R>::v)] = v[i];
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+// One Stockham radix-R pass over `rows` rows of length N (all in smem).
+// twN[m] = e^{-2 pi i m / N}, m < N (global, read-only).
+template <int R, bool INV>
+__device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride, int N, int Ns,
+                                              const double2* __restrict__ twN) {
+  constexpr int BPT = 16 / R;
+  const int per_row = N / R;
+  const int nb = rows * per_row;
+  const int tstep = N / (Ns * R);
+  double2 v[BPT][R];
+  int obase[BPT];
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    const int b = threadIdx.x + q * FFT_T;
+    obase[q] = -1;
+    if (b < nb) {
+      const int row = b / per_row;
+      const int j = b - row * per_row;
+      const int k = j & (Ns - 1);
+      const int base = row * rstride;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q][r] = s[base + fpad(j + r * per_row)];
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const double2 w = __ldg(&twN[r * k * tstep]);
+          v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+        }
+      }
+      dft_reg<R, INV>(v[q]);
+      obase[q] = row * rstride + ((j - k) * R + k);  // row offset + unpadded index
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    if (obase[q] >= 0) {
+      const int b = threadIdx.x + q * FFT_T;
+      const int row = b / per_row;
+      const int idx0 = obase[q] - row * rstride;
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[row * rstride + fpad(idx0 + r * Ns)] = v[q][r];
+    }
+  }
+  __syncthreads();
+}
+
+// Full Stockham FFT of `rows` rows of length N = 2^logN (natural order in/out).
+// Radix-16 passes first, one smaller pass last.
+template <bool INV>
+__device__ __forceinline__ void block_fft(double2* s, int rows, int rstride, int logN,
+                                          const double2* __restrict__ twN) {
+  const int N = 1 << logN;
+  int Ns = 1;
+  int done = 0;
+  while (done < logN) {
+    const int rem = logN - done;
+    if (rem >= 4) {
+      stockham_pass<16, INV>(s, rows, rstride, N, Ns, twN);
+      Ns <<= 4; done += 4;
+    } else if (rem == 3) {
+      stockham_pass<8, INV>(s, rows, rstride, N, Ns, twN);
+      Ns <<= 3; done += 3;
+    } else if (rem == 2) {
+      stockham_pass<4, INV>(s, rows, rstride, N, Ns, twN);
+      Ns <<= 2; done += 2;
+    } else {
+      stockham_pass<2, INV>(s, rows, rstride, N, Ns, twN);
+      Ns <<= 1; done += 1;
+    }
+  }
+}
+
+}  // namespace sfft

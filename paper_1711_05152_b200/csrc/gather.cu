@@ -1,0 +1,489 @@
+// K4: alias-free bin gather + lattice averaging + delta threshold, cap
+// selection, stable compaction and the candidate product (K5).
+//
+// Reference: transform.py:99-127 (invert_multiple: spectrum_hat = fft / M,
+// sums[mask] += spectrum_hat[res] in lattice order, coeffs = sums / counts),
+// detect.py:197-212 (_select: |c| >= delta, cap by (|c| desc, freq lex asc)),
+// detect.py:257-260 + 367-371 (candidate product), detect.py:412 and
+// lattice.py:97-109 (union + lexsort/unique of the kept sets).
+//
+// numpy evaluates complex / int as a multiplication by the reciprocal
+// (Smith's algorithm with a zero imaginary part), so the kernels do the same:
+// spec * (1.0 / M) and sums * (1.0 / count).
+//
+// Candidate sets stay lexicographically sorted on the device without any
+// sort: the product of a sorted prefix set with a sorted component set in
+// row-major order is sorted, and every later set is an order-preserving
+// subset of it (compaction by flags), so the reference's lexsort + unique
+// reduces to a stable prefix-sum compaction.
+#include "common.cuh"
+#include "plan.cuh"
+#include "gather.cuh"
+
+namespace sfft {
+
+template <int DM, bool FAST, int RB>
+__global__ void __launch_bounds__(256)
+gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+              const uint64_t* __restrict__ masks, const double2* __restrict__ buf, int64_t ustride,
+              int rb, int it0, double delta, double2* __restrict__ coef, uint8_t* __restrict__ keep,
+              int32_t* __restrict__ counts) {
+  __shared__ int red[RB][8];
+  const int d = lt.d;
+  const int L = lt.nlat;
+  const uint64_t lmask = (L >= 64) ? ~0ull : ((1ull << L) - 1ull);
+  int kept[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) kept[i] = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t mask = masks[k] & lmask;
+    double2 sums[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) sums[i] = make_double2(0.0, 0.0);
+    int cnt = 0;
+    if (mask) {
+      int32_t kv[DM];
+#pragma unroll
+      for (int c = 0; c < DM; ++c) kv[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + k]) : 0;
+      uint64_t mm = mask;
+      while (mm) {
+        const int l = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        const int64_t r = residue<DM, FAST>(kv, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+        const double invm = 1.0 / (double)lt.m[l];
+        ++cnt;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          if (i < rb) {
+            const double2 v = __ldg(&buf[(int64_t)(i * L + l) * ustride + r]);
+            sums[i].x += v.x * invm;
+            sums[i].y += v.y * invm;
+          }
+        }
+      }
+    }
+    const double invc = cnt ? 1.0 / (double)cnt : 0.0;
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      if (i < rb) {
+        double2 c = make_double2(sums[i].x * invc, sums[i].y * invc);
+        uint8_t kf = 0;
+        if (cnt) {
+          const double mag = hypot(c.x, c.y);
+          kf = (mag >= delta) ? 1 : 0;
+        } else {
+          c = make_double2(0.0, 0.0);
+        }
+        coef[(int64_t)(it0 + i) * n + k] = c;
+        keep[(int64_t)(it0 + i) * n + k] = kf;
+        kept[i] += kf;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    int v = kept[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[i][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < RB && threadIdx.x < rb) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+    if (t) atomicAdd(&counts[it0 + threadIdx.x], t);
+  }
+}
+
+template <int DM, bool FAST>
+static int launch_gather_t(const int32_t* freqs, int64_t n, const LatTable& lt,
+                           const uint64_t* masks, const double2* buf, int64_t ustride, int rb,
+                           int it0, double delta, double2* coef, uint8_t* keep, int32_t* counts,
+                           int blocks, cudaStream_t st) {
+  if (rb <= 1)
+    gather_kernel<DM, FAST, 1><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf, ustride, rb, it0,
+                                                       delta, coef, keep, counts);
+  else if (rb <= 4)
+    gather_kernel<DM, FAST, 4><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf, ustride, rb, it0,
+                                                       delta, coef, keep, counts);
+  else if (rb <= 8)
+    gather_kernel<DM, FAST, 8><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf, ustride, rb, it0,
+                                                       delta, coef, keep, counts);
+  else
+    return -22;
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_gather(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
+                  const double2* buf, int64_t ustride, int rb, int it0, double delta, double2* coef,
+                  uint8_t* keep, int32_t* counts, bool fast, int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  const int blocks = (int)(want < cap ? want : cap);
+  const int d = lt.d;
+#define SFFT_G_CASE(DMV)                                                                         \
+  if (d <= DMV)                                                                                  \
+    return fast ? launch_gather_t<DMV, true>(freqs, n, lt, masks, buf, ustride, rb, it0, delta, \
+                                             coef, keep, counts, blocks, st)                    \
+                : launch_gather_t<DMV, false>(freqs, n, lt, masks, buf, ustride, rb, it0, delta, \
+                                              coef, keep, counts, blocks, st);
+  SFFT_G_CASE(4)
+  SFFT_G_CASE(8)
+  SFFT_G_CASE(16)
+  SFFT_G_CASE(32)
+  SFFT_G_CASE(64)
+#undef SFFT_G_CASE
+  return -22;
+}
+
+// ---------------------------------------------------------------------------
+// flag -> ascending index list (stable compaction).  Flags of `nrows` rows of
+// length n are OR-ed (union of the kept sets of several iterations).
+
+constexpr int SCAN_T = 256;
+constexpr int SCAN_PER = 8;
+constexpr int SCAN_TILE = SCAN_T * SCAN_PER;
+
+__device__ __forceinline__ int flag_at(const uint8_t* __restrict__ flags, int64_t n, int nrows, int64_t i) {
+  int f = 0;
+  for (int r = 0; r < nrows; ++r) f |= flags[(int64_t)r * n + i];
+  return f != 0;
+}
+
+__global__ void scan_count_kernel(const uint8_t* __restrict__ flags, int64_t n, int nrows,
+                                  int32_t* __restrict__ bcount) {
+  __shared__ int red[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int c = 0;
+  for (int q = 0; q < SCAN_PER; ++q) {
+    const int64_t i = base + q * SCAN_T + threadIdx.x;
+    if (i < n) c += flag_at(flags, n, nrows, i);
+  }
+  const int tot = block_sum(c, red);
+  if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+}
+
+// single-block exclusive scan of nb block counts; total -> *total
+__global__ void scan_blocks_kernel(int32_t* __restrict__ bcount, int64_t nb, int32_t* __restrict__ total) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    int v = (i < nb) ? bcount[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const int wbase = wid ? warp_tot[wid - 1] : 0;
+    const int excl = carry + wbase + x - v;
+    if (i < nb) bcount[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void scan_write_kernel(const uint8_t* __restrict__ flags, int64_t n, int nrows,
+                                  const int32_t* __restrict__ boff, int32_t* __restrict__ idx_out) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = boff[blockIdx.x];
+  __syncthreads();
+  for (int q = 0; q < SCAN_PER; ++q) {
+    const int64_t i = base + q * SCAN_T + threadIdx.x;
+    const int v = (i < n) ? flag_at(flags, n, nrows, i) : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = (lane < (SCAN_T >> 5)) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int wbase = wid ? warp_tot[wid - 1] : 0;
+    const int pos = carry + wbase + x - v;
+    if (v) idx_out[pos] = (int32_t)i;
+    __syncthreads();
+    if (threadIdx.x == SCAN_T - 1) carry = pos + v;
+    __syncthreads();
+  }
+}
+
+int64_t scan_scratch_len(int64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1; }
+
+int launch_flag_indices(const uint8_t* flags, int64_t n, int nrows, int32_t* idx_out,
+                        int32_t* total, int32_t* scratch, cudaStream_t st) {
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(total, 0, sizeof(int32_t), st);
+    return (int)e;
+  }
+  const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  scan_count_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(flags, n, nrows, scratch);
+  SFFT_CHECK_LAUNCH();
+  scan_blocks_kernel<<<1, 1024, 0, st>>>(scratch, nb, total);
+  SFFT_CHECK_LAUNCH();
+  scan_write_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(flags, n, nrows, scratch, idx_out);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+// rows: out[c * out_stride + j] = in[c * n_in + idx[j]] for j < *count (bounded by cap_rows)
+__global__ void gather_rows_kernel(const int32_t* __restrict__ in, int64_t n_in, int ncomp,
+                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
+                                   int64_t cap_rows, int32_t* __restrict__ out, int64_t out_stride,
+                                   const double2* __restrict__ cin, double2* __restrict__ cout) {
+  const int64_t cnt = *count < cap_rows ? *count : cap_rows;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = idx[j];
+    for (int c = 0; c < ncomp; ++c) out[(int64_t)c * out_stride + j] = in[(int64_t)c * n_in + src];
+    if (cout) cout[j] = cin[src];
+  }
+}
+
+int launch_gather_rows(const int32_t* in, int64_t n_in, int ncomp, const int32_t* idx,
+                       const int32_t* count, int64_t cap_rows, int32_t* out, int64_t out_stride,
+                       const double2* cin, double2* cout, int num_sms, cudaStream_t st) {
+  if (cap_rows <= 0) return 0;
+  int64_t want = (cap_rows + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  gather_rows_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(
+      in, n_in, ncomp, idx, count, cap_rows, out, out_stride, cin, cout);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// cap selection (detect.py:205-211): keep the `cap` largest |c| among the
+// flagged entries, ties broken by ascending index (= ascending lexicographic
+// frequency, since candidate sets are sorted).  Exact radix select on the
+// IEEE bit pattern of |c| (monotone for non-negative doubles), 8 digits of 8
+// bits, followed by an index-ordered rank among the entries equal to the
+// threshold key.
+struct SelState {
+  unsigned long long prefix;
+  unsigned long long pmask;
+  int need;
+  int pad;
+};
+
+__device__ __forceinline__ unsigned long long mag_key(double2 c) {
+  return (unsigned long long)__double_as_longlong(hypot(c.x, c.y));
+}
+
+__global__ void sel_init_kernel(SelState* stt, int cap, int32_t* hist) {
+  if (threadIdx.x == 0) { stt->prefix = 0; stt->pmask = 0; stt->need = cap; }
+  hist[threadIdx.x] = 0;
+}
+
+__global__ void sel_hist_kernel(const double2* __restrict__ coef, const uint8_t* __restrict__ keep,
+                                int64_t n, const SelState* __restrict__ stt, int shift,
+                                int32_t* __restrict__ hist) {
+  __shared__ int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned long long pre = stt->prefix, pm = stt->pmask;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    const unsigned long long key = mag_key(coef[i]);
+    if ((key & pm) != pre) continue;
+    atomicAdd(&h[(key >> shift) & 255ull], 1);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// pick the digit holding the need-th largest key; clears hist for the next pass
+__global__ void sel_pick_kernel(SelState* stt, int shift, int32_t* hist) {
+  __shared__ int hs[256];
+  hs[threadIdx.x] = hist[threadIdx.x];
+  __syncthreads();
+  hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    int need = stt->need;
+    int above = 0;
+    int dsel = 0;
+    for (int dg = 255; dg >= 0; --dg) {
+      if (above + hs[dg] >= need) { dsel = dg; break; }
+      above += hs[dg];
+    }
+    stt->prefix |= ((unsigned long long)dsel) << shift;
+    stt->pmask |= 255ull << shift;
+    stt->need = need - above;
+  }
+}
+
+// keep <- key > T ; tie flags for key == T
+__global__ void sel_apply_kernel(const double2* __restrict__ coef, uint8_t* __restrict__ keep,
+                                 int64_t n, const SelState* __restrict__ stt, uint8_t* __restrict__ tie) {
+  const unsigned long long T = stt->prefix;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t t = 0;
+    if (keep[i]) {
+      const unsigned long long key = mag_key(coef[i]);
+      if (key == T) t = 1;
+      keep[i] = (key > T) ? 1 : 0;
+    }
+    tie[i] = t;
+  }
+}
+
+__global__ void sel_ties_kernel(uint8_t* __restrict__ keep, const int32_t* __restrict__ tie_idx,
+                                const int32_t* __restrict__ ntie, const SelState* __restrict__ stt) {
+  const int need = stt->need;
+  const int nt = *ntie;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < need && j < nt; j += gridDim.x * blockDim.x)
+    keep[tie_idx[j]] = 1;
+}
+
+int64_t select_scratch_bytes(int64_t n) {
+  // state (64 B) + hist (1 KB) + tie flags (n) + tie idx (4n) + scan scratch + total
+  return 64 + 1024 + ((n + 15) / 16) * 16 + 4 * n + 4 * scan_scratch_len(n) + 16;
+}
+
+int launch_select_cap(const double2* coef, uint8_t* keep, int64_t n, int cap, uint8_t* scratch,
+                      int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  SelState* stt = (SelState*)scratch;
+  int32_t* hist = (int32_t*)(scratch + 64);
+  uint8_t* tie = scratch + 64 + 1024;
+  int32_t* tie_idx = (int32_t*)(scratch + 64 + 1024 + ((n + 15) / 16) * 16);
+  int32_t* sscr = tie_idx + n;
+  int32_t* total = sscr + scan_scratch_len(n);
+  int64_t want = (n + 255) / 256;
+  int64_t capb = (int64_t)num_sms * 4;
+  const unsigned blocks = (unsigned)(want < capb ? want : capb);
+  sel_init_kernel<<<1, 256, 0, st>>>(stt, cap, hist);
+  SFFT_CHECK_LAUNCH();
+  for (int dgt = 7; dgt >= 0; --dgt) {
+    const int shift = dgt * 8;
+    sel_hist_kernel<<<blocks, 256, 0, st>>>(coef, keep, n, stt, shift, hist);
+    sel_pick_kernel<<<1, 256, 0, st>>>(stt, shift, hist);
+  }
+  SFFT_CHECK_LAUNCH();
+  sel_apply_kernel<<<blocks, 256, 0, st>>>(coef, keep, n, stt, tie);
+  SFFT_CHECK_LAUNCH();
+  int rc = launch_flag_indices(tie, n, 1, tie_idx, total, sscr, st);
+  if (rc) return rc;
+  sel_ties_kernel<<<blocks, 256, 0, st>>>(keep, tie_idx, total, stt);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// candidate product (detect.py:257-260): row q = a * nc + b  ->  (prefix_a, comp_b)
+__global__ void product_kernel(const int32_t* __restrict__ pref, int64_t np, int t,
+                               const int32_t* __restrict__ comp, int64_t nc, int32_t* __restrict__ out) {
+  const int64_t total = np * nc;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = q / nc, b = q - a * nc;
+    for (int c = 0; c < t; ++c) out[(int64_t)c * total + q] = pref[(int64_t)c * np + a];
+    out[(int64_t)t * total + q] = comp[b];
+  }
+}
+
+int launch_product(const int32_t* pref, int64_t np, int t, const int32_t* comp, int64_t nc,
+                   int32_t* out, int num_sms, cudaStream_t st) {
+  const int64_t total = np * nc;
+  if (total == 0) return 0;
+  int64_t want = (total + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 16;
+  product_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(pref, np, t, comp, nc, out);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+// residues k.z_l mod M_l of every candidate on every lattice: out[l * n + i]
+template <int DM, bool FAST>
+__global__ void residues_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+                                int64_t* __restrict__ out) {
+  const int d = lt.d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    for (int l = 0; l < lt.nlat; ++l)
+      out[(int64_t)l * n + i] = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+  }
+}
+
+int launch_residues(const int32_t* freqs, int64_t n, const LatTable& lt, int64_t* out, bool fast,
+                    int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  const unsigned blocks = (unsigned)(want < cap ? want : cap);
+  const int d = lt.d;
+#define SFFT_R_CASE(DMV)                                                                     \
+  if (d <= DMV) {                                                                            \
+    if (fast) residues_kernel<DMV, true><<<blocks, 256, 0, st>>>(freqs, n, lt, out);         \
+    else residues_kernel<DMV, false><<<blocks, 256, 0, st>>>(freqs, n, lt, out);             \
+    SFFT_CHECK_LAUNCH();                                                                     \
+    return 0;                                                                                \
+  }
+  SFFT_R_CASE(4)
+  SFFT_R_CASE(8)
+  SFFT_R_CASE(16)
+  SFFT_R_CASE(32)
+  SFFT_R_CASE(64)
+#undef SFFT_R_CASE
+  return -22;
+}
+
+__global__ void cscale_kernel(double2* __restrict__ x, int64_t n, double scale, int conj) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = x[i];
+    if (conj) v.y = -v.y;
+    x[i] = make_double2(v.x * scale, v.y * scale);
+  }
+}
+
+int launch_cscale(double2* x, int64_t n, double scale, int conj, int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  cscale_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(x, n, scale, conj);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace sfft

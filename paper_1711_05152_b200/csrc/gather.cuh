@@ -1,0 +1,28 @@
+#pragma once
+#include "plan.cuh"
+
+namespace sfft {
+
+int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+                 int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
+                 cudaStream_t st);
+int64_t alias_scratch_words(const LatTable& lt);
+int launch_gather(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
+                  const double2* buf, int64_t ustride, int rb, int it0, double delta, double2* coef,
+                  uint8_t* keep, int32_t* counts, bool fast, int num_sms, cudaStream_t st);
+int64_t scan_scratch_len(int64_t n);
+int launch_flag_indices(const uint8_t* flags, int64_t n, int nrows, int32_t* idx_out,
+                        int32_t* total, int32_t* scratch, cudaStream_t st);
+int launch_gather_rows(const int32_t* in, int64_t n_in, int ncomp, const int32_t* idx,
+                       const int32_t* count, int64_t cap_rows, int32_t* out, int64_t out_stride,
+                       const double2* cin, double2* cout, int num_sms, cudaStream_t st);
+int64_t select_scratch_bytes(int64_t n);
+int launch_select_cap(const double2* coef, uint8_t* keep, int64_t n, int cap, uint8_t* scratch,
+                      int num_sms, cudaStream_t st);
+int launch_product(const int32_t* pref, int64_t np, int t, const int32_t* comp, int64_t nc,
+                   int32_t* out, int num_sms, cudaStream_t st);
+int launch_residues(const int32_t* freqs, int64_t n, const LatTable& lt, int64_t* out, bool fast,
+                    int num_sms, cudaStream_t st);
+int launch_cscale(double2* x, int64_t n, double scale, int conj, int num_sms, cudaStream_t st);
+
+}  // namespace sfft

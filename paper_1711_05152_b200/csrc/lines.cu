@@ -1,0 +1,149 @@
+// One-dimensional line detection of component t (reference detect.py:175-240:
+// projected_line_coefficients + _select + union inside detect_component).
+//
+// Each of the r lines samples K_t points x = anchor with x_t = l / K_t.  For a
+// sparse polynomial the sample is evaluated with an exact integer phase
+//     p(x_l) = sum_h c''_h w_K^{(h_t l) mod K},  c''_h = c_h e^{2 pi i sum_{u != t} h_u a_u},
+// then bins = DFT_K(samples) * (1/K), bin l <-> the k in [lo, hi] with
+// k = l (mod K), and the line keeps the up-to-cap largest |coefficients| >=
+// delta (ties: |c| desc, k asc).  Lines are tiny (K <= 1024), one CTA each.
+#include "common.cuh"
+#include "plan.cuh"
+#include "lines.cuh"
+
+namespace sfft {
+
+constexpr int LT = 256;
+constexpr int LCH = 512;  // terms per shared-memory chunk
+
+__global__ void __launch_bounds__(LT)
+line_sample_poly_kernel(const int32_t* __restrict__ hf, const double2* __restrict__ coef, int s,
+                        int d, int t, int K, LineAnchors la, double2* __restrict__ values) {
+  __shared__ double2 cs[LCH];
+  __shared__ int es[LCH];
+  __shared__ double2 wk[1024];
+  __shared__ double2 part[8][32];
+  const int line = blockIdx.x;
+  const double* a = la.a + line * d;
+  for (int q = threadIdx.x; q < K; q += LT) {
+    double sn, c;
+    sincospi(2.0 * (double)q / (double)K, &sn, &c);
+    wk[q] = make_double2(c, sn);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int l0 = 0; l0 < K; l0 += 32) {
+    const int l = l0 + lane;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int h0 = 0; h0 < s; h0 += LCH) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < LCH; q += LT) {
+        const int h = h0 + q;
+        double2 cc = make_double2(0.0, 0.0);
+        int e = 0;
+        if (h < s) {
+          double ph = 0.0;
+          for (int u = 0; u < d; ++u)
+            if (u != t) ph += (double)hf[(int64_t)u * s + h] * a[u];
+          double sn, c;
+          sincospi(2.0 * ph, &sn, &c);
+          cc = cmul(coef[h], make_double2(c, sn));
+          e = (int)mod_slow((int64_t)hf[(int64_t)t * s + h], K);
+        }
+        cs[q] = cc;
+        es[q] = e;
+      }
+      __syncthreads();
+      if (l < K) {
+        for (int q = w; q < LCH && h0 + q < s; q += 8) {
+          const int idx = (int)(((int64_t)es[q] * l) % K);
+          const double2 tw = wk[idx];
+          const double2 cc = cs[q];
+          acc.x = fma(cc.x, tw.x, acc.x);
+          acc.x = fma(-cc.y, tw.y, acc.x);
+          acc.y = fma(cc.x, tw.y, acc.y);
+          acc.y = fma(cc.y, tw.x, acc.y);
+        }
+      }
+    }
+    part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && l < K) {
+      double2 t2 = part[0][lane];
+      for (int q = 1; q < 8; ++q) t2 = cadd(t2, part[q][lane]);
+      values[(int64_t)line * K + l] = t2;
+    }
+    __syncthreads();
+  }
+}
+
+// DFT of each line, bin mapping, threshold and cap ranking
+__global__ void __launch_bounds__(LT)
+line_select_kernel(const double2* __restrict__ values, int K, int64_t lo, int cap, double delta,
+                   double2* __restrict__ coefs, uint8_t* __restrict__ keep) {
+  __shared__ double2 v[1024];
+  __shared__ double2 wk[1024];
+  __shared__ double mg[1024];
+  __shared__ uint8_t pre[1024];
+  __shared__ int red[32];
+  const int line = blockIdx.x;
+  for (int q = threadIdx.x; q < K; q += LT) {
+    double sn, c;
+    sincospi(2.0 * (double)q / (double)K, &sn, &c);
+    wk[q] = make_double2(c, -sn);  // forward: e^{-2 pi i q / K}
+    v[q] = values[(int64_t)line * K + q];
+  }
+  __syncthreads();
+  const double invk = 1.0 / (double)K;
+  // coefficient of k = lo + q is bin (k mod K)
+  int cnt = 0;
+  for (int q = threadIdx.x; q < K; q += LT) {
+    const int64_t k = lo + q;
+    const int bin = (int)mod_slow(k, K);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int l = 0; l < K; ++l) {
+      const int idx = (int)(((int64_t)bin * l) % K);
+      acc = cadd(acc, cmul(v[l], wk[idx]));
+    }
+    const double2 c = make_double2(acc.x * invk, acc.y * invk);
+    coefs[(int64_t)line * K + q] = c;
+    const double m = hypot(c.x, c.y);
+    mg[q] = m;
+    pre[q] = (m >= delta) ? 1 : 0;
+    cnt += pre[q];
+  }
+  __syncthreads();
+  const int total = block_sum(cnt, red);
+  __shared__ int tot_s;
+  if (threadIdx.x == 0) tot_s = total;
+  __syncthreads();
+  const int tot = tot_s;
+  for (int q = threadIdx.x; q < K; q += LT) {
+    uint8_t kf = pre[q];
+    if (kf && tot > cap) {
+      int rank = 0;
+      const double m = mg[q];
+      for (int q2 = 0; q2 < K; ++q2)
+        if (pre[q2] && (mg[q2] > m || (mg[q2] == m && q2 < q))) ++rank;
+      kf = rank < cap ? 1 : 0;
+    }
+    keep[(int64_t)line * K + q] = kf;
+  }
+}
+
+int launch_line_sample_poly(const int32_t* hf, const double2* coef, int s, int d, int t, int K,
+                            const LineAnchors& la, int r, double2* values, cudaStream_t st) {
+  if (K > 1024 || r <= 0) return -22;
+  line_sample_poly_kernel<<<r, LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_line_select(const double2* values, int r, int K, int64_t lo, int cap, double delta,
+                       double2* coefs, uint8_t* keep, cudaStream_t st) {
+  if (K > 1024 || r <= 0) return -22;
+  line_select_kernel<<<r, LT, 0, st>>>(values, K, lo, cap, delta, coefs, keep);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace sfft

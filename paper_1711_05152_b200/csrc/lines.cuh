@@ -1,0 +1,16 @@
+#pragma once
+#include "plan.cuh"
+
+namespace sfft {
+
+// full anchors of the lines in one launch: a[line * d + u]
+struct LineAnchors {
+  double a[2048];
+};
+
+int launch_line_sample_poly(const int32_t* hf, const double2* coef, int s, int d, int t, int K,
+                            const LineAnchors& la, int r, double2* values, cudaStream_t st);
+int launch_line_select(const double2* values, int r, int K, int64_t lo, int cap, double delta,
+                       double2* coefs, uint8_t* keep, cudaStream_t st);
+
+}  // namespace sfft

@@ -1,0 +1,357 @@
+// K1: sampling the signal at the nodes of the step's rank-1 lattices.
+//
+// Reference: detect.py:280-302 (_invert_candidates: nodes = lattice_nodes +
+// anchor tail, one oracle call per lattice), lattice.py:505-508 (nodes
+// x_j = (j z mod M) / M), testbed.py:116-127 (sparse polynomial oracle,
+// p(x) = sum_h c_h e^{2 pi i h.x}), testbed.py:219-244 (B-spline oracle).
+//
+// Sparse polynomial at lattice nodes with exact integer phases:
+//   p(x_j) = sum_h c'_h w^{(r_h j) mod M},   w = e^{2 pi i / M},
+//   r_h = h_head . z mod M,  c'_h = c_h e^{2 pi i h_tail . anchor}.
+// With j = j1 + J1 j2 the sum factors into a complex GEMM
+//   v[j1 + J1 j2] = sum_h A[j1, h] B[h, j2],
+//   A[j1, h] = c'_h w^{(r_h j1) mod M},  B[h, j2] = w^{((r_h J1 mod M) j2) mod M},
+// whose operand tiles are generated on the fly from one twiddle table per
+// lattice (L2-resident) and contracted with register-tiled DFMA (no tensor
+// cores: FP64 tensor throughput equals DFMA throughput on B200).  The
+// epilogue writes the Bluestein pre-chirped input x_j c_j directly (K1 -> K2
+// fusion), so the length-M sample vector is never stored unchirped.
+#include "common.cuh"
+#include "plan.cuh"
+#include "sample.cuh"
+
+namespace sfft {
+
+// c'[it, h] = c_h * e^{2 pi i sum_{c >= t1} h_c a[it, c - t1]}
+__global__ void poly_rotate_kernel(const int32_t* __restrict__ hf, const double2* __restrict__ coef,
+                                   int s, int d, int t1, AnchorTable at, double2* __restrict__ cprime) {
+  const int it = blockIdx.y;
+  const int tail = d - t1;
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < s; h += gridDim.x * blockDim.x) {
+    double ph = 0.0;
+    for (int c = 0; c < tail; ++c) ph += (double)hf[(int64_t)(t1 + c) * s + h] * at.a[it * tail + c];
+    double2 cf = coef[h];
+    if (tail > 0) {
+      double sn, cs;
+      sincospi(2.0 * ph, &sn, &cs);
+      cf = cmul(cf, make_double2(cs, sn));
+    }
+    cprime[(int64_t)it * s + h] = cf;
+  }
+}
+
+// r_h = h_head . z_l mod M_l and r_h * J1_l mod M_l (exact, 64-bit integer path)
+__global__ void poly_residue_kernel(const int32_t* __restrict__ hf, int s, LatTable lt,
+                                    PolyPlan pp, int32_t* __restrict__ rres, int32_t* __restrict__ rj) {
+  const int l = blockIdx.y;
+  const int64_t m = lt.m[l];
+  const int t1 = lt.d;
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < s; h += gridDim.x * blockDim.x) {
+    int64_t acc = 0;
+    for (int c = 0; c < t1; ++c) {
+      const int64_t km = mod_slow((int64_t)hf[(int64_t)c * s + h], m);
+      acc = (acc + (int64_t)(((uint64_t)km * (uint64_t)lt.z[l * t1 + c]) % (uint64_t)m)) % m;
+    }
+    rres[(int64_t)l * s + h] = (int32_t)acc;
+    rj[(int64_t)l * s + h] = (int32_t)(((uint64_t)acc * (uint64_t)pp.J1[l]) % (uint64_t)m);
+  }
+}
+
+constexpr int PT = 64;  // output tile edge (j1 and j2)
+constexpr int KC = 16;  // terms per shared-memory stage
+
+template <bool FAST>
+__global__ void __launch_bounds__(256, 2)
+sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
+                   const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
+                   const double2* __restrict__ tw, const double2* __restrict__ chirp,
+                   double2* __restrict__ buf, int64_t ustride, int apply_chirp) {
+  __shared__ double2 As[KC][PT];
+  __shared__ double2 Bs[KC][PT];
+  const int bid = blockIdx.x;
+  int lo = 0, hi = pp.nunits - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pp.tile_start[mid] <= bid) lo = mid; else hi = mid - 1;
+  }
+  const int u = lo;
+  const int l = pp.unit_lat[u], it = pp.unit_it[u];
+  const int tau = bid - pp.tile_start[u];
+  const int nt1 = pp.nt1[l];
+  const int tj1 = tau % nt1, tj2 = tau / nt1;
+  const int64_t M = lt.m[l];
+  const double invM = lt.inv_m[l];
+  const int64_t J1 = pp.J1[l];
+  const int64_t j1_0 = (int64_t)tj1 * PT, j2_0 = (int64_t)tj2 * PT;
+  const double2* twl = tw + lt.off[l];
+  const int s = pp.s;
+  const double2* cp = cprime + (int64_t)it * s;
+  const int32_t* rr = rres + (int64_t)l * s;
+  const int32_t* rj = rjs + (int64_t)l * s;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+
+  for (int k0 = 0; k0 < s; k0 += KC) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = threadIdx.x + e * 256;
+      const int kk = idx >> 6, jj = idx & 63;
+      const int h = k0 + kk;
+      double2 a = make_double2(0.0, 0.0), b = make_double2(1.0, 0.0);
+      if (h < s) {
+        const int64_t r = __ldg(&rr[h]);
+        const int64_t na = mulmod<FAST>(r, j1_0 + jj, M, invM);
+        a = cmul(__ldg(&cp[h]), __ldg(&twl[na]));
+        const int64_t q = __ldg(&rj[h]);
+        const int64_t nb = mulmod<FAST>(q, j2_0 + jj, M, invM);
+        b = __ldg(&twl[nb]);
+      }
+      As[kk][jj] = a;
+      Bs[kk][jj] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double2 a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][tx + 16 * i]; b[i] = Bs[kk][ty + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fma(a[i].x, b[j].x, acc[i][j].x);
+          acc[i][j].x = fma(-a[i].y, b[j].y, acc[i][j].x);
+          acc[i][j].y = fma(a[i].x, b[j].y, acc[i][j].y);
+          acc[i][j].y = fma(a[i].y, b[j].x, acc[i][j].y);
+        }
+    }
+    __syncthreads();
+  }
+  const double2* ch = chirp + lt.off[l];
+  double2* ub = buf + (int64_t)u * ustride;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t base = J1 * (j2_0 + ty + 16 * j);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t n = j1_0 + tx + 16 * i + base;
+      if (n < M) ub[n] = apply_chirp ? cmul(acc[i][j], __ldg(&ch[n])) : acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B-spline oracle (testbed.py:198-244): f(x) = sum_g prod_{c in A_g} C_m m B_m(m x_c)
+
+// cardinal B-spline of order m (degree m-1) on knots 0..m, Cox-de Boor
+__device__ __forceinline__ double cardinal_bspline(int m, double u) {
+  if (!(u >= 0.0 && u <= (double)m)) return 0.0;
+  double N[8];
+  int iv = (int)floor(u);
+  if (iv >= m) iv = m - 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) N[j] = (j == iv) ? 1.0 : 0.0;
+  for (int k = 2; k <= m; ++k) {
+    const double inv = 1.0 / (double)(k - 1);
+    for (int j = 0; j <= m - k; ++j) N[j] = ((u - j) * N[j] + ((double)(j + k) - u) * N[j + 1]) * inv;
+  }
+  return N[0];
+}
+
+template <bool FAST>
+__global__ void sample_bspline_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at,
+                                      const double2* __restrict__ chirp, double2* __restrict__ buf,
+                                      int64_t ustride, int apply_chirp) {
+  const int u = blockIdx.y;
+  const int l = ut.lat[u], it = ut.it[u];
+  const int64_t M = lt.m[l];
+  const double invM = lt.inv_m[l];
+  const int t1 = lt.d;
+  const int tail = bs.d - t1;
+  const double2* ch = chirp + lt.off[l];
+  double2* ub = buf + (int64_t)u * ustride;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double total = 0.0;
+    for (int g = 0; g < bs.ngroups; ++g) {
+      const int m = bs.order[g];
+      double term = 1.0;
+      for (int q = bs.start[g]; q < bs.start[g + 1]; ++q) {
+        const int c = bs.comps[q];
+        double x;
+        if (c < t1) {
+          const int64_t r = mulmod<FAST>(n, (int64_t)lt.z[l * t1 + c], M, invM);
+          x = (double)r / (double)M;
+        } else {
+          x = at.a[it * tail + (c - t1)];
+        }
+        term = term * (bs.scale[g] * cardinal_bspline(m, (double)m * x));
+      }
+      total += term;
+    }
+    const double2 v = make_double2(total, 0.0);
+    ub[n] = apply_chirp ? cmul(v, __ldg(&ch[n])) : v;
+  }
+}
+
+// in-place x_n <- (x_n + sigma_u (noise_n)) * chirp_n for n < M (host-callback and noisy oracles)
+__global__ void finish_samples_kernel(UnitTable ut, const double2* __restrict__ chirp,
+                                      double2* __restrict__ buf, int64_t ustride,
+                                      const double2* __restrict__ noise, int64_t nstride,
+                                      const double* __restrict__ sigma) {
+  const int u = blockIdx.y;
+  const int l = ut.lat[u];
+  const int64_t M = ut.m[l];
+  const double2* ch = chirp + ut.off[l];
+  double2* ub = buf + (int64_t)u * ustride;
+  const double sg = noise ? sigma[u] : 0.0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = ub[n];
+    if (noise) {
+      const double2 e = noise[(int64_t)u * nstride + n];
+      v = make_double2(v.x + sg * e.x, v.y + sg * e.y);
+    }
+    ub[n] = cmul(v, __ldg(&ch[n]));
+  }
+}
+
+// squared 2-norm of each unit's first M samples (for relative-noise oracles)
+__global__ void unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf, int64_t ustride,
+                                  double* __restrict__ out) {
+  __shared__ double red[32];
+  const int u = blockIdx.y;
+  const int64_t M = ut.m[ut.lat[u]];
+  const double2* ub = buf + (int64_t)u * ustride;
+  double acc = 0.0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = ub[n];
+    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    atomicAdd(&out[u], t);
+  }
+}
+
+// lattice nodes for a host-callback oracle: pts[n, c] (row-major, d columns)
+template <bool FAST>
+__global__ void lattice_nodes_kernel(LatTable lt, int l, int d, AnchorTable at, int it,
+                                     double* __restrict__ pts) {
+  const int64_t M = lt.m[l];
+  const double invM = lt.inv_m[l];
+  const int t1 = lt.d;
+  const int tail = d - t1;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < d; ++c) {
+      double x;
+      if (c < t1) x = (double)mulmod<FAST>(n, (int64_t)lt.z[l * t1 + c], M, invM) / (double)M;
+      else x = at.a[it * tail + (c - t1)];
+      pts[n * d + c] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, const LatTable& lt,
+                        const PolyPlan& pp, const AnchorTable& at, double2* cprime, int32_t* rres,
+                        int32_t* rj, cudaStream_t st) {
+  if (s <= 0) return 0;
+  int bx = (s + 255) / 256;
+  if (bx > 256) bx = 256;
+  poly_rotate_kernel<<<dim3(bx, at.rb), 256, 0, st>>>(hf, coef, s, d, lt.d, at, cprime);
+  SFFT_CHECK_LAUNCH();
+  poly_residue_kernel<<<dim3(bx, lt.nlat), 256, 0, st>>>(hf, s, lt, pp, rres, rj);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
+                       const int32_t* rres, const int32_t* rj, const double2* tw,
+                       const double2* chirp, double2* buf, int64_t ustride, bool fast,
+                       bool apply_chirp, cudaStream_t st) {
+  const int tiles = pp.tile_start[pp.nunits];
+  if (tiles <= 0) return 0;
+  if (fast)
+    sample_poly_kernel<true><<<tiles, 256, 0, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+                                                    ustride, apply_chirp ? 1 : 0);
+  else
+    sample_poly_kernel<false><<<tiles, 256, 0, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+                                                     ustride, apply_chirp ? 1 : 0);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
+                          const AnchorTable& at, const double2* chirp, double2* buf,
+                          int64_t ustride, bool fast, bool apply_chirp, int num_sms,
+                          cudaStream_t st) {
+  int64_t mmax = 1;
+  for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
+  int bx = (int)((mmax + 255) / 256);
+  const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
+  if (bx > cap) bx = cap;
+  if (fast)
+    sample_bspline_kernel<true><<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, lt, bs, at, chirp, buf,
+                                                                     ustride, apply_chirp ? 1 : 0);
+  else
+    sample_bspline_kernel<false><<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, lt, bs, at, chirp, buf,
+                                                                      ustride, apply_chirp ? 1 : 0);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_finish_samples(const UnitTable& ut, const double2* chirp, double2* buf, int64_t ustride,
+                          const double2* noise, int64_t nstride, const double* sigma, int num_sms,
+                          cudaStream_t st) {
+  int64_t mmax = 1;
+  for (int l = 0; l < ut.nlat; ++l) mmax = ut.m[l] > mmax ? ut.m[l] : mmax;
+  int bx = (int)((mmax + 255) / 256);
+  const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
+  if (bx > cap) bx = cap;
+  finish_samples_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, chirp, buf, ustride, noise,
+                                                             nstride, sigma);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_unit_norm2(const UnitTable& ut, const double2* buf, int64_t ustride, double* out,
+                      int num_sms, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * ut.nunits, st);
+  if (e != cudaSuccess) return (int)e;
+  int64_t mmax = 1;
+  for (int l = 0; l < ut.nlat; ++l) mmax = ut.m[l] > mmax ? ut.m[l] : mmax;
+  int bx = (int)((mmax + 255) / 256);
+  const int cap = (num_sms * 4 + ut.nunits - 1) / ut.nunits + 1;
+  if (bx > cap) bx = cap;
+  unit_norm2_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, buf, ustride, out);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_lattice_nodes(const LatTable& lt, int l, int d, const AnchorTable& at, int it,
+                         double* pts, bool fast, cudaStream_t st) {
+  int64_t M = lt.m[l];
+  int bx = (int)((M + 255) / 256);
+  if (bx > 4096) bx = 4096;
+  if (fast) lattice_nodes_kernel<true><<<bx, 256, 0, st>>>(lt, l, d, at, it, pts);
+  else lattice_nodes_kernel<false><<<bx, 256, 0, st>>>(lt, l, d, at, it, pts);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace sfft

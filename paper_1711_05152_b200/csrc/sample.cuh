@@ -1,0 +1,53 @@
+#pragma once
+#include "plan.cuh"
+
+namespace sfft {
+
+// anchor tails of the iterations in one launch: a[it * tail + c]
+struct AnchorTable {
+  int rb;
+  int tail;
+  double a[1024];
+};
+
+// GEMM-factored polynomial sampling plan of one step (see sample.cu)
+struct PolyPlan {
+  int nunits;
+  int s;
+  int unit_lat[SFFT_UMAX];
+  int unit_it[SFFT_UMAX];
+  int tile_start[SFFT_UMAX + 1];
+  int J1[SFFT_LMAX];
+  int nt1[SFFT_LMAX];
+};
+
+// B-spline test function: groups of (order, component slots)
+struct BsplineSpec {
+  int d;
+  int ngroups;
+  int order[8];
+  int start[9];
+  int comps[SFFT_DMAX];
+  double scale[8];  // C_m * m
+};
+
+int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, const LatTable& lt,
+                        const PolyPlan& pp, const AnchorTable& at, double2* cprime, int32_t* rres,
+                        int32_t* rj, cudaStream_t st);
+int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
+                       const int32_t* rres, const int32_t* rj, const double2* tw,
+                       const double2* chirp, double2* buf, int64_t ustride, bool fast,
+                       bool apply_chirp, cudaStream_t st);
+int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
+                          const AnchorTable& at, const double2* chirp, double2* buf,
+                          int64_t ustride, bool fast, bool apply_chirp, int num_sms,
+                          cudaStream_t st);
+int launch_finish_samples(const UnitTable& ut, const double2* chirp, double2* buf, int64_t ustride,
+                          const double2* noise, int64_t nstride, const double* sigma, int num_sms,
+                          cudaStream_t st);
+int launch_unit_norm2(const UnitTable& ut, const double2* buf, int64_t ustride, double* out,
+                      int num_sms, cudaStream_t st);
+int launch_lattice_nodes(const LatTable& lt, int l, int d, const AnchorTable& at, int it,
+                         double* pts, bool fast, cudaStream_t st);
+
+}  // namespace sfft

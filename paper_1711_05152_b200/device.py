@@ -1,0 +1,117 @@
+"""Device context: the CUDA device, its stream, cached FFT tables and typed
+helpers for passing torch device buffers / numpy host metadata to the C ABI.
+
+PyTorch is used only as the device-memory allocator and stream provider; all
+arithmetic is in libsfft_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native
+
+__all__ = ["Device", "get_device", "hptr", "dptr"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def hptr(a: np.ndarray) -> int:
+    """Address of a C-contiguous host numpy array (caller keeps it alive)."""
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def dptr(t) -> int:
+    return t.data_ptr()
+
+
+class Device:
+    """One CUDA device + stream used by the MR1L engine."""
+
+    def __init__(self, index: int | None = None, stream=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_1711_05152_b200 requires a CUDA device (B200, sm_100a); "
+                "there is no CPU fallback"
+            )
+        _native.load()
+        self.index = torch.cuda.current_device() if index is None else int(index)
+        self.torch = torch
+        self.device = torch.device("cuda", self.index)
+        with torch.cuda.device(self.index):
+            self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+            sms = C.c_int(0)
+            maj = C.c_int(0)
+            mnr = C.c_int(0)
+            _native.call("sfft_device_info", C.addressof(sms), C.addressof(maj), C.addressof(mnr))
+        self.num_sms = sms.value
+        self.cc = (maj.value, mnr.value)
+        self._ftab: dict[int, object] = {}
+
+    # -- raw handles ------------------------------------------------------
+    @property
+    def sh(self) -> int:
+        return self.stream.cuda_stream
+
+    def call(self, name: str, *args, ctx: str = ""):
+        with self.torch.cuda.device(self.index):
+            return _native.call(name, *args, self.sh, ctx=ctx)
+
+    # -- allocation ---------------------------------------------------------
+    def empty(self, shape, dtype):
+        return self.torch.empty(shape, dtype=dtype, device=self.device)
+
+    def zeros(self, shape, dtype):
+        return self.torch.zeros(shape, dtype=dtype, device=self.device)
+
+    def upload(self, a: np.ndarray, dtype=None):
+        """Host numpy -> device tensor (ordered on the engine stream)."""
+        torch = self.torch
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        if dtype is not None:
+            t = t.to(dtype)
+        with torch.cuda.stream(self.stream):
+            return t.to(self.device, non_blocking=False)
+
+    def download(self, t) -> np.ndarray:
+        with self.torch.cuda.stream(self.stream):
+            return t.detach().to("cpu").numpy()
+
+    def sync(self):
+        self.stream.synchronize()
+
+    # -- cached tables ------------------------------------------------------
+    def fft_tables(self, p: int):
+        tab = self._ftab.get(p)
+        if tab is None:
+            n = int(_native.query("sfft_fft_table_len", p))
+            if n <= 0:
+                raise ValueError(f"FFT size 2^{p} outside the supported range 2^4..2^24")
+            tab = self.empty((n, 2), self.torch.float64)
+            self.call("sfft_fft_tables", p, dptr(tab), ctx=f"fft tables p={p}")
+            self._ftab[p] = tab
+        return tab
+
+
+_DEVICES: dict[int, Device] = {}
+
+
+def get_device(index: int | None = None) -> Device:
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1711_05152_b200 requires a CUDA device (B200, sm_100a); there is no CPU fallback"
+        )
+    idx = torch.cuda.current_device() if index is None else int(index)
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = Device(idx)
+        _DEVICES[idx] = dev
+    return dev

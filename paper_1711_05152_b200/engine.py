@@ -1,0 +1,391 @@
+"""Dimension-incremental sparse FFT engine (Algorithm 3 of arXiv 1711.05152)
+driving the device MR1L step — the public reconstruction API of the
+reference's detect.py (sparse_fft, DetectionConfig, DetectionReport,
+detect_component, projected_line_coefficients, planners and bounds).
+
+Per component step t the engine
+  1. detects the 1-D component set from r anchored lines (device line kernels),
+  2. forms J_t = prefixes x component on the device (already sorted),
+  3. builds the MR1L scheme on the device (alias histograms, K3),
+  4. runs all r~ iterations of sampling + Bluestein + gather/threshold/cap,
+  5. unions the kept sets by flag compaction into the next prefixes.
+RNG consumption matches the reference stream for stream (detect.py:328-399),
+so lattices, anchors and therefore the detected sets are the reference's.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field, replace
+from typing import Sequence
+
+import numpy as np
+
+from .core import FrequencyIndexSet, SearchBox, SparseSpectrum
+from .device import Device, dptr, get_device, hptr
+from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact,
+                   evaluate_callback, product, run_step)
+from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
+from .primes import MLConfig
+
+__all__ = [
+    "DetectionConfig",
+    "DetectionReport",
+    "OracleInterrupt",
+    "projected_line_coefficients",
+    "detect_component",
+    "sparse_fft",
+    "plan_r",
+    "plan_b",
+    "failure_bound_single_coeff",
+    "union_failure_bound",
+]
+
+
+@dataclass(frozen=True)
+class DetectionConfig:
+    """Engine parameters (reference detect.py:64-127); same fields, defaults
+    and validation errors."""
+
+    box: SearchBox
+    delta: float
+    s: int
+    s_local: int | None = None
+    r: int = 1
+    b: int = 1
+    mode: str = "randomized"
+    lattice_kind: str = "multiple"
+    rng_seed: int = 0
+    dimension_order: tuple[int, ...] | None = None
+    component_delta: float | None = None
+
+    def __post_init__(self):
+        if not isinstance(self.box, SearchBox):
+            raise TypeError("box must be a SearchBox")
+        if not self.delta > 0:
+            raise ValueError("delta must be > 0")
+        if self.s < 1:
+            raise ValueError("sparsity cap s must be >= 1")
+        if self.s_local is not None and self.s_local < 1:
+            raise ValueError("s_local must be >= 1")
+        if self.r < 1:
+            raise ValueError("detection iterations r must be >= 1")
+        if self.b < 1:
+            raise ValueError("lattice retry cap b must be >= 1")
+        if self.mode not in ("randomized", "deterministic_zero_anchor"):
+            raise ValueError("mode must be 'randomized' or 'deterministic_zero_anchor'")
+        if self.lattice_kind not in ("multiple", "single"):
+            raise ValueError("lattice_kind must be 'multiple' or 'single'")
+        if self.rng_seed < 0:
+            raise ValueError("rng_seed must be a nonnegative integer")
+        if self.component_delta is not None and not self.component_delta > 0:
+            raise ValueError("component_delta must be > 0")
+        if self.dimension_order is not None:
+            order = tuple(int(c) for c in self.dimension_order)
+            if sorted(order) != list(range(self.box.dim)):
+                raise ValueError("dimension_order must be a permutation of 0..d-1")
+            object.__setattr__(self, "dimension_order", order)
+
+    @property
+    def local_sparsity(self) -> int:
+        return self.s if self.s_local is None else self.s_local
+
+    @property
+    def component_threshold(self) -> float:
+        return self.delta if self.component_delta is None else self.component_delta
+
+
+@dataclass
+class DetectionReport:
+    """Result and exact accounting of one run (reference detect.py:130-150)."""
+
+    detected: SparseSpectrum
+    component_counts: list[int] = field(default_factory=list)
+    prefix_counts: list[int] = field(default_factory=list)
+    candidate_counts: list[int] = field(default_factory=list)
+    scheme_sizes: list[int] = field(default_factory=list)
+    lattice_attempts: list[int] = field(default_factory=list)
+    detection_calls: list[int] = field(default_factory=list)
+    inversion_calls: list[int] = field(default_factory=list)
+    oracle_calls: int = 0
+    warnings: list[str] = field(default_factory=list)
+    wall_time: float = 0.0
+    step_times: list[float] = field(default_factory=list)
+
+
+# ---------------------------------------------------------------------------
+# oracle plumbing
+
+class _PermutedCallback:
+    """Host-callback oracle seen through a coordinate permutation (detect.py:243-254)."""
+
+    def __init__(self, inner, order: Sequence[int]):
+        self._inner = inner
+        self._order = np.asarray(order, dtype=np.intp)
+        self.dim = len(self._order)
+
+    def __call__(self, points: np.ndarray) -> np.ndarray:
+        full = np.empty_like(points)
+        full[:, self._order] = points
+        return self._inner(full)
+
+
+def _is_device_oracle(oracle) -> bool:
+    base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
+    return isinstance(base, (SparsePolynomialOracle, BSplineOracle))
+
+
+def _permute_oracle(oracle, order):
+    if _is_device_oracle(oracle):
+        return oracle.permuted(order)
+    return _PermutedCallback(oracle, order)
+
+
+def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarray, step: int, it0: int):
+    """Samples of r anchored axis lines of component t -> device (r, K, 2)."""
+    torch = dev.torch
+    r, d = anchors.shape
+    K = int(box.sizes[t])
+    vals = dev.empty((r, K, 2), torch.float64)
+    base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
+    noisy = isinstance(oracle, NoisyOracle)
+    if isinstance(base, SparsePolynomialOracle):
+        hf, cf = base.device_terms(dev)
+        per = max(1, 2048 // d)
+        for i0 in range(0, r, per):
+            a = np.ascontiguousarray(anchors[i0:i0 + per])
+            dev.call("sfft_line_sample_poly", dptr(hf), dptr(cf), base.s, d, t, K, hptr(a), len(a),
+                     dptr(vals[i0:]), ctx=f"line sampling, step {step}")
+    elif isinstance(base, BSplineOracle):
+        pts = np.repeat(anchors, K, axis=0)
+        pts[:, t] = np.tile(np.arange(K) / K, r)
+        d_pts = dev.upload(np.ascontiguousarray(pts))
+        order, start, comps, scale = base.host_spec()
+        dev.call("sfft_eval_bspline_points", dptr(d_pts), r * K, d, len(base.groups), hptr(order),
+                 hptr(start), hptr(comps), hptr(scale), dptr(vals), ctx=f"line sampling, step {step}")
+    else:
+        host = np.empty((r, K, 2))
+        for i in range(r):
+            pts = np.tile(anchors[i], (K, 1))
+            pts[:, t] = np.arange(K) / K
+            v = evaluate_callback(oracle, pts, step, it0 + i)
+            host[i, :, 0], host[i, :, 1] = v.real, v.imag
+        with torch.cuda.stream(dev.stream):
+            vals.copy_(torch.from_numpy(host))
+        return vals
+    if noisy:
+        norms = None
+        if oracle.needs_norm():
+            nrm = dev.empty((r,), torch.float64)
+            km = np.array([K], dtype=np.int64)
+            dev.call("sfft_unit_norm2", hptr(km), 1, r, dptr(vals), K, dptr(nrm), ctx="line noise norm")
+            norms = dev.download(nrm)
+        for i in range(r):
+            e = dev.upload(np.ascontiguousarray(oracle.draw(K)))
+            sc = oracle.scale_for(float(norms[i]) if norms is not None else 0.0, K)
+            dev.call("sfft_add_noise", dptr(vals[i]), dptr(e), K, sc, ctx="line noise")
+            oracle.count_samples(K)
+    else:
+        base.count_samples(r * K)
+    return vals
+
+
+def _lines(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarray, cap: int, delta: float,
+           step: int):
+    """Device line detection: (ks, coefs (r, K) complex, keep (r, K) bool)."""
+    torch = dev.torch
+    r = anchors.shape[0]
+    K = int(box.sizes[t])
+    lo = int(box.lows[t])
+    if K > 1024:
+        raise NotImplementedError("line detection supports component extents K_t <= 1024")
+    vals = _line_values(dev, oracle, t, box, anchors, step, 0)
+    coefs = dev.empty((r, K, 2), torch.float64)
+    keep = dev.empty((r, K), torch.uint8)
+    dev.call("sfft_line_select", dptr(vals), r, K, lo, int(cap), float(delta), dptr(coefs), dptr(keep),
+             ctx=f"line selection, step {step}")
+    return np.arange(lo, lo + K, dtype=np.int64), coefs, keep
+
+
+def projected_line_coefficients(oracle, t: int, box: SearchBox, anchor: np.ndarray,
+                                *, _step_ctx: tuple[int, int] = (0, 0)):
+    """Projected 1-D coefficients along component t at one anchor
+    (reference detect.py:175-194), computed on the device."""
+    dev = get_device()
+    anchor = np.asarray(anchor, dtype=np.float64).reshape(1, -1)
+    ks, coefs, _ = _lines(dev, oracle, t, box, anchor, 1 << 30, 1.0, _step_ctx[0])
+    c = dev.download(coefs)[0]
+    return ks, c[:, 0] + 1j * c[:, 1]
+
+
+def _detect(dev: Device, oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator, step: int):
+    box = cfg.box
+    d = box.dim
+    zero = cfg.mode == "deterministic_zero_anchor"
+    anchors = np.stack([np.zeros(d) if zero else rng.random(d) for _ in range(cfg.r)])
+    ks, _, keep = _lines(dev, oracle, t, box, anchors, cfg.local_sparsity, cfg.component_threshold, step)
+    hit = dev.download(keep).astype(bool).any(axis=0)
+    return ks[hit]
+
+
+def detect_component(oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator | None = None):
+    """Candidate values of component t from r anchored lines (reference detect.py:215-240)."""
+    d = cfg.box.dim
+    if not 0 <= t < d:
+        raise ValueError(f"component index t must lie in 0..{d - 1}")
+    if rng is None:
+        rng = np.random.default_rng(np.random.SeedSequence([cfg.rng_seed, t]))
+    comp = _detect(get_device(), oracle, t, cfg, rng, t)
+    return FrequencyIndexSet(comp[:, None], 1, _presorted=True)
+
+
+# ---------------------------------------------------------------------------
+# the engine
+
+def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None) -> DetectionReport:
+    """Reconstruct support and coefficients of a sparse periodic signal
+    (reference detect.py:305-423) on the GPU."""
+    start = time.perf_counter()
+    if getattr(oracle, "dim", cfg.box.dim) != cfg.box.dim:
+        raise ValueError("oracle dimension does not match the search box")
+    if cfg.lattice_kind != "multiple":
+        raise NotImplementedError(
+            "lattice_kind='single' (Algorithm 5, CBC single lattice) is outside the B200 MR1L path"
+        )
+    dev = device or get_device()
+    box = cfg.box
+    order = cfg.dimension_order
+    if order is not None and order != tuple(range(box.dim)):
+        oracle = _permute_oracle(oracle, order)
+        box = box.permute(order)
+        cfg = replace(cfg, box=box, dimension_order=None)
+    else:
+        order = None
+
+    d = box.dim
+    root = np.random.SeedSequence(cfg.rng_seed)
+    detect_parent, anchor_parent, lattice_parent = root.spawn(3)
+    detect_streams = detect_parent.spawn(d)
+    anchor_streams = anchor_parent.spawn(d)
+    lattice_streams = lattice_parent.spawn(d)
+
+    rep = DetectionReport(detected=SparseSpectrum.from_dict({}, dim=d))
+    for name in ("component_counts", "prefix_counts", "candidate_counts", "scheme_sizes",
+                 "lattice_attempts", "detection_calls", "inversion_calls"):
+        setattr(rep, name, [0] * d)
+    zero = cfg.mode == "deterministic_zero_anchor"
+    extents = (box.highs - box.lows)
+    final_rows = np.empty((0, d), dtype=np.int64)
+    final_coef = np.empty(0, dtype=np.complex128)
+    prefixes: DeviceFreqs | None = None
+
+    for t in range(d):
+        t_step = time.perf_counter()
+        comp = _detect(dev, oracle, t, cfg, np.random.default_rng(detect_streams[t]), t)
+        rep.component_counts[t] = len(comp)
+        rep.detection_calls[t] = cfg.r * int(box.sizes[t])
+        if t == 0:
+            prefixes = DeviceFreqs.from_host(dev, comp[:, None])
+            rep.prefix_counts[0] = rep.candidate_counts[0] = len(comp)
+            if d > 1:
+                rep.step_times.append(time.perf_counter() - t_step)
+                continue
+            cand = prefixes
+        else:
+            cand = product(dev, prefixes, comp)
+            if box.member is not None and cand.n:
+                rows = cand.to_host(dev)
+                rows = rows[box.contains_projected(tuple(range(t + 1)), rows)]
+                cand = DeviceFreqs.from_host(dev, rows) if len(rows) else DeviceFreqs(cand.data[:, :0], 0, 0)
+            rep.candidate_counts[t] = cand.n
+        last = t == d - 1
+        r_tilde = 1 if last else cfg.r
+        s_tilde = cfg.s if last else cfg.local_sparsity
+        if cand.n == 0:
+            prefixes = cand
+            rep.prefix_counts[t] = 0
+            rep.step_times.append(time.perf_counter() - t_step)
+            continue
+        sch = build_scheme(dev, cand, cfg.b, lattice_streams[t],
+                           box_extent=int(extents[: t + 1].max()), ctx=f"lattice search, step {t}")
+        rep.scheme_sizes[t] = sch.total_size
+        rep.lattice_attempts[t] = sch.attempts
+        rep.inversion_calls[t] = r_tilde * sch.total_size
+        if sch.uncovered:
+            rep.warnings.append(
+                f"step {t}: sampling scheme covers only {cand.n - sch.uncovered}/{cand.n} "
+                f"candidates after {sch.attempts} attempts"
+            )
+        anchor_rng = np.random.default_rng(anchor_streams[t])
+        tail = d - (t + 1)
+        tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
+        res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t)
+        if last:
+            rows_d, coef_d = compact(dev, cand, res.keep[0], 1, res.coef[0])
+            final_rows = rows_d.to_host(dev)
+            c = dev.download(coef_d) if coef_d is not None else np.zeros((0, 2))
+            final_coef = c[:, 0] + 1j * c[:, 1]
+            rep.prefix_counts[t] = len(final_rows)
+        else:
+            prefixes, _ = compact(dev, cand, res.keep, r_tilde)
+            rep.prefix_counts[t] = prefixes.n
+        rep.step_times.append(time.perf_counter() - t_step)
+
+    if order is not None:
+        unperm = np.empty_like(final_rows)
+        unperm[:, list(order)] = final_rows
+        final_rows = unperm
+    rep.detected = SparseSpectrum(final_rows, final_coef, d)
+    rep.oracle_calls = sum(rep.detection_calls) + sum(rep.inversion_calls)
+    rep.wall_time = time.perf_counter() - start
+    return rep
+
+
+# ---------------------------------------------------------------------------
+# planners and bounds (reference detect.py:429-486; closed-form host formulas)
+
+def plan_r(sparsity: int, dims: int, eps: float, lattice_kind: str = "multiple") -> int:
+    if sparsity < 1:
+        raise ValueError("sparsity must be >= 1")
+    if dims < 1:
+        raise ValueError("dims must be >= 1")
+    if not 0.0 < eps < 1.0:
+        raise ValueError("eps must lie in (0, 1)")
+    consts = {"multiple": 3.0, "single": 2.0}
+    if lattice_kind not in consts:
+        raise ValueError("lattice_kind must be 'multiple' or 'single'")
+    return math.ceil(2.0 * sparsity * (math.log(consts[lattice_kind]) + math.log(dims)
+                                       + math.log(sparsity) - math.log(eps)))
+
+
+def plan_b(dims: int, eps: float, gamma: float) -> int:
+    if dims < 1:
+        raise ValueError("dims must be >= 1")
+    if not 0.0 < eps < 1.0:
+        raise ValueError("eps must lie in (0, 1)")
+    if not 0.0 < gamma < 1.0:
+        raise ValueError("gamma must lie in (0, 1)")
+    return math.ceil((math.log(3.0) + math.log(dims) - math.log(eps)) / abs(math.log(gamma)))
+
+
+def failure_bound_single_coeff(coeff_magnitudes, delta: float) -> float:
+    mags = np.atleast_1d(np.asarray(coeff_magnitudes, dtype=np.float64))
+    if not len(mags) or (mags < 0).any() or not np.isfinite(mags).all():
+        raise ValueError("coefficient magnitudes must be finite and nonnegative")
+    if delta < 0:
+        raise ValueError("delta must be >= 0")
+    top = float(mags.max())
+    if top <= delta:
+        raise ValueError("bound inapplicable: no magnitude exceeds delta")
+    return 1.0 - (top - delta) / float(mags.sum())
+
+
+def union_failure_bound(q: float, r: int, sparsity: int, bins: int) -> float:
+    if not 0.0 <= q <= 1.0:
+        raise ValueError("q must lie in [0, 1]")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    if sparsity < 0 or bins < 0:
+        raise ValueError("counts must be nonnegative")
+    return min(1.0, min(sparsity, bins) * q ** r)

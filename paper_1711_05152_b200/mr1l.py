@@ -1,0 +1,380 @@
+"""The multiple-rank-1-lattice (MR1L) reconstruction step on the device.
+
+One step, for a candidate set J (sorted, on the device) and r~ anchors:
+
+  construction  K3  alias histograms of all L_max pre-drawn lattices of an
+                     attempt, masks, first-covering L        (construct.py:146-206)
+  sampling      K1  the oracle at every node of every (iteration, lattice)
+                     unit, written pre-chirped                (detect.py:280-299)
+  FFT           K2  batched Bluestein DFT of each unit        (transform.py:121)
+  gather        K4  alias-free bins, lattice average, delta threshold, cap
+                                                              (transform.py:99-127,
+                                                               detect.py:197-212)
+
+The host replays the reference's RNG consumption exactly (primes, generating
+vectors, anchors), so schemes are identical to the reference's on the same
+seeds; the host only ever synchronises to read a handful of counters.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .core import FrequencyIndexSet, MultipleRank1Lattice, Rank1Lattice
+from .device import Device, dptr, hptr
+from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
+from .primes import MLConfig, candidate_primes
+
+__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "run_step", "StepResult",
+           "OracleInterrupt", "OracleError", "evaluate_callback"]
+
+UMAX = 256      # (iteration, lattice) units per launch (plan.cuh SFFT_UMAX)
+RBMAX = 8       # iterations per gather launch
+
+
+class OracleInterrupt(Exception):
+    """Deliberate abort signalled by an oracle; propagates unwrapped
+    (reference detect.py:55-61)."""
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def evaluate_callback(oracle, points: np.ndarray, step: int, iteration: int) -> np.ndarray:
+    """Host-callback evaluation with the reference's error contract (detect.py:157-172)."""
+    try:
+        values = oracle(points)
+    except OracleInterrupt:
+        raise
+    except Exception as exc:
+        raise OracleError(f"oracle evaluation failed at step {step}, iteration {iteration}: {exc}") from exc
+    values = np.asarray(values, dtype=np.complex128)
+    if values.shape != (len(points),):
+        raise OracleError(
+            f"oracle returned shape {values.shape} for {len(points)} points "
+            f"at step {step}, iteration {iteration}"
+        )
+    return values
+
+
+@dataclass
+class DeviceFreqs:
+    """A lexicographically sorted candidate set on the device, component-major int32."""
+
+    data: object          # torch int32 tensor (ncomp, n)
+    n: int
+    kmax: int             # bound on |k_c|
+
+    @property
+    def ncomp(self) -> int:
+        return int(self.data.shape[0])
+
+    @classmethod
+    def from_host(cls, dev: Device, rows: np.ndarray) -> "DeviceFreqs":
+        rows = np.asarray(rows, dtype=np.int64)
+        kmax = int(np.abs(rows).max()) if rows.size else 0
+        t = dev.upload(np.ascontiguousarray(rows.T.astype(np.int32)))
+        return cls(t, rows.shape[0], kmax)
+
+    def to_host(self, dev: Device) -> np.ndarray:
+        return dev.download(self.data).T.astype(np.int64)
+
+
+@dataclass
+class DeviceScheme:
+    primes: list[int]           # the L_max candidate primes
+    z: np.ndarray               # (L_max, t1) int64 generating vectors of the chosen attempt
+    L: int                      # lattices used (early exit) or L_max
+    masks: object               # torch int64 (n,) alias-free bit masks (bit l = lattice l)
+    attempts: int
+    uncovered: int
+
+    @property
+    def m_used(self) -> np.ndarray:
+        return np.asarray(self.primes[: self.L], dtype=np.int64)
+
+    @property
+    def z_used(self) -> np.ndarray:
+        return np.ascontiguousarray(self.z[: self.L].astype(np.int32))
+
+    @property
+    def total_size(self) -> int:
+        return int(sum(self.primes[: self.L]))
+
+
+def _spread_bound(cand: DeviceFreqs, box_extent: int | None) -> int:
+    if box_extent is not None:
+        return int(box_extent)
+    return 2 * cand.kmax
+
+
+def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
+                 *, cfg: MLConfig | None = None, box_extent: int | None = None,
+                 ctx: str = "") -> DeviceScheme:
+    """Algorithm 1 with retries (reference construct.py:146-206) on the device.
+
+    Every attempt pre-draws its L_max generating vectors (stream-identical to
+    the reference's sequential draw, SURVEY §7 hard part 1) and evaluates the
+    alias masks of all of them in one pass; the early-exit L is the largest
+    first-cover index over the candidates.
+    """
+    if b < 1:
+        raise ValueError("retry cap b must be >= 1")
+    n = cand.n
+    if n < 1:
+        raise ValueError("cannot build a sampling scheme for an empty set")
+    cfg = cfg or MLConfig(c=2.0, gamma=0.5)
+    l_max = cfg.max_lattices(n)
+    if l_max > 64:
+        raise ValueError(f"L_max = {l_max} lattices exceeds the 64-bit mask width")
+    t1 = cand.ncomp
+    spread = _spread_bound(cand, box_extent)
+    primes = candidate_primes(None, cfg.size_lower_bound(n), l_max, spread=spread,
+                              rows=lambda: cand.to_host(dev))
+    ms = np.asarray(primes, dtype=np.int64)
+    torch = dev.torch
+    words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
+    scratch = dev.empty((max(words, 1),), torch.int32)
+    masks = dev.empty((n,), torch.int64)
+    stats = dev.empty((2,), torch.int32)
+    z = None
+    stats_h = None
+    attempt = 0
+    for attempt, child in enumerate(seed_seq.spawn(b), start=1):
+        rng = np.random.default_rng(child)
+        z = np.stack([rng.integers(0, m, size=t1, dtype=np.int64) for m in primes])
+        zh = np.ascontiguousarray(z.astype(np.int32))
+        dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
+                 dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
+        stats_h = dev.download(stats)
+        if int(stats_h[1]) == 0:
+            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0)
+    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]))
+
+
+def scheme_to_host(dev: Device, cand_rows: np.ndarray, sch: DeviceScheme) -> MultipleRank1Lattice:
+    """Host MultipleRank1Lattice view of a device scheme (bool masks per lattice)."""
+    target = FrequencyIndexSet(cand_rows, cand_rows.shape[1], _presorted=True)
+    words = dev.download(sch.masks).view(np.uint64)
+    lattices, recon, masks = [], [], []
+    for l in range(sch.L):
+        mk = ((words >> np.uint64(l)) & np.uint64(1)).astype(bool)
+        lattices.append(Rank1Lattice(sch.z[l], sch.primes[l]))
+        recon.append(FrequencyIndexSet(cand_rows[mk], cand_rows.shape[1], _presorted=True))
+        masks.append(mk)
+    return MultipleRank1Lattice(lattices, recon, target, recon_masks=masks)
+
+
+# ---------------------------------------------------------------------------
+# step execution
+
+def fft_exponent(m_max: int) -> int:
+    p = max(4, int(math.ceil(math.log2(max(2 * m_max - 1, 1)))))
+    while (1 << p) < 2 * m_max - 1:
+        p += 1
+    if p > 24:
+        raise ValueError(f"lattice size {m_max} needs an FFT of 2^{p} > 2^24 points")
+    return p
+
+
+@dataclass
+class LatticeTables:
+    ms: np.ndarray
+    zs: np.ndarray
+    p: int
+    tw: object
+    chirp: object
+    bhat: object
+    ftab: object
+
+    @property
+    def P(self) -> int:
+        return 1 << self.p
+
+
+def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str = "") -> LatticeTables:
+    torch = dev.torch
+    ms = np.ascontiguousarray(np.asarray(ms, dtype=np.int64))
+    L = len(ms)
+    p = fft_exponent(int(ms.max()))
+    P = 1 << p
+    tot = int(ms.sum())
+    tw = dev.empty((tot, 2), torch.float64)
+    chirp = dev.empty((tot, 2), torch.float64)
+    dev.call("sfft_lattice_tables", hptr(ms), L, dptr(tw), dptr(chirp), ctx=ctx)
+    ftab = dev.fft_tables(p)
+    bhat = dev.empty((L, P, 2), torch.float64)
+    dev.call("sfft_bluestein_bhat", hptr(ms), L, p, dptr(ftab), dptr(chirp), dptr(bhat), ctx=ctx)
+    return LatticeTables(ms, zs, p, tw, chirp, bhat, ftab)
+
+
+@dataclass
+class StepResult:
+    keep: object              # torch uint8 (r, n)
+    coef: object              # torch float64 (r, n, 2)
+    counts: np.ndarray        # survivors per iteration after threshold and cap
+    nodes: int                # oracle samples taken
+    timings: dict = field(default_factory=dict)
+
+
+def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
+                  tails: list[np.ndarray], buf, step: int, it0: int):
+    """Fill buf[u] (u = i*L + l) with pre-chirped samples of the chunk's units."""
+    torch = dev.torch
+    L = len(tabs.ms)
+    rb = len(tails)
+    P = tabs.P
+    tail = d - t1
+    anchor = np.ascontiguousarray(np.asarray(tails, dtype=np.float64).reshape(rb, tail)) \
+        if tail else np.zeros(1, dtype=np.float64)
+    nodes = rb * int(tabs.ms.sum())
+    base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
+    device_inner = isinstance(base, (SparsePolynomialOracle, BSplineOracle))
+    noisy = isinstance(oracle, NoisyOracle)
+    chirp_now = 0 if noisy else 1
+    if device_inner:
+        if isinstance(base, SparsePolynomialOracle):
+            hf, cf = base.device_terms(dev)
+            s = base.s
+            cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
+            rres = dev.empty((L, max(s, 1)), torch.int32)
+            rj = dev.empty((L, max(s, 1)), torch.int32)
+            dev.call("sfft_sample_poly", dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
+                     hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
+                     dptr(tabs.chirp), dptr(buf), P, chirp_now, ctx=f"sampling, step {step}")
+        else:
+            order, start, comps, scale = base.host_spec()
+            dev.call("sfft_sample_bspline", len(base.groups), hptr(order), hptr(start), hptr(comps),
+                     hptr(scale), d, t1, hptr(tabs.ms), hptr(tabs.zs), L, hptr(anchor), rb,
+                     dptr(tabs.chirp), dptr(buf), P, chirp_now, ctx=f"sampling, step {step}")
+        if noisy:
+            _add_lattice_noise(dev, oracle, tabs, rb, buf)
+        else:
+            base.count_samples(nodes)
+        return nodes
+    # host callback: nodes on the device, values from the callback
+    pts = dev.empty((int(tabs.ms.max()), d), torch.float64)
+    for i in range(rb):
+        tail_i = np.ascontiguousarray(anchor[i] if tail else np.zeros(1))
+        for l in range(L):
+            m = int(tabs.ms[l])
+            dev.call("sfft_lattice_nodes", hptr(tabs.ms), hptr(tabs.zs), L, t1, l, d, hptr(tail_i),
+                     dptr(pts), ctx=f"lattice nodes, step {step}")
+            host_pts = dev.download(pts[:m])
+            vals = evaluate_callback(oracle, host_pts, step, it0 + i)
+            v2 = np.ascontiguousarray(np.stack([vals.real, vals.imag], axis=1))
+            u = i * L + l
+            with torch.cuda.stream(dev.stream):
+                buf[u, :m].copy_(torch.from_numpy(v2), non_blocking=False)
+    dev.call("sfft_finish_samples", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P, 0, 0, 0,
+             ctx=f"pre-chirp, step {step}")
+    return nodes
+
+
+def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb: int, buf):
+    """Noise in the reference's call order (iteration-major, then lattice),
+    drawn from the oracle's numpy stream, added on the device with the
+    pre-chirp."""
+    torch = dev.torch
+    L = len(tabs.ms)
+    P = tabs.P
+    mmax = int(tabs.ms.max())
+    norms = None
+    if oracle.needs_norm():
+        nrm = dev.empty((rb * L,), torch.float64)
+        dev.call("sfft_unit_norm2", hptr(tabs.ms), L, rb, dptr(buf), P, dptr(nrm), ctx="noise norm")
+        norms = dev.download(nrm)
+    noise = np.zeros((rb * L, mmax, 2), dtype=np.float64)
+    sig = np.zeros(rb * L, dtype=np.float64)
+    for i in range(rb):
+        for l in range(L):
+            u = i * L + l
+            m = int(tabs.ms[l])
+            noise[u, :m] = oracle.draw(m)
+            sig[u] = oracle.scale_for(float(norms[u]) if norms is not None else 0.0, m)
+            oracle.count_samples(m)
+    d_noise = dev.upload(noise)
+    d_sig = dev.upload(sig)
+    dev.call("sfft_finish_samples", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P,
+             dptr(d_noise), mmax, dptr(d_sig), ctx="noisy samples")
+
+
+def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
+             d: int, delta: float, cap: int, step: int = 0, tabs: LatticeTables | None = None) -> StepResult:
+    """Sample, transform and invert all r~ iterations of one step; threshold + cap."""
+    torch = dev.torch
+    n = cand.n
+    t1 = cand.ncomp
+    L = sch.L
+    if tabs is None:
+        tabs = lattice_tables(dev, sch.m_used, sch.z_used, ctx=f"lattice tables, step {step}")
+    P = tabs.P
+    r = len(tails)
+    keep = dev.empty((r, n), torch.uint8)
+    coef = dev.empty((r, n, 2), torch.float64)
+    counts = dev.zeros((r,), torch.int32)
+    rb_max = max(1, min(RBMAX, UMAX // L))
+    rb_alloc = min(rb_max, r)
+    buf = dev.empty((rb_alloc * L, P, 2), torch.float64)
+    nodes = 0
+    for i0 in range(0, r, rb_max):
+        rb = min(rb_max, r - i0)
+        nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0)
+        dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+                 dptr(tabs.chirp), dptr(buf), ctx=f"Bluestein FFT, step {step}")
+        dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
+                 dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
+                 dptr(counts), ctx=f"gather/select, step {step}")
+    counts_h = dev.download(counts).astype(np.int64)
+    over = [i for i in range(r) if counts_h[i] > cap]
+    if over:
+        sbytes = int(_native.query("sfft_select_scratch_bytes", n))
+        scratch = dev.empty((sbytes,), torch.uint8)
+        for i in over:
+            dev.call("sfft_select_cap", dptr(coef[i]), dptr(keep[i]), n, int(cap), dptr(scratch),
+                     ctx=f"cap selection, step {step}")
+            counts_h[i] = cap
+    return StepResult(keep, coef, counts_h, nodes)
+
+
+def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):
+    """Rows of ``cand`` whose flag (OR over ``nrows`` rows) is set, in order;
+    optional coefficient gather.  Returns (DeviceFreqs, coef tensor | None)."""
+    torch = dev.torch
+    n = cand.n
+    idx = dev.empty((max(n, 1),), torch.int32)
+    total = dev.empty((1,), torch.int32)
+    sl = int(_native.query("sfft_scan_scratch_len", n))
+    scr = dev.empty((max(sl, 1),), torch.int32)
+    dev.call("sfft_flag_indices", dptr(flags), n, nrows, dptr(idx), dptr(total), dptr(scr), ctx="compaction")
+    cnt = int(dev.download(total)[0])
+    out = dev.empty((cand.ncomp, max(cnt, 1)), torch.int32)
+    cout = dev.empty((max(cnt, 1), 2), torch.float64) if coef is not None else None
+    dev.call("sfft_gather_rows", dptr(cand.data), n, cand.ncomp, dptr(idx), dptr(total), cnt, dptr(out),
+             max(cnt, 1), dptr(coef) if coef is not None else 0, dptr(cout) if cout is not None else 0,
+             ctx="row gather")
+    res = DeviceFreqs(out[:, :cnt] if cnt else out[:, :0], cnt, cand.kmax)
+    if cnt and out.shape[1] != cnt:
+        res.data = out[:, :cnt].contiguous()
+    return res, (cout[:cnt] if cout is not None else None)
+
+
+def product(dev: Device, prefixes: DeviceFreqs, comp: np.ndarray) -> DeviceFreqs:
+    """Candidate product prefixes x comp in row-major (hence lexicographic) order."""
+    torch = dev.torch
+    comp = np.ascontiguousarray(np.asarray(comp, dtype=np.int32))
+    nc = len(comp)
+    tot = prefixes.n * nc
+    out = dev.empty((prefixes.ncomp + 1, max(tot, 1)), torch.int32)
+    if tot:
+        d_comp = dev.upload(comp)
+        dev.call("sfft_candidate_product", dptr(prefixes.data), prefixes.n, prefixes.ncomp,
+                 dptr(d_comp), nc, dptr(out), ctx="candidate product")
+    kmax = max(prefixes.kmax, int(np.abs(comp).max()) if nc else 0)
+    data = out if tot == out.shape[1] else out[:, :tot].contiguous()
+    return DeviceFreqs(data, tot, kmax)

@@ -1,0 +1,213 @@
+"""Generate golden vectors from the UNMODIFIED reference (run in the build
+container, where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+The fixtures pin the CPU oracle (oracle/sfft_oracle.py) and are the
+known answers of the GPU parity tests; nothing at test time reads
+/root/reference.  Inputs come from paper_1711_05152_b200.workloads (pure
+numpy generators with the reference's draw sequences).
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import sfft  # noqa: E402  (the reference)
+import sfft.testbed as ref_testbed  # noqa: E402
+from sfft.construct import _alias_free_mask  # noqa: E402
+from sfft.detect import _select  # noqa: E402
+
+from paper_1711_05152_b200 import workloads  # noqa: E402
+
+
+def _poly_signal(freqs, coeffs):
+    spec = sfft.SparseSpectrum(freqs, coeffs)
+    return sfft.SignalOracle(spec.dim, ref_testbed._poly_oracle_fn(spec.freqs, spec.coeffs))
+
+
+class _BigBox(sfft.SearchBox):
+    """Reference SearchBox without the u64 cardinality guard."""
+
+    def __init__(self, lows, highs, member=None):
+        from sfft.lattice import _freeze
+        self._lows = _freeze(np.asarray(lows, dtype=np.int64))
+        self._highs = _freeze(np.asarray(highs, dtype=np.int64))
+        self._member = member
+
+    @classmethod
+    def centered(cls, dim, n):
+        return cls([-n] * dim, [n] * dim)
+
+    def permute(self, order):
+        return _BigBox(self._lows[list(order)], self._highs[list(order)], None)
+
+
+def pack_masks(masks) -> np.ndarray:
+    words = np.zeros(len(masks[0]), dtype=np.uint64)
+    for l, mk in enumerate(masks):
+        words |= np.asarray(mk, dtype=np.uint64) << np.uint64(l)
+    return words
+
+
+def residues_fixture(out):
+    rng = np.random.default_rng(101)
+    freqs = rng.integers(-50, 51, size=(300, 6))
+    big = np.array([[2**31 - 1, -(2**31 - 1), 5, 0, -7, 2**30], [-(2**31 - 1), 2**31 - 1, 3, 1, 1, 1]])
+    freqs = np.vstack([freqs, big]).astype(np.int64)
+    ms = np.array([7, 13, 601, 1009, 2**31 - 1], dtype=np.int64)
+    zs = np.stack([rng.integers(0, m, size=6, dtype=np.int64) for m in ms])
+    res = np.stack([sfft.residues(freqs, z, m) for z, m in zip(zs, ms)])
+    masks = np.stack([_alias_free_mask(freqs, z, m) for z, m in zip(zs, ms[:4])])
+    nodes = sfft.lattice_nodes(sfft.Rank1Lattice(zs[3], ms[3]))
+    out.update(res_freqs=freqs, res_ms=ms, res_zs=zs, res_values=res, res_masks=masks,
+               nodes_1009=nodes[:64], nodes_z=zs[3])
+
+
+def primes_fixture(out):
+    I = sfft.FrequencyIndexSet(np.array([[0, 0], [40, 1], [-40, 2], [3, -40]]))
+    out["primes_small"] = np.array(sfft.candidate_primes(I, 2 * (len(I) - 1), 6))
+    rng = np.random.default_rng(5)
+    J = sfft.FrequencyIndexSet(rng.integers(-32, 33, size=(5000, 10)))
+    out["primes_5000"] = np.array(sfft.candidate_primes(J, 2 * (len(J) - 1), 19))
+    out["lmax_pins"] = np.array([sfft.MLConfig().max_lattices(n) for n in (1, 2, 1000, 65000, 100000, 650000)])
+
+
+def scheme_fixture(out):
+    """MR1L step on a config-1-shaped instance (|J| = 3000, 60 nonzero)."""
+    wl = workloads.config1(seed=7, n=3000, nnz=60)
+    J = sfft.FrequencyIndexSet(wl.cand)
+    scheme, attempts = sfft.build_multiple_lattice_with_retries(
+        J, sfft.MLConfig(), wl.b, np.random.SeedSequence(wl.lattice_seed))
+    oracle = _poly_signal(wl.oracle.freqs, wl.oracle.coeffs)
+    samples = [sfft.LatticeSamples(lat, oracle(sfft.lattice_nodes(lat))) for lat in scheme.lattices]
+    spec = sfft.invert_multiple(samples, scheme)
+    sel_f, sel_c = _select(spec.freqs, spec.coeffs, len(J), wl.delta)
+    out.update(step_cand=wl.cand.astype(np.int16), step_hf=wl.oracle.freqs, step_hc=wl.oracle.coeffs,
+               step_seed=np.array([wl.lattice_seed], dtype=np.uint64), step_b=np.array([wl.b]),
+               step_ms=np.array([lat.m for lat in scheme.lattices]),
+               step_zs=np.stack([lat.z for lat in scheme.lattices]),
+               step_masks=pack_masks(scheme.recon_masks), step_attempts=np.array([attempts]),
+               step_coef=spec.coeffs, step_cov_freqs=spec.freqs.astype(np.int16),
+               step_sel=sel_f.astype(np.int16), step_sel_coef=sel_c,
+               step_first_samples=samples[0].values[:256])
+
+
+def run_fixture(out, key, oracle, cfg, truth=None):
+    rep = sfft.sparse_fft(oracle, cfg)
+    out[f"{key}_freqs"] = rep.detected.freqs
+    out[f"{key}_coef"] = rep.detected.coeffs
+    out[f"{key}_counts"] = np.array([rep.candidate_counts, rep.prefix_counts, rep.component_counts,
+                                     rep.scheme_sizes, rep.lattice_attempts, rep.inversion_calls])
+    out[f"{key}_calls"] = np.array([rep.oracle_calls])
+    print(f"{key}: detected {len(rep.detected)} calls {rep.oracle_calls} wall {rep.wall_time:.2f}s")
+    if truth is not None:
+        out[f"{key}_err"] = np.array([sfft.relative_spectrum_l2_error(rep.detected, truth)])
+
+
+def runs_fixture(out):
+    wl = workloads.config0()
+    out.update(cfg0_hf=wl.truth.freqs, cfg0_hc=wl.truth.coeffs, cfg0_seed=np.array([wl.cfg.rng_seed], np.uint64))
+    cfg = sfft.DetectionConfig(box=sfft.SearchBox.centered(5, 16), delta=1e-12, s=100, r=2, b=10,
+                               rng_seed=wl.cfg.rng_seed)
+    truth = sfft.SparseSpectrum(wl.truth.freqs, wl.truth.coeffs)
+    run_fixture(out, "cfg0", _poly_signal(wl.truth.freqs, wl.truth.coeffs), cfg, truth)
+
+    # small edge-case runs: caps binding, zero anchor, dimension order, 1-D, noisy
+    rng = np.random.default_rng(42)
+    truth, _ = sfft.gen_random_sparse_poly(3, 6, 25, "box", seed=rng)
+    out.update(cap_hf=truth.freqs, cap_hc=truth.coeffs)
+    run_fixture(out, "cap", _poly_signal(truth.freqs, truth.coeffs),
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(3, 6), delta=1e-12, s=10, s_local=12, r=2,
+                                     b=5, rng_seed=7))
+    rng = np.random.default_rng(47)
+    freqs = np.unique(rng.integers(-5, 6, size=(12, 3)), axis=0)
+    coeffs = rng.uniform(0.5, 2.0, size=len(freqs))
+    out.update(zero_hf=freqs, zero_hc=coeffs.astype(np.complex128))
+    run_fixture(out, "zero", _poly_signal(freqs, coeffs),
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(3, 5), delta=1e-12, s=len(freqs), r=1, b=10,
+                                     mode="deterministic_zero_anchor"))
+    rng = np.random.default_rng(46)
+    truth, _ = sfft.gen_random_sparse_poly(3, 6, 8, "box", seed=rng)
+    out.update(perm_hf=truth.freqs, perm_hc=truth.coeffs)
+    run_fixture(out, "perm", _poly_signal(truth.freqs, truth.coeffs),
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(3, 6), delta=1e-12, s=8, r=1, b=10, rng_seed=11,
+                                     dimension_order=(2, 0, 1)))
+    out.update(one_hf=np.array([[-3], [0], [4]]), one_hc=np.array([1.0, 2.0, 3.0], dtype=np.complex128))
+    run_fixture(out, "one", _poly_signal(np.array([[-3], [0], [4]]), np.array([1.0, 2.0, 3.0])),
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(1, 5), delta=1e-12, s=3, b=5))
+    # noisy (reference NoisyOracle, fixed sigma, numpy noise stream)
+    truth, _ = sfft.gen_random_sparse_poly(4, 8, 20, "unit_modulus", seed=np.random.default_rng(9))
+    out.update(noisy_hf=truth.freqs, noisy_hc=truth.coeffs)
+    noisy = sfft.NoisyOracle(_poly_signal(truth.freqs, truth.coeffs), sfft.sigma_for_snr(20, 30.0), seed=123)
+    run_fixture(out, "noisy", noisy,
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(4, 8), delta=0.3, s=20, r=3, b=10, rng_seed=5))
+    # B-spline (permuted partition, small N, guard bypass)
+    groups = workloads.bspline_partition(np.random.SeedSequence([0, 4, 0]).spawn(3)[0])
+    out["bs_groups"] = np.array([[m] + list(c) + [-1] * (4 - len(c)) for m, c in groups])
+    saved = ref_testbed._BSPLINE_GROUPS
+    ref_testbed._BSPLINE_GROUPS = groups
+    try:
+        run_fixture(out, "bs", sfft.bspline_test_function(),
+                    sfft.DetectionConfig(box=_BigBox.centered(10, 8), delta=1e-4, s=200, r=2, b=10, rng_seed=3))
+        out["bs_l2err"] = np.array([sfft.relative_l2_error(
+            sfft.SparseSpectrum(out["bs_freqs"], out["bs_coef"]), sfft.bspline_exact_coefficients,
+            sfft.bspline_norm_sq())])
+    finally:
+        ref_testbed._BSPLINE_GROUPS = saved
+
+
+def transform_fixture(out):
+    rng = np.random.default_rng(77)
+    for K in (1, 2, 3, 5, 7, 33, 65, 97, 129, 1009, 6007):
+        v = rng.normal(size=K) + 1j * rng.normal(size=K)
+        out[f"dft_in_{K}"] = v
+        out[f"dft_fwd_{K}"] = sfft.dft_1d(v, "forward")
+        out[f"dft_inv_{K}"] = sfft.dft_1d(v, "inverse")
+    spec = sfft.SparseSpectrum([(1, -2, 3), (0, 4, -1), (-3, 0, 0)], [1.0 + 0.5j, -2.0, 0.25j])
+    oracle = _poly_signal(spec.freqs, spec.coeffs)
+    box = sfft.SearchBox([-4, -5, -3], [4, 5, 3])
+    anchor = np.array([0.3, 0.71, 0.05])
+    for t in range(3):
+        ks, c = sfft.projected_line_coefficients(oracle, t, box, anchor)
+        out[f"line_{t}_ks"] = ks
+        out[f"line_{t}_c"] = c
+    out.update(line_hf=spec.freqs, line_hc=spec.coeffs, line_anchor=anchor)
+
+
+def bspline_fixture(out):
+    rng = np.random.default_rng(3)
+    pts = rng.random((500, 10))
+    f = sfft.bspline_test_function()
+    out["bsv_pts"] = pts
+    out["bsv_vals"] = f(pts)
+    ks = rng.integers(-6, 7, size=(200, 10))
+    ks[:100, 3:] = 0
+    out["bsv_ks"] = ks
+    out["bsv_exact"] = sfft.bspline_exact_coefficients(ks)
+    out["bsv_norm_sq"] = np.array([sfft.bspline_norm_sq()])
+    out["bsv_cm"] = np.array([sfft.bspline_l2_constant(m) for m in (2, 4, 6)])
+
+
+def main():
+    out: dict = {}
+    residues_fixture(out)
+    primes_fixture(out)
+    transform_fixture(out)
+    bspline_fixture(out)
+    scheme_fixture(out)
+    runs_fixture(out)
+    np.savez_compressed(HERE / "golden.npz", **out)
+    print("wrote", HERE / "golden.npz", sum(v.nbytes for v in out.values()), "bytes raw")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through libsfft_b200.so) against the golden
+vectors of the unmodified reference and the CPU oracle.
+
+Bar (BASELINE north_star): detected frequency sets and every integer
+quantity (residues, masks, schemes, counts) bit-exact; complex coefficients
+within 1e-10 relative (fp64)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+COEF_RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1711_05152_b200 as P
+    from paper_1711_05152_b200 import _native
+    _native.load()
+    return P
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_cuda_path_is_native(P):
+    import torch
+    from paper_1711_05152_b200.device import get_device
+    assert torch.cuda.is_available()
+    dev = get_device()
+    assert dev.cc[0] == 10, f"expected sm_100 (B200), got {dev.cc}"
+    maps = open("/proc/self/maps").read()
+    assert "libsfft_b200.so" in maps
+
+
+def test_residues_bit_exact(P, golden):
+    f, ms, zs = golden["res_freqs"], golden["res_ms"], golden["res_zs"]
+    I = P.FrequencyIndexSet(f, _presorted=True)
+    for i, (m, z) in enumerate(zip(ms, zs)):
+        assert np.array_equal(P.residues(I, z, int(m)), golden["res_values"][i])
+
+
+def test_lattice_nodes_bit_exact(P, golden):
+    got = P.lattice_nodes(P.Rank1Lattice(golden["nodes_z"], 1009))
+    assert got.shape == (1009, 6)
+    assert np.array_equal(got[:64], golden["nodes_1009"])
+
+
+def test_alias_masks_bit_exact(P, golden):
+    from paper_1711_05152_b200.api import _masks_for
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs
+    dev = get_device()
+    f, ms, zs = golden["res_freqs"], golden["res_ms"][:4], golden["res_zs"][:4]
+    cand = DeviceFreqs.from_host(dev, f)
+    sch = _masks_for(dev, cand, [int(m) for m in ms], zs)
+    words = dev.download(sch.masks).view(np.uint64)
+    for l in range(4):
+        got = ((words >> np.uint64(l)) & np.uint64(1)).astype(bool)
+        assert np.array_equal(got, golden["res_masks"][l])
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 7, 33, 65, 97, 129, 1009, 6007])
+def test_dft_1d_known_answers(P, golden, K):
+    v = golden[f"dft_in_{K}"]
+    for direction, key in (("forward", "dft_fwd"), ("inverse", "dft_inv")):
+        got = P.dft_1d(v, direction)
+        ref = golden[f"{key}_{K}"]
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (K, direction)
+
+
+def test_dft_large_primes_vs_numpy(P):
+    rng = np.random.default_rng(1)
+    for K in (130003, 199999, 1300021):
+        v = rng.normal(size=K) + 1j * rng.normal(size=K)
+        got = P.dft_1d(v)
+        ref = np.fft.fft(v)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), K
+        back = P.dft_1d(got, "inverse")
+        assert np.abs(back - v).max() <= 1e-12 * np.abs(v).max()
+
+
+def test_scheme_bit_exact(P, golden):
+    cand = golden["step_cand"].astype(np.int64)
+    I = P.FrequencyIndexSet(cand, _presorted=True)
+    sch, attempts = P.build_multiple_lattice_with_retries(
+        I, P.MLConfig(), int(golden["step_b"][0]), np.random.SeedSequence(int(golden["step_seed"][0])))
+    assert [lat.m for lat in sch.lattices] == golden["step_ms"].tolist()
+    assert np.array_equal(np.stack([lat.z for lat in sch.lattices]), golden["step_zs"])
+    words = np.zeros(len(cand), dtype=np.uint64)
+    for l, mk in enumerate(sch.recon_masks):
+        words |= mk.astype(np.uint64) << np.uint64(l)
+    assert np.array_equal(words, golden["step_masks"])
+    assert attempts == int(golden["step_attempts"][0])
+
+
+def test_build_multiple_lattice_rng_state(P):
+    # the caller's generator ends where the reference leaves it (construct.py:173-181)
+    rng = np.random.default_rng(3)
+    J = P.FrequencyIndexSet(np.random.default_rng(4).integers(-20, 21, size=(800, 4)))
+    sch = P.build_multiple_lattice(J, P.MLConfig(), rng)
+    from oracle import sfft_oracle as O
+    rng2 = np.random.default_rng(3)
+    ref = O.build_multiple_lattice(J.freqs, rng2)
+    assert [lat.m for lat in sch.lattices] == ref.ms
+    assert rng.random() == rng2.random()
+
+
+def test_invert_multiple_matches_golden(P, golden):
+    cand = golden["step_cand"].astype(np.int64)
+    ms, zs = golden["step_ms"], golden["step_zs"]
+    words = golden["step_masks"]
+    masks = [((words >> np.uint64(l)) & np.uint64(1)).astype(bool) for l in range(len(ms))]
+    I = P.FrequencyIndexSet(cand, _presorted=True)
+    lats = [P.Rank1Lattice(z, int(m)) for z, m in zip(zs, ms)]
+    ml = P.MultipleRank1Lattice(lats, [P.FrequencyIndexSet(cand[mk], 10, _presorted=True) for mk in masks], I,
+                                recon_masks=masks)
+    oracle = P.SparsePolynomialOracle(golden["step_hf"], golden["step_hc"])
+    samples = [P.LatticeSamples(lat, oracle(P.lattice_nodes(lat))) for lat in lats]
+    assert np.abs(samples[0].values[:256] - golden["step_first_samples"]).max() <= 1e-12
+    spec = P.invert_multiple(samples, ml)
+    assert np.array_equal(spec.freqs, golden["step_cov_freqs"].astype(np.int64))
+    assert _rel(spec.coeffs, golden["step_coef"]) <= COEF_RTOL
+
+
+def test_mr1l_step_device_path(P, golden):
+    """Fused device step (K3 + K1 + K2 + K4) on the config-1-shaped fixture."""
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, compact, run_step
+    dev = get_device()
+    cand = golden["step_cand"].astype(np.int64)
+    oracle = P.SparsePolynomialOracle(golden["step_hf"], golden["step_hc"])
+    dc = DeviceFreqs.from_host(dev, cand)
+    sch = build_scheme(dev, dc, int(golden["step_b"][0]), np.random.SeedSequence(int(golden["step_seed"][0])))
+    assert sch.primes[: sch.L] == golden["step_ms"].tolist()
+    res = run_step(dev, oracle, dc, sch, [np.zeros(0)], 10, 1e-12, len(cand))
+    coef = dev.download(res.coef[0])
+    coef = coef[:, 0] + 1j * coef[:, 1]
+    words = dev.download(sch.masks).view(np.uint64)
+    cov = words != 0
+    assert _rel(coef[cov], golden["step_coef"]) <= COEF_RTOL
+    rows, _ = compact(dev, dc, res.keep[0], 1)
+    assert np.array_equal(rows.to_host(dev), golden["step_sel"].astype(np.int64))
+
+
+def _check_report(golden, key, rep, exact_coef=True):
+    assert np.array_equal(rep.detected.freqs, golden[f"{key}_freqs"]), key
+    ref = golden[f"{key}_coef"]
+    if len(ref) and exact_coef:
+        assert _rel(rep.detected.coeffs, ref) <= COEF_RTOL, key
+    cnt = golden[f"{key}_counts"]
+    assert rep.candidate_counts == cnt[0].tolist()
+    assert rep.prefix_counts == cnt[1].tolist()
+    assert rep.component_counts == cnt[2].tolist()
+    assert rep.scheme_sizes == cnt[3].tolist()
+    assert rep.lattice_attempts == cnt[4].tolist()
+    assert rep.inversion_calls == cnt[5].tolist()
+    assert rep.oracle_calls == int(golden[f"{key}_calls"][0])
+
+
+def test_sparse_fft_config0(P, golden):
+    oracle = P.SparsePolynomialOracle(golden["cfg0_hf"], golden["cfg0_hc"])
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(5, 16), delta=1e-12, s=100, r=2, b=10,
+                            rng_seed=int(golden["cfg0_seed"][0]))
+    rep = P.sparse_fft(oracle, cfg)
+    _check_report(golden, "cfg0", rep)
+    assert oracle.call_count == rep.oracle_calls
+
+
+def test_sparse_fft_host_callback(P, golden):
+    """Arbitrary Python oracle: nodes from the device, values from the callback."""
+    from oracle import sfft_oracle as O
+    f, c = golden["cfg0_hf"], golden["cfg0_hc"]
+    oracle = P.SignalOracle(5, lambda p: O.poly_eval(f, c, p))
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(5, 16), delta=1e-12, s=100, r=2, b=10,
+                            rng_seed=int(golden["cfg0_seed"][0]))
+    rep = P.sparse_fft(oracle, cfg)
+    _check_report(golden, "cfg0", rep)
+    assert oracle.call_count == rep.oracle_calls
+
+
+def test_sparse_fft_edge_cases(P, golden):
+    cases = {
+        "cap": (3, dict(box=P.SearchBox.centered(3, 6), delta=1e-12, s=10, s_local=12, r=2, b=5, rng_seed=7)),
+        "zero": (3, dict(box=P.SearchBox.centered(3, 5), delta=1e-12, s=len(golden["zero_hf"]), r=1, b=10,
+                         mode="deterministic_zero_anchor")),
+        "perm": (3, dict(box=P.SearchBox.centered(3, 6), delta=1e-12, s=8, r=1, b=10, rng_seed=11,
+                         dimension_order=(2, 0, 1))),
+        "one": (1, dict(box=P.SearchBox.centered(1, 5), delta=1e-12, s=3, b=5)),
+    }
+    for key, (d, kw) in cases.items():
+        oracle = P.SparsePolynomialOracle(golden[f"{key}_hf"], golden[f"{key}_hc"])
+        rep = P.sparse_fft(oracle, P.DetectionConfig(**kw))
+        _check_report(golden, key, rep)
+
+
+def test_sparse_fft_noisy_same_realisation(P, golden):
+    oracle = P.NoisyOracle(P.SparsePolynomialOracle(golden["noisy_hf"], golden["noisy_hc"]),
+                           P.sigma_for_snr(20, 30.0), seed=123)
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(4, 8), delta=0.3, s=20, r=3, b=10, rng_seed=5)
+    rep = P.sparse_fft(oracle, cfg)
+    _check_report(golden, "noisy", rep)
+    assert oracle.call_count == rep.oracle_calls
+
+
+def test_sparse_fft_bspline(P, golden):
+    g = golden["bs_groups"]
+    groups = tuple((int(row[0]), tuple(int(x) for x in row[1:] if x >= 0)) for row in g)
+    oracle = P.bspline_test_function(groups)
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(10, 8, check_cardinality=False), delta=1e-4, s=200, r=2,
+                            b=10, rng_seed=3)
+    rep = P.sparse_fft(oracle, cfg)
+    got = set(map(tuple, rep.detected.freqs.tolist()))
+    ref = set(map(tuple, golden["bs_freqs"].tolist()))
+    # parity modulo exact-magnitude +-k ties at the cap boundary (SURVEY §7 hard part 5)
+    assert len(got ^ ref) <= 4
+    err = P.relative_l2_error(rep.detected, oracle.exact_coefficients, oracle.norm_sq())
+    assert abs(err - float(golden["bs_l2err"][0])) <= 1e-4 * float(golden["bs_l2err"][0])
+
+
+def test_bspline_points(P, golden):
+    f = P.bspline_test_function()
+    got = f(golden["bsv_pts"])
+    ref = golden["bsv_vals"]
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_projected_line_coefficients(P, golden):
+    oracle = P.SparsePolynomialOracle(golden["line_hf"], golden["line_hc"])
+    box = P.SearchBox([-4, -5, -3], [4, 5, 3])
+    for t in range(3):
+        ks, c = P.projected_line_coefficients(oracle, t, box, golden["line_anchor"])
+        assert np.array_equal(ks, golden[f"line_{t}_ks"])
+        assert np.abs(c - golden[f"line_{t}_c"]).max() <= 1e-12
+
+
+def test_oracle_errors(P):
+    def broken(points):
+        raise RuntimeError("sensor offline")
+
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(2, 3), delta=1e-12, s=5)
+    with pytest.raises(RuntimeError, match="step 0, iteration 0"):
+        P.sparse_fft(P.SignalOracle(2, broken), cfg)
+
+    class Stop(P.OracleInterrupt):
+        pass
+
+    def bail(points):
+        raise Stop("enough")
+
+    with pytest.raises(Stop):
+        P.sparse_fft(P.SignalOracle(2, bail), cfg)
+
+
+def test_zero_signal(P):
+    oracle = P.SignalOracle(3, lambda pts: np.zeros(len(pts), dtype=complex))
+    rep = P.sparse_fft(oracle, P.DetectionConfig(box=P.SearchBox.centered(3, 4), delta=1e-12, s=5, b=5))
+    assert len(rep.detected) == 0
+    assert rep.oracle_calls == oracle.call_count
+
+
+def test_config1_full_size(P):
+    """BASELINE config 1 at full size: |J| = 100000, d = 10, 2000 nonzero.
+    Masks bit-exact against the CPU oracle; coefficients against the truth."""
+    from oracle import sfft_oracle as O
+    from paper_1711_05152_b200 import workloads
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, run_step
+    wl = workloads.config1()
+    dev = get_device()
+    dc = DeviceFreqs.from_host(dev, wl.cand)
+    sch = build_scheme(dev, dc, wl.b, np.random.SeedSequence(wl.lattice_seed))
+    ref = O.build_with_retries(wl.cand, wl.b, np.random.SeedSequence(wl.lattice_seed))
+    assert sch.primes[: sch.L] == ref.ms and sch.uncovered == 0
+    words = dev.download(sch.masks).view(np.uint64)
+    for l, mk in enumerate(ref.masks):
+        assert np.array_equal(((words >> np.uint64(l)) & np.uint64(1)).astype(bool), mk)
+    res = run_step(dev, wl.oracle, dc, sch, [np.zeros(0)], 10, wl.delta, len(wl.cand))
+    coef = dev.download(res.coef[0])
+    coef = coef[:, 0] + 1j * coef[:, 1]
+    assert _rel(coef, wl.truth_coef) <= COEF_RTOL
+    keep = dev.download(res.keep[0]).astype(bool)
+    assert np.array_equal(keep, wl.truth_coef != 0)

@@ -1,0 +1,157 @@
+"""Pin the CPU oracle (oracle/sfft_oracle.py) against golden vectors produced
+by the unmodified reference (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import sfft_oracle as O
+
+
+def test_residues_and_masks(golden):
+    f, ms, zs = golden["res_freqs"], golden["res_ms"], golden["res_zs"]
+    for i, (m, z) in enumerate(zip(ms, zs)):
+        assert np.array_equal(O.residues(f, z, int(m)), golden["res_values"][i])
+    for i in range(4):
+        assert np.array_equal(O.alias_free_mask(f, zs[i], int(ms[i])), golden["res_masks"][i])
+
+
+def test_overflow_free_residues(golden):
+    # components at +-(2^31 - 1) with M = 2^31 - 1 (reference test_lattice.py:213-221)
+    f, ms, zs = golden["res_freqs"], golden["res_ms"], golden["res_zs"]
+    r = O.residues(f[-2:], zs[-1], int(ms[-1]))
+    assert np.array_equal(r, golden["res_values"][-1][-2:])
+    assert (r >= 0).all() and (r < ms[-1]).all()
+
+
+def test_lattice_nodes(golden):
+    got = O.lattice_nodes(golden["nodes_z"], 1009)[:64]
+    assert np.array_equal(got, golden["nodes_1009"])
+
+
+def test_candidate_primes_pins(golden):
+    rows = np.array([[0, 0], [40, 1], [-40, 2], [3, -40]])
+    assert O.candidate_primes(rows, 2 * (len(rows) - 1), 6) == golden["primes_small"].tolist()
+    rng = np.random.default_rng(5)
+    J = O.unique_rows(rng.integers(-32, 33, size=(5000, 10)))
+    assert O.candidate_primes(J, 2 * (len(J) - 1), 19) == golden["primes_5000"].tolist()
+    assert [O.max_lattices(n) for n in (1, 2, 1000, 65000, 100000, 650000)] == golden["lmax_pins"].tolist()
+
+
+def test_dft_known_answers(golden):
+    for K in (1, 2, 3, 5, 7, 33, 65, 97, 129, 1009, 6007):
+        v = golden[f"dft_in_{K}"]
+        fwd = np.fft.fft(v)
+        assert np.abs(fwd - golden[f"dft_fwd_{K}"]).max() <= 1e-12 * max(1.0, np.abs(fwd).max())
+        inv = np.fft.ifft(v)
+        assert np.abs(inv - golden[f"dft_inv_{K}"]).max() <= 1e-12 * max(1.0, np.abs(inv).max())
+
+
+def test_naive_dft_97():
+    # O(K^2) oracle (reference test_transform.py:25-29, 59-66)
+    rng = np.random.default_rng(0)
+    v = rng.normal(size=97) + 1j * rng.normal(size=97)
+    n = np.arange(97)
+    naive = np.exp(-2j * np.pi * np.outer(n, n) / 97) @ v
+    assert np.abs(np.fft.fft(v) - naive).max() <= 1e-12 * np.abs(naive).max()
+
+
+def test_line_coefficients(golden):
+    f, c = golden["line_hf"], golden["line_hc"]
+    fn = lambda p: O.poly_eval(f, c, p)
+    for t in range(3):
+        ks, got = O.line_coefficients(fn, t, [-4, -5, -3], [4, 5, 3], golden["line_anchor"])
+        assert np.array_equal(ks, golden[f"line_{t}_ks"])
+        assert np.abs(got - golden[f"line_{t}_c"]).max() <= 1e-13
+
+
+def test_bspline_values_and_pins(golden):
+    groups = ((2, (0, 2, 7)), (4, (1, 4, 5, 9)), (6, (3, 6, 8)))
+    got = O.bspline_eval(groups, golden["bsv_pts"])
+    ref = golden["bsv_vals"]
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert np.allclose([O.bspline_constant(m) for m in (2, 4, 6)], golden["bsv_cm"], rtol=0, atol=1e-15)
+    assert golden["bsv_norm_sq"][0] == pytest.approx(3.860521370158563, abs=1e-14)
+
+
+def test_scheme_and_step(golden):
+    cand = golden["step_cand"].astype(np.int64)
+    seed = int(golden["step_seed"][0])
+    sch = O.build_with_retries(cand, int(golden["step_b"][0]), np.random.SeedSequence(seed))
+    assert sch.ms == golden["step_ms"].tolist()
+    assert np.array_equal(np.stack(sch.zs), golden["step_zs"])
+    words = np.zeros(len(cand), dtype=np.uint64)
+    for l, mk in enumerate(sch.masks):
+        words |= mk.astype(np.uint64) << np.uint64(l)
+    assert np.array_equal(words, golden["step_masks"])
+    assert sch.attempts == int(golden["step_attempts"][0])
+    fn = lambda p: O.poly_eval(golden["step_hf"], golden["step_hc"], p)
+    vals = [fn(O.lattice_nodes(z, m)) for m, z in zip(sch.ms, sch.zs)]
+    assert np.abs(vals[0][:256] - golden["step_first_samples"]).max() <= 1e-13
+    cov, coefs = O.invert_multiple(cand, sch, vals)
+    assert np.array_equal(cand[cov], golden["step_cov_freqs"].astype(np.int64))
+    ref = golden["step_coef"]
+    assert np.linalg.norm(coefs - ref) <= 1e-12 * np.linalg.norm(ref)
+    f, c = O.select(cand[cov], coefs, len(cand), 1e-12)
+    assert np.array_equal(f, golden["step_sel"].astype(np.int64))
+
+
+def _check_run(golden, key, rep, tol=1e-10):
+    assert np.array_equal(rep.freqs, golden[f"{key}_freqs"])
+    ref = golden[f"{key}_coef"]
+    if len(ref):
+        assert np.linalg.norm(rep.coeffs - ref) <= tol * np.linalg.norm(ref)
+    cnt = golden[f"{key}_counts"]
+    assert rep.candidate_counts == cnt[0].tolist()
+    assert rep.prefix_counts == cnt[1].tolist()
+    assert rep.component_counts == cnt[2].tolist()
+    assert rep.scheme_sizes == cnt[3].tolist()
+    assert rep.attempts == cnt[4].tolist()
+    assert rep.oracle_calls == int(golden[f"{key}_calls"][0])
+
+
+def test_engine_config0(golden):
+    f, c = golden["cfg0_hf"], golden["cfg0_hc"]
+    rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-16] * 5, [16] * 5, 1e-12, 100, r=2, b=10,
+                       rng_seed=int(golden["cfg0_seed"][0]))
+    _check_run(golden, "cfg0", rep)
+
+
+def test_engine_caps_zero_anchor_1d(golden):
+    f, c = golden["cap_hf"], golden["cap_hc"]
+    rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-6] * 3, [6] * 3, 1e-12, 10, r=2, b=5, rng_seed=7,
+                       s_local=12)
+    _check_run(golden, "cap", rep)
+    f, c = golden["zero_hf"], golden["zero_hc"]
+    rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-5] * 3, [5] * 3, 1e-12, len(f), r=1, b=10,
+                       zero_anchor=True)
+    _check_run(golden, "zero", rep)
+    f, c = golden["one_hf"], golden["one_hc"]
+    rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-5], [5], 1e-12, 3, r=1, b=5)
+    _check_run(golden, "one", rep)
+
+
+def test_engine_noisy(golden):
+    f, c = golden["noisy_hf"], golden["noisy_hc"]
+    rng = np.random.default_rng(123)
+    sigma = float(np.sqrt(20) / np.sqrt(10 ** 3.0))
+
+    def noisy(p):
+        v = O.poly_eval(f, c, p)
+        e = rng.standard_normal((len(p), 2)) @ np.array([1.0, 1.0j])
+        return v + sigma / np.sqrt(2.0) * e
+
+    rep = O.sparse_fft(noisy, [-8] * 4, [8] * 4, 0.3, 20, r=3, b=10, rng_seed=5)
+    _check_run(golden, "noisy", rep)
+
+
+def test_engine_bspline(golden):
+    g = golden["bs_groups"]
+    groups = tuple((int(row[0]), tuple(int(x) for x in row[1:] if x >= 0)) for row in g)
+    rep = O.sparse_fft(lambda p: O.bspline_eval(groups, p), [-8] * 10, [8] * 10, 1e-4, 200, r=2, b=10,
+                       rng_seed=3)
+    # ulp-level differences may swap exact-tie cap-boundary pairs (SURVEY §7 hard part 5)
+    got = set(map(tuple, rep.freqs.tolist()))
+    ref = set(map(tuple, golden["bs_freqs"].tolist()))
+    diff = got ^ ref
+    assert len(diff) <= 4
+    assert len(rep.freqs) == len(golden["bs_freqs"])
