@@ -36,6 +36,8 @@ extern "C" {
 #define SFFT_B200_ABI_VERSION 1
 
 int sfft_abi_version(void);
+/* kernels launched by this library since load (all devices, all streams) */
+long long sfft_launch_count(void);
 const char* sfft_error_string(int code);
 /* number of SMs and compute capability of the current device */
 int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);

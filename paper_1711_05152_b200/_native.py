@@ -19,6 +19,7 @@ _int = C.c_int
 # name -> (restype, argtypes); pointers are passed as integers (c_void_p)
 _SIGS = {
     "sfft_abi_version": (_int, []),
+    "sfft_launch_count": (C.c_longlong, []),
     "sfft_error_string": (C.c_char_p, [_int]),
     "sfft_device_info": (_int, [_vp, _vp, _vp]),
     "sfft_alias_scratch_words": (_i64, [_vp, _int]),

@@ -144,6 +144,57 @@ def build_multiple_lattice_with_retries(I: FrequencyIndexSet, cfg: MLConfig, b: 
 
 
 # ---------------------------------------------------------------------------
+# one MR1L reconstruction step with a known candidate set (BASELINE config 1)
+
+@dataclass
+class StepReport:
+    coeffs: np.ndarray        # (n,) complex; 0 where uncovered
+    covered: np.ndarray       # (n,) bool
+    kept: np.ndarray          # (n,) bool: |c| >= delta (and within the cap)
+    lattice_sizes: list
+    generating_vectors: np.ndarray
+    attempts: int
+    oracle_calls: int
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: float = 0.0,
+                     cap: int | None = None, anchor_tail=None, device=None) -> StepReport:
+    """Build the MR1L scheme for ``candidates``, sample ``oracle`` on it,
+    invert and threshold: the composition build_multiple_lattice_with_retries
+    -> oracle(lattice nodes) -> invert_multiple -> _select of the reference
+    (construct.py:185-206, detect.py:290-299, transform.py:99-127,
+    detect.py:197-212) as one device pipeline."""
+    from .mr1l import compact, run_step
+    rows = np.asarray(candidates, dtype=np.int64)
+    if rows.ndim != 2 or not len(rows):
+        raise ValueError("candidates must be a nonempty (n, d) integer array")
+    dev = device or get_device()
+    n, t1 = rows.shape
+    d = oracle.dim
+    tail = np.zeros(d - t1) if anchor_tail is None else np.asarray(anchor_tail, dtype=np.float64)
+    if seed_seq is None:
+        seed_seq = np.random.SeedSequence(0)
+    elif not isinstance(seed_seq, np.random.SeedSequence):
+        seed_seq = np.random.SeedSequence(seed_seq)
+    cand = DeviceFreqs.from_host(dev, rows)
+    h2d = cand.n * cand.ncomp * 4
+    if hasattr(oracle, "device_terms"):
+        oracle._dev_cache.pop(dev.index, None)
+        hf, cf = oracle.device_terms(dev)
+        h2d += hf.numel() * 4 + cf.numel() * 8
+    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((rows.max(0) - rows.min(0)).max()))
+    res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap))
+    coef = dev.download(res.coef[0])
+    keep = dev.download(res.keep[0]).astype(bool)
+    words = dev.download(sch.masks).view(np.uint64)
+    d2h = coef.nbytes + keep.nbytes + words.nbytes
+    return StepReport(coef[:, 0] + 1j * coef[:, 1], words != 0, keep, sch.primes[: sch.L], sch.z[: sch.L],
+                      sch.attempts, res.nodes, h2d, d2h)
+
+
+# ---------------------------------------------------------------------------
 # transforms
 
 @dataclass(frozen=True)

@@ -129,7 +129,7 @@ int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* 
   if (d <= DMV) {                                                                            \
     if (fast) launch_alias_t<DMV, true>(freqs, n, lt, bits, words, masks, stats, blocks, st); \
     else launch_alias_t<DMV, false>(freqs, n, lt, bits, words, masks, stats, blocks, st);     \
-    SFFT_CHECK_LAUNCH();                                                                     \
+    SFFT_CHECK_LAUNCHES(2);                                                                  \
     return 0;                                                                                \
   }
   SFFT_ALIAS_CASE(4)

@@ -147,6 +147,8 @@ extern "C" {
 
 int sfft_abi_version(void) { return SFFT_B200_ABI_VERSION; }
 
+long long sfft_launch_count(void) { return g_launches.load(); }
+
 const char* sfft_error_string(int code) {
   if (code == 0) return "ok";
   if (code == E_INVAL) return "invalid argument";

@@ -10,10 +10,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define SFFT_DMAX 64          // largest dimension handled by the device kernels
 #define SFFT_LMAX 64          // masks are one uint64 word per candidate
 
 namespace sfft {
+
+// number of kernels this library has launched (reported by sfft_launch_count)
+inline std::atomic<long long> g_launches{0};
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -95,8 +100,12 @@ __device__ __forceinline__ int block_sum(int v, int* smem32) {
 
 }  // namespace sfft
 
-#define SFFT_CHECK_LAUNCH()                           \
+// every kernel launch is followed by SFFT_CHECK_LAUNCH() (one launch) or
+// SFFT_CHECK_LAUNCHES(n) (n launches since the last check)
+#define SFFT_CHECK_LAUNCHES(n)                        \
   do {                                                \
+    ::sfft::g_launches += (n);                        \
     cudaError_t _e = cudaGetLastError();              \
     if (_e != cudaSuccess) return (int)_e;            \
   } while (0)
+#define SFFT_CHECK_LAUNCH() SFFT_CHECK_LAUNCHES(1)

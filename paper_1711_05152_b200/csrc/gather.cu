@@ -396,7 +396,7 @@ int launch_select_cap(const double2* coef, uint8_t* keep, int64_t n, int cap, ui
     sel_hist_kernel<<<blocks, 256, 0, st>>>(coef, keep, n, stt, shift, hist);
     sel_pick_kernel<<<1, 256, 0, st>>>(stt, shift, hist);
   }
-  SFFT_CHECK_LAUNCH();
+  SFFT_CHECK_LAUNCHES(16);
   sel_apply_kernel<<<blocks, 256, 0, st>>>(coef, keep, n, stt, tie);
   SFFT_CHECK_LAUNCH();
   int rc = launch_flag_indices(tie, n, 1, tie_idx, total, sscr, st);

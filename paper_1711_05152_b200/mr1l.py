@@ -304,15 +304,55 @@ def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb
              dptr(d_noise), mmax, dptr(d_sig), ctx="noisy samples")
 
 
+class StageTimer:
+    """CUDA-event brackets around the stages of run_step (on the engine stream)."""
+
+    def __init__(self, dev: Device):
+        self.dev = dev
+        self.marks: list[tuple[str, object, object]] = []
+
+    def span(self, name: str):
+        timer = self
+
+        class _Span:
+            def __enter__(self_inner):
+                self_inner.a = timer.dev.torch.cuda.Event(enable_timing=True)
+                self_inner.a.record(timer.dev.stream)
+
+            def __exit__(self_inner, *exc):
+                b = timer.dev.torch.cuda.Event(enable_timing=True)
+                b.record(timer.dev.stream)
+                timer.marks.append((name, self_inner.a, b))
+                return False
+
+        return _Span()
+
+    def totals_ms(self) -> dict:
+        self.dev.sync()
+        out: dict = {}
+        for name, a, b in self.marks:
+            out.setdefault(name, []).append(a.elapsed_time(b))
+        return out
+
+
+class _NoTimer:
+    def span(self, name):
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
-             d: int, delta: float, cap: int, step: int = 0, tabs: LatticeTables | None = None) -> StepResult:
+             d: int, delta: float, cap: int, step: int = 0, tabs: LatticeTables | None = None,
+             timer: StageTimer | None = None) -> StepResult:
     """Sample, transform and invert all r~ iterations of one step; threshold + cap."""
     torch = dev.torch
+    tm = timer or _NoTimer()
     n = cand.n
     t1 = cand.ncomp
     L = sch.L
     if tabs is None:
-        tabs = lattice_tables(dev, sch.m_used, sch.z_used, ctx=f"lattice tables, step {step}")
+        with tm.span("tables"):
+            tabs = lattice_tables(dev, sch.m_used, sch.z_used, ctx=f"lattice tables, step {step}")
     P = tabs.P
     r = len(tails)
     keep = dev.empty((r, n), torch.uint8)
@@ -324,12 +364,15 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     nodes = 0
     for i0 in range(0, r, rb_max):
         rb = min(rb_max, r - i0)
-        nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0)
-        dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
-                 dptr(tabs.chirp), dptr(buf), ctx=f"Bluestein FFT, step {step}")
-        dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
-                 dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
-                 dptr(counts), ctx=f"gather/select, step {step}")
+        with tm.span("sample"):
+            nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0)
+        with tm.span("fft"):
+            dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+                     dptr(tabs.chirp), dptr(buf), ctx=f"Bluestein FFT, step {step}")
+        with tm.span("gather"):
+            dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
+                     dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
+                     dptr(counts), ctx=f"gather/select, step {step}")
     counts_h = dev.download(counts).astype(np.int64)
     over = [i for i in range(r) if counts_h[i] > cap]
     if over:
