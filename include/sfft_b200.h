@@ -80,13 +80,18 @@ int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_fta
  * x_n * chirp_l[n] (n < M_l) in its buffer, x_n = p(node n of lattice l with
  * anchor tail i).  Terms: d_hfreqs component-major (d x s int32), d_hcoef s
  * complex.  h_anchor: rb x (d - t1) doubles.  Scratch: d_cprime rb*s complex,
- * d_rres and d_rj L*s int32 each.  apply_chirp = 0 leaves the raw samples. */
+ * d_rres and d_rj L*s int32 each, d_partial partial_len complex (term-slice
+ * partial sums; sfft_sample_poly_scratch() gives the size for the best
+ * split, a smaller buffer selects a smaller split, 0 disables it).
+ * apply_chirp = 0 leaves the raw samples. */
+int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s);
 int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
                      const int64_t* h_m, const int32_t* h_z, int L,
                      const double* h_anchor, int rb,
                      double* d_cprime, int32_t* d_rres, int32_t* d_rj,
                      const double* d_tw, const double* d_chirp,
-                     double* d_buf, int64_t P, int apply_chirp, void* stream);
+                     double* d_buf, int64_t P, int apply_chirp,
+                     double* d_partial, int64_t partial_len, void* stream);
 /* B-spline oracle (testbed.py:198-244): ngroups tensor-product terms; group g
  * has spline order h_order[g] (<= 8), scale h_scale[g] = C_m * m, and the
  * component slots h_comps[h_start[g] .. h_start[g+1]). */

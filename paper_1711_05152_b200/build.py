@@ -43,16 +43,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     cc = nvcc()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                     "-I", str(HERE.parent / "include")]
-    objs = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = objdir / (Path(src).stem + ".o")
         cmd = [cc, "-c", str(CSRC / src), "-o", str(obj)] + flags
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
-        if verbose and res.stderr:
-            print(res.stderr, file=sys.stderr)
-        objs.append(str(obj))
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        for src, obj, res in ex.map(compile_one, SOURCES):
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
+            if verbose and res.stderr:
+                print(res.stderr, file=sys.stderr)
+            objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [cc, "-shared", "-o", str(tmp)] + objs + ARCH + ["-cudart", "static"]
     res = subprocess.run(cmd, capture_output=True, text=True)

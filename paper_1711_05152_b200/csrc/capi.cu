@@ -141,6 +141,67 @@ void choose_j1(int64_t m, int& j1, int& nt1, int& nt2) {
   nt2 = (int)((J2 + 63) / 64);
 }
 
+// Tiles, K split and table split of the GEMM-factored polynomial sampling.
+// The K split (term slices reduced in order by a second kernel) is chosen to
+// maximise the fraction of the last wave that is busy; `need` = partial-sum
+// scratch in complex elements (0 without a split).  partial_cap < 0: unlimited.
+int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int num_sms,
+                    int64_t partial_cap, int64_t* need) {
+  if (L < 1 || L > SFFT_LMAX || rb < 1 || (int64_t)rb * L > SFFT_UMAX || s < 0) return E_2BIG;
+  memset(pp, 0, sizeof(PolyPlan));
+  pp->nunits = rb * L;
+  pp->s = s;
+  int64_t mmax = 1;
+  for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
+  int bl = 1;
+  while (((int64_t)1 << (2 * bl)) < mmax) ++bl;
+  pp->bl = bl;
+  const size_t smem = sample_poly_smem(bl, mmax);
+  if (smem > 227 * 1024) return E_2BIG;
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  int64_t tiles_l[SFFT_LMAX];
+  int64_t tiles_total = 0;
+  for (int l = 0; l < L; ++l) {
+    int j1, nt1, nt2;
+    choose_j1(h_m[l], j1, nt1, nt2);
+    pp->J1[l] = j1;
+    pp->nt1[l] = nt1;
+    tiles_l[l] = (int64_t)nt1 * nt2;
+    tiles_total += (int64_t)rb * tiles_l[l];
+    pp->mu[l] = ~0ull / (uint64_t)h_m[l];
+  }
+  const int64_t slots = (int64_t)per_sm * num_sms;
+  int best_ks = 1, best_kper = ((s + 15) / 16) * 16;
+  double best_eff = -1.0;
+  for (int ks = 1; ks <= 8; ++ks) {
+    int kper = (((s + ks - 1) / ks + 15) / 16) * 16;
+    if (kper < 16) kper = 16;
+    const int kse = (s + kper - 1) / kper > 0 ? (s + kper - 1) / kper : 1;
+    if (ks > 1 && (kper < 64 || kse != ks)) continue;
+    if (kse > 1 && partial_cap >= 0 && (int64_t)kse * pp->nunits * mmax > partial_cap) continue;
+    const int64_t units = tiles_total * kse;
+    const int64_t waves = (units + slots - 1) / slots;
+    double eff = (double)units / (double)(waves * slots);
+    if (kse > 1) eff *= 0.97;  // partial-sum write/read + reduce kernel
+    if (eff > best_eff + 1e-9) { best_eff = eff; best_ks = kse; best_kper = kper; }
+  }
+  pp->ks = best_ks;
+  pp->kper = best_kper;
+  int64_t acc = 0;
+  for (int i = 0; i < rb; ++i)
+    for (int l = 0; l < L; ++l) {
+      const int u = i * L + l;
+      pp->unit_lat[u] = l;
+      pp->unit_it[u] = i;
+      pp->tile_start[u] = (int)acc;
+      acc += tiles_l[l] * best_ks;
+    }
+  pp->tile_start[rb * L] = (int)acc;
+  if (acc > 0x7fffffffLL) return E_2BIG;
+  *need = best_ks > 1 ? (int64_t)best_ks * pp->nunits * mmax : 0;
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -232,7 +293,7 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
                      const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
                      double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
                      const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
-                     void* stream) {
+                     double* d_partial, int64_t partial_len, void* stream) {
   if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
@@ -245,37 +306,31 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
   at.tail = tail;
   for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
   PolyPlan* pp = new PolyPlan;
-  memset(pp, 0, sizeof(PolyPlan));
-  pp->nunits = rb * L;
-  pp->s = s;
-  int tiles_l[SFFT_LMAX];
-  for (int l = 0; l < L; ++l) {
-    int j1, nt1, nt2;
-    choose_j1(h_m[l], j1, nt1, nt2);
-    pp->J1[l] = j1;
-    pp->nt1[l] = nt1;
-    tiles_l[l] = nt1 * nt2;
-  }
-  int64_t acc = 0;
-  for (int i = 0; i < rb; ++i)
-    for (int l = 0; l < L; ++l) {
-      const int u = i * L + l;
-      pp->unit_lat[u] = l;
-      pp->unit_it[u] = i;
-      pp->tile_start[u] = (int)acc;
-      acc += tiles_l[l];
-    }
-  pp->tile_start[rb * L] = (int)acc;
-  if (acc > 0x7fffffffLL) { delete pp; return E_2BIG; }
+  int64_t need = 0;
+  rc = build_poly_plan(pp, h_m, L, rb, s, num_sms_current(), partial_len, &need);
+  if (rc) { delete pp; return rc; }
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb);
+  if (rc) { delete pp; return rc; }
+  int64_t mmax = 1;
+  for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
   cudaStream_t st = S(stream);
   rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at,
                            (double2*)d_cprime, d_rres, d_rj, st);
   if (!rc)
-    rc = launch_sample_poly(*pp, lt, (const double2*)d_cprime, d_rres, d_rj, (const double2*)d_tw,
-                            (const double2*)d_chirp, (double2*)d_buf, P, mulmod_fast(h_m, L),
-                            apply_chirp != 0, st);
+    rc = launch_sample_poly(*pp, lt, ut, (const double2*)d_cprime, d_rres, d_rj,
+                            (const double2*)d_tw, (const double2*)d_chirp, (double2*)d_buf, P,
+                            apply_chirp != 0, (double2*)d_partial, mmax, num_sms_current(), st);
   delete pp;
   return rc;
+}
+
+int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s) {
+  PolyPlan* pp = new PolyPlan;
+  int64_t need = 0;
+  int rc = build_poly_plan(pp, h_m, L, rb, s, num_sms_current(), -1, &need);
+  delete pp;
+  return rc ? -1 : need;
 }
 
 int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_start,

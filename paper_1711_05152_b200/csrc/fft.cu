@@ -88,18 +88,19 @@ __global__ void bluestein_b_kernel(LatTable lt, const double2* __restrict__ chir
 }
 
 // ---------------------------------------------------------------------------
-// column pass (P1 > 1).  CTA = C = 4096/P1 consecutive columns of one unit.
-// FWD: mask n >= M to zero if MASK, forward FFT, twiddle, store transposed.
-// INV: inverse FFT, post-chirp, store n < M.
-template <bool INV>
-__global__ void __launch_bounds__(FFT_T)
+// column pass (P1 = 2^LOG1 > 1, P2 = 4096).  CTA = C = 4096/P1 consecutive
+// columns of one unit.  FWD: mask n >= M to zero if mask_input, forward FFT,
+// twiddle, store transposed.  INV: inverse FFT, post-chirp, store n < M.
+template <int LOG1, bool INV>
+__global__ void __launch_bounds__(FFT_T, 2)
 fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int mask_input,
                const double2* __restrict__ ftab, const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
+  constexpr int P1 = 1 << LOG1;
+  constexpr int P2 = FFT_E;
+  constexpr int C = FFT_E / P1;
+  constexpr int rstride = fft_rstride(P1);
   const FftGeom g = fft_geom(p);
-  const int P1 = g.P1, P2 = g.P2;
-  const int C = FFT_E / P1;
-  const int rstride = fft_rstride(P1);
   const int u = blockIdx.y;
   const int c0 = blockIdx.x * C;
   const int lat = ut.lat[u];
@@ -107,6 +108,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   double2* ub = buf + (int64_t)u * ustride;
 
   // load (coalesced along columns), transpose into rows of length P1
+#pragma unroll 4
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int c = f % C, n1 = f / C;
     const int64_t n = (int64_t)n1 * P2 + c0 + c;
@@ -116,8 +118,9 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     s[c * rstride + fpad(n1)] = v;
   }
   __syncthreads();
-  block_fft<INV>(s, C, rstride, g.p1, ftab + g.off_p1);
+  block_fft<LOG1, INV>(s, ftab + g.off_p1);
   if (!INV) {
+#pragma unroll 4
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int c = f % C, k1 = f / C;
       const int64_t n2 = c0 + c;
@@ -127,6 +130,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     }
   } else {
     const double2* ch = chirp + ut.off[lat];
+#pragma unroll 4
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int c = f % C, n1 = f / C;
       const int64_t n = (int64_t)n1 * P2 + c0 + c;
@@ -136,25 +140,27 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 }
 
 // ---------------------------------------------------------------------------
-// row pass.  CTA = 4096/P2 rows (rows index (unit, k1) flattened).
+// row pass (P2 = 2^LOG2).  CTA = 4096/P2 rows (rows index (unit, k1) flattened).
 // MODE 0 (conv): forward FFT, * bhat, inverse FFT, then twiddle (P1 > 1) or
 //                post-chirp (P1 == 1, whole transform in one row).
 // MODE 1 (fwd only, builds bhat): forward FFT, scale by 1/P.
-template <int MODE>
-__global__ void __launch_bounds__(FFT_T)
+template <int LOG2, int MODE>
+__global__ void __launch_bounds__(FFT_T, 2)
 fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int total_rows,
                const double2* __restrict__ ftab, const double2* __restrict__ bhat,
                const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
+  constexpr int P2 = 1 << LOG2;
+  constexpr int rows = FFT_E / P2;
+  constexpr int rstride = fft_rstride(P2);
   const FftGeom g = fft_geom(p);
-  const int P1 = g.P1, P2 = g.P2;
-  const int rows = FFT_E / P2;
-  const int rstride = fft_rstride(P2);
+  const int P1 = g.P1;
   const int g0 = blockIdx.x * rows;
   const bool single = (P1 == 1);
 
+#pragma unroll 4
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
-    const int r = f / P2, i = f - r * P2;
+    const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
     double2 v = make_double2(0.0, 0.0);
     if (grow < total_rows) {
@@ -166,11 +172,12 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     s[r * rstride + fpad(i)] = v;
   }
   __syncthreads();
-  block_fft<false>(s, rows, rstride, g.p2, ftab + g.off_p2);
+  block_fft<LOG2, false>(s, ftab + g.off_p2);
   if (MODE == 1) {
     const double scale = 1.0 / (double)g.P;  // exact: P is a power of two
+#pragma unroll 4
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
-      const int r = f / P2, i = f - r * P2;
+      const int r = f / P2, i = f % P2;
       const int grow = g0 + r;
       if (grow < total_rows) {
         const int u = grow / P1, k1 = grow - u * P1;
@@ -181,8 +188,9 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     return;
   }
   // pointwise product with Bhat (same layout)
+#pragma unroll 4
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
-    const int r = f / P2, i = f - r * P2;
+    const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
     if (grow < total_rows) {
       const int u = grow / P1, k1 = grow - u * P1;
@@ -193,9 +201,10 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     }
   }
   __syncthreads();
-  block_fft<true>(s, rows, rstride, g.p2, ftab + g.off_p2);
+  block_fft<LOG2, true>(s, ftab + g.off_p2);
+#pragma unroll 4
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
-    const int r = f / P2, i = f - r * P2;
+    const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
     if (grow < total_rows) {
       const int u = grow / P1, k1 = grow - u * P1;
@@ -210,6 +219,51 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
       }
     }
   }
+}
+
+// compile-time size dispatch
+template <bool INV>
+static int launch_col(int lg, dim3 grid, size_t sm, cudaStream_t st, double2* buf, int64_t us,
+                      const UnitTable& ut, int p, int mask, const double2* ftab, const double2* chirp) {
+#define SFFT_COL(L)                                                                            \
+  case L: {                                                                                    \
+    cudaError_t e = cudaFuncSetAttribute((const void*)fft_col_kernel<L, INV>,                  \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    if (e != cudaSuccess) return (int)e;                                                       \
+    fft_col_kernel<L, INV><<<grid, FFT_T, sm, st>>>(buf, us, ut, p, mask, ftab, chirp);        \
+    break;                                                                                     \
+  }
+  switch (lg) {
+    SFFT_COL(1) SFFT_COL(2) SFFT_COL(3) SFFT_COL(4) SFFT_COL(5) SFFT_COL(6)
+    SFFT_COL(7) SFFT_COL(8) SFFT_COL(9) SFFT_COL(10) SFFT_COL(11) SFFT_COL(12)
+    default: return -22;
+  }
+#undef SFFT_COL
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+template <int MODE>
+static int launch_row(int lg, unsigned blocks, size_t sm, cudaStream_t st, double2* buf, int64_t us,
+                      const UnitTable& ut, int p, int total_rows, const double2* ftab,
+                      const double2* bhat, const double2* chirp) {
+#define SFFT_ROW(L)                                                                            \
+  case L: {                                                                                    \
+    cudaError_t e = cudaFuncSetAttribute((const void*)fft_row_kernel<L, MODE>,                 \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    if (e != cudaSuccess) return (int)e;                                                       \
+    fft_row_kernel<L, MODE><<<blocks, FFT_T, sm, st>>>(buf, us, ut, p, total_rows, ftab, bhat,  \
+                                                       chirp);                                 \
+    break;                                                                                     \
+  }
+  switch (lg) {
+    SFFT_ROW(4) SFFT_ROW(5) SFFT_ROW(6) SFFT_ROW(7) SFFT_ROW(8)
+    SFFT_ROW(9) SFFT_ROW(10) SFFT_ROW(11) SFFT_ROW(12)
+    default: return -22;
+  }
+#undef SFFT_ROW
+  SFFT_CHECK_LAUNCH();
+  return 0;
 }
 
 static size_t fft_smem_bytes(int rows_len) {
@@ -236,23 +290,14 @@ int launch_lattice_tables(const LatTable& lt, double2* tw, double2* chirp, cudaS
   return 0;
 }
 
-static int set_smem(const void* fn, size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  return (int)e;
-}
-
 // forward passes on `nunits` buffers (column pass if P1 > 1, then row pass in `mode`)
 static int run_forward_cols(double2* buf, int64_t ustride, const UnitTable& ut, int p, int mask,
                             const double2* ftab, const double2* chirp, cudaStream_t st) {
   const FftGeom g = fft_geom(p);
   if (g.P1 == 1) return 0;
   const size_t sm = fft_smem_bytes(g.P1);
-  int rc = set_smem((const void*)fft_col_kernel<false>, sm);
-  if (rc) return rc;
   dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
-  fft_col_kernel<false><<<grid, FFT_T, sm, st>>>(buf, ustride, ut, p, mask, ftab, chirp);
-  SFFT_CHECK_LAUNCH();
-  return 0;
+  return launch_col<false>(g.p1, grid, sm, st, buf, ustride, ut, p, mask, ftab, chirp);
 }
 
 int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
@@ -270,14 +315,10 @@ int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
   int rc = run_forward_cols(bhat, P, ut, p, 0, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.P2);
-  rc = set_smem((const void*)fft_row_kernel<1>, sm);
-  if (rc) return rc;
   const int total_rows = ut.nunits * g.P1;
   const int rows = FFT_E / g.P2;
-  fft_row_kernel<1><<<(total_rows + rows - 1) / rows, FFT_T, sm, st>>>(bhat, P, ut, p, total_rows,
-                                                                       ftab, nullptr, chirp);
-  SFFT_CHECK_LAUNCH();
-  return 0;
+  return launch_row<1>(g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, p, total_rows,
+                       ftab, nullptr, chirp);
 }
 
 int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ftab,
@@ -287,22 +328,17 @@ int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ft
   int rc = run_forward_cols(buf, P, ut, p, 1, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.P2);
-  rc = set_smem((const void*)fft_row_kernel<0>, sm);
-  if (rc) return rc;
   const int total_rows = ut.nunits * g.P1;
   const int rows = FFT_E / g.P2;
-  fft_row_kernel<0><<<(total_rows + rows - 1) / rows, FFT_T, sm, st>>>(buf, P, ut, p, total_rows,
-                                                                       ftab, bhat, chirp);
-  SFFT_CHECK_LAUNCH();
+  rc = launch_row<0>(g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, p, total_rows, ftab,
+                     bhat, chirp);
+  if (rc) return rc;
   if (g.P1 > 1) {
     const size_t smc = fft_smem_bytes(g.P1);
-    rc = set_smem((const void*)fft_col_kernel<true>, smc);
-    if (rc) return rc;
     dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
-    fft_col_kernel<true><<<grid, FFT_T, smc, st>>>(buf, P, ut, p, 0, ftab, chirp);
-    SFFT_CHECK_LAUNCH();
+    rc = launch_col<true>(g.p1, grid, smc, st, buf, P, ut, p, 0, ftab, chirp);
   }
-  return 0;
+  return rc;
 }
 
 }  // namespace sfft

@@ -53,7 +53,9 @@ struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
 template <>
 struct Log2<1> { static constexpr int v = 0; };
 
-// Radix-R DFT in registers, natural order in and out.
+// Radix-R DFT in registers (decimation in frequency): natural order in,
+// X[k] left in v[bitrev(k)] (callers index the outputs through bitrev_small,
+// a compile-time permutation, so no register shuffle is needed).
 template <int R, bool INV>
 __device__ __forceinline__ void dft_reg(double2* v) {
 #pragma unroll
@@ -68,11 +70,6 @@ __device__ __forceinline__ void dft_reg(double2* v) {
       }
     }
   }
-  double2 t[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) t[bitrev_small(i, Log2<R>::v)] = v[i];
-#pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = t[i];
 }
 
 // One Stockham radix-R pass over `rows` rows of length N (all in smem).
@@ -98,9 +95,19 @@ __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride,
 #pragma unroll
       for (int r = 0; r < R; ++r) v[q][r] = s[base + fpad(j + r * per_row)];
       if (Ns > 1) {
+        // w^r for r < R from two table entries (w^1, w^4): few live registers
+        const double2 w1 = __ldg(&twN[k * tstep]);
+        double2 wl[4];
+        wl[0] = make_double2(1.0, 0.0);
+        wl[1] = w1;
+        if (R > 2) { wl[2] = cmul(w1, w1); wl[3] = cmul(wl[2], w1); }
+        double2 w4 = make_double2(1.0, 0.0);
+        if (R > 4) w4 = __ldg(&twN[4 * k * tstep]);
+        double2 wh = make_double2(1.0, 0.0);
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          const double2 w = __ldg(&twN[r * k * tstep]);
+          if ((r & 3) == 0) wh = (r == 4) ? w4 : cmul(wh, w4);
+          const double2 w = (r & 3) == 0 ? wh : ((r < 4) ? wl[r & 3] : cmul(wh, wl[r & 3]));
           v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
         }
       }
@@ -116,36 +123,29 @@ __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride,
       const int row = b / per_row;
       const int idx0 = obase[q] - row * rstride;
 #pragma unroll
-      for (int r = 0; r < R; ++r) s[row * rstride + fpad(idx0 + r * Ns)] = v[q][r];
+      for (int r = 0; r < R; ++r)
+        s[row * rstride + fpad(idx0 + r * Ns)] = v[q][bitrev_small(r, Log2<R>::v)];
     }
   }
   __syncthreads();
 }
 
-// Full Stockham FFT of `rows` rows of length N = 2^logN (natural order in/out).
-// Radix-16 passes first, one smaller pass last.
-template <bool INV>
-__device__ __forceinline__ void block_fft(double2* s, int rows, int rstride, int logN,
-                                          const double2* __restrict__ twN) {
-  const int N = 1 << logN;
-  int Ns = 1;
-  int done = 0;
-  while (done < logN) {
-    const int rem = logN - done;
-    if (rem >= 4) {
-      stockham_pass<16, INV>(s, rows, rstride, N, Ns, twN);
-      Ns <<= 4; done += 4;
-    } else if (rem == 3) {
-      stockham_pass<8, INV>(s, rows, rstride, N, Ns, twN);
-      Ns <<= 3; done += 3;
-    } else if (rem == 2) {
-      stockham_pass<4, INV>(s, rows, rstride, N, Ns, twN);
-      Ns <<= 2; done += 2;
-    } else {
-      stockham_pass<2, INV>(s, rows, rstride, N, Ns, twN);
-      Ns <<= 1; done += 1;
-    }
+// Full Stockham FFT of FFT_E >> LOGN rows of length 2^LOGN (natural order
+// in/out), fully unrolled at compile time: radix-16 passes first, one
+// smaller pass last.
+template <int LOGN, int DONE, bool INV>
+__device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ twN) {
+  if constexpr (DONE < LOGN) {
+    constexpr int REM = LOGN - DONE;
+    constexpr int RB = REM >= 4 ? 4 : REM;
+    stockham_pass<(1 << RB), INV>(s, FFT_E >> LOGN, fft_rstride(1 << LOGN), 1 << LOGN, 1 << DONE, twN);
+    fft_passes<LOGN, DONE + RB, INV>(s, twN);
   }
+}
+
+template <int LOGN, bool INV>
+__device__ __forceinline__ void block_fft(double2* s, const double2* __restrict__ twN) {
+  fft_passes<LOGN, 0, INV>(s, twN);
 }
 
 }  // namespace sfft

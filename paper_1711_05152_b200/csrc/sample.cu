@@ -60,14 +60,40 @@ __global__ void poly_residue_kernel(const int32_t* __restrict__ hf, int s, LatTa
 constexpr int PT = 64;  // output tile edge (j1 and j2)
 constexpr int KC = 16;  // terms per shared-memory stage
 
-template <bool FAST>
+// (x mod m) for any x < 2^64 by Barrett reduction with mu = floor((2^64-1)/m):
+// the quotient estimate is low by at most one, so one correction is exact.
+// Integer pipe only (keeps the FP64 pipe for the contraction).
+__device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t m, uint64_t mu) {
+  const uint64_t q = __umul64hi(x, mu);
+  uint64_t r = x - q * (uint64_t)m;
+  if (r >= m) r -= m;
+  return (uint32_t)r;
+}
+
+// Twiddle w^n = e^{2 pi i n / M} from the two shared-memory tables of the
+// CTA's lattice: w^n = Thi[n >> bl] * Tlo[n & (2^bl - 1)].
+__device__ __forceinline__ double2 tw2(const double2* __restrict__ tlo, const double2* __restrict__ thi,
+                                       uint32_t n, int bl) {
+  return cmul(thi[n >> bl], tlo[n & ((1u << bl) - 1u)]);
+}
+
+// One CTA = one 64 x 64 tile (j1, j2) of one unit and one slice of the terms.
+// Warp w covers j1 in [8 (w & 1), +8) + 16 a and j2 in [4 (w >> 1), +4) + 16 b
+// so every shared-memory operand load of a warp is served by one wavefront.
+// SPLIT: write the unchirped partial sum of this term slice to `part`
+// (reduced in slice order by poly_split_reduce_kernel, deterministic).
+template <bool SPLIT>
 __global__ void __launch_bounds__(256, 2)
 sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
                    const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
                    const double2* __restrict__ tw, const double2* __restrict__ chirp,
-                   double2* __restrict__ buf, int64_t ustride, int apply_chirp) {
-  __shared__ double2 As[KC][PT];
-  __shared__ double2 Bs[KC][PT];
+                   double2* __restrict__ buf, int64_t ustride, int apply_chirp,
+                   double2* __restrict__ part, int64_t pstride) {
+  extern __shared__ double2 sm[];
+  double2* As = sm;                  // [KC][PT]
+  double2* Bs = sm + KC * PT;        // [KC][PT]
+  double2* tlo = sm + 2 * KC * PT;   // [2^bl]
+  double2* thi = tlo + (1 << pp.bl); // [nhi]
   const int bid = blockIdx.x;
   int lo = 0, hi = pp.nunits - 1;
   while (lo < hi) {
@@ -76,19 +102,34 @@ sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
   }
   const int u = lo;
   const int l = pp.unit_lat[u], it = pp.unit_it[u];
-  const int tau = bid - pp.tile_start[u];
+  const int local = bid - pp.tile_start[u];
+  const int q = local % pp.ks;
+  const int tau = local / pp.ks;
   const int nt1 = pp.nt1[l];
   const int tj1 = tau % nt1, tj2 = tau / nt1;
   const int64_t M = lt.m[l];
-  const double invM = lt.inv_m[l];
+  const uint32_t M32 = (uint32_t)M;
+  const uint64_t mu = pp.mu[l];
+  const int bl = pp.bl;
   const int64_t J1 = pp.J1[l];
-  const int64_t j1_0 = (int64_t)tj1 * PT, j2_0 = (int64_t)tj2 * PT;
+  const uint32_t j1_0 = (uint32_t)tj1 * PT, j2_0 = (uint32_t)tj2 * PT;
   const double2* twl = tw + lt.off[l];
   const int s = pp.s;
+  const int h_begin = q * pp.kper;
+  const int h_end = min(s, h_begin + pp.kper);
   const double2* cp = cprime + (int64_t)it * s;
   const int32_t* rr = rres + (int64_t)l * s;
   const int32_t* rj = rjs + (int64_t)l * s;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+
+  // stage this lattice's two-level twiddle tables
+  const int nlo = 1 << bl;
+  const int nhi = (int)((M + nlo - 1) >> bl);
+  for (int i = threadIdx.x; i < nlo; i += 256) tlo[i] = __ldg(&twl[i < M ? i : 0]);
+  for (int i = threadIdx.x; i < nhi; i += 256) thi[i] = __ldg(&twl[(int64_t)i << bl]);
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = (lane & 7) + 8 * (w & 1);
+  const int ty = (lane >> 3) + 4 * (w >> 1);
 
   double2 acc[4][4];
 #pragma unroll
@@ -96,52 +137,70 @@ sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
 
-  for (int k0 = 0; k0 < s; k0 += KC) {
+  for (int k0 = h_begin; k0 < h_end; k0 += KC) {
+    __syncthreads();  // tables staged / previous stage consumed
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int idx = threadIdx.x + e * 256;
       const int kk = idx >> 6, jj = idx & 63;
       const int h = k0 + kk;
       double2 a = make_double2(0.0, 0.0), b = make_double2(1.0, 0.0);
-      if (h < s) {
-        const int64_t r = __ldg(&rr[h]);
-        const int64_t na = mulmod<FAST>(r, j1_0 + jj, M, invM);
-        a = cmul(__ldg(&cp[h]), __ldg(&twl[na]));
-        const int64_t q = __ldg(&rj[h]);
-        const int64_t nb = mulmod<FAST>(q, j2_0 + jj, M, invM);
-        b = __ldg(&twl[nb]);
+      if (h < h_end) {
+        const uint32_t r = (uint32_t)__ldg(&rr[h]);
+        const uint32_t na = mod_barrett((uint64_t)r * (j1_0 + jj), M32, mu);
+        a = cmul(__ldg(&cp[h]), tw2(tlo, thi, na, bl));
+        const uint32_t qq = (uint32_t)__ldg(&rj[h]);
+        const uint32_t nb = mod_barrett((uint64_t)qq * (j2_0 + jj), M32, mu);
+        b = tw2(tlo, thi, nb, bl);
       }
-      As[kk][jj] = a;
-      Bs[kk][jj] = b;
+      As[kk * PT + jj] = a;
+      Bs[kk * PT + jj] = b;
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
-      double2 a[4], b[4];
+      double2 b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = As[kk][tx + 16 * i]; b[i] = Bs[kk][ty + 16 * i]; }
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk * PT + ty + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        const double2 a = As[kk * PT + tx + 16 * i];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          acc[i][j].x = fma(a[i].x, b[j].x, acc[i][j].x);
-          acc[i][j].x = fma(-a[i].y, b[j].y, acc[i][j].x);
-          acc[i][j].y = fma(a[i].x, b[j].y, acc[i][j].y);
-          acc[i][j].y = fma(a[i].y, b[j].x, acc[i][j].y);
+          acc[i][j].x = fma(a.x, b[j].x, acc[i][j].x);
+          acc[i][j].x = fma(-a.y, b[j].y, acc[i][j].x);
+          acc[i][j].y = fma(a.x, b[j].y, acc[i][j].y);
+          acc[i][j].y = fma(a.y, b[j].x, acc[i][j].y);
         }
+      }
     }
-    __syncthreads();
   }
   const double2* ch = chirp + lt.off[l];
-  double2* ub = buf + (int64_t)u * ustride;
+  double2* ub = SPLIT ? part + ((int64_t)q * pp.nunits + u) * pstride : buf + (int64_t)u * ustride;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int64_t base = J1 * (j2_0 + ty + 16 * j);
+    const int64_t base = J1 * (int64_t)(j2_0 + ty + 16 * j);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t n = j1_0 + tx + 16 * i + base;
-      if (n < M) ub[n] = apply_chirp ? cmul(acc[i][j], __ldg(&ch[n])) : acc[i][j];
+      if (n < M) ub[n] = (!SPLIT && apply_chirp) ? cmul(acc[i][j], __ldg(&ch[n])) : acc[i][j];
     }
+  }
+}
+
+// sum the term slices of every unit in slice order, then pre-chirp
+__global__ void poly_split_reduce_kernel(UnitTable ut, int ks, const double2* __restrict__ part,
+                                         int64_t pstride, const double2* __restrict__ chirp,
+                                         double2* __restrict__ buf, int64_t ustride, int apply_chirp) {
+  const int u = blockIdx.y;
+  const int l = ut.lat[u];
+  const int64_t M = ut.m[l];
+  const double2* ch = chirp + ut.off[l];
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = part[(int64_t)u * pstride + n];
+    for (int q = 1; q < ks; ++q) v = cadd(v, part[((int64_t)q * ut.nunits + u) * pstride + n]);
+    buf[(int64_t)u * ustride + n] = apply_chirp ? cmul(v, __ldg(&ch[n])) : v;
   }
 }
 
@@ -280,19 +339,43 @@ int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, co
   return 0;
 }
 
-int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
-                       const int32_t* rres, const int32_t* rj, const double2* tw,
-                       const double2* chirp, double2* buf, int64_t ustride, bool fast,
-                       bool apply_chirp, cudaStream_t st) {
-  const int tiles = pp.tile_start[pp.nunits];
-  if (tiles <= 0) return 0;
-  if (fast)
-    sample_poly_kernel<true><<<tiles, 256, 0, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
-                                                    ustride, apply_chirp ? 1 : 0);
-  else
-    sample_poly_kernel<false><<<tiles, 256, 0, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
-                                                     ustride, apply_chirp ? 1 : 0);
-  SFFT_CHECK_LAUNCH();
+size_t sample_poly_smem(int bl, int64_t mmax) {
+  const int64_t nlo = (int64_t)1 << bl;
+  const int64_t nhi = (mmax + nlo - 1) / nlo;
+  return (size_t)(2 * KC * PT + nlo + nhi) * sizeof(double2);
+}
+
+int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& ut,
+                       const double2* cprime, const int32_t* rres, const int32_t* rj,
+                       const double2* tw, const double2* chirp, double2* buf, int64_t ustride,
+                       bool apply_chirp, double2* part, int64_t pstride, int num_sms,
+                       cudaStream_t st) {
+  const int ctas = pp.tile_start[pp.nunits];
+  if (ctas <= 0) return 0;
+  int64_t mmax = 1;
+  for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
+  const size_t smem = sample_poly_smem(pp.bl, mmax);
+  if (pp.ks > 1) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    sample_poly_kernel<true><<<ctas, 256, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+                                                      ustride, apply_chirp ? 1 : 0, part, pstride);
+    SFFT_CHECK_LAUNCH();
+    int bx = (int)((mmax + 255) / 256);
+    const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
+    if (bx > cap) bx = cap;
+    poly_split_reduce_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, pp.ks, part, pstride, chirp,
+                                                                  buf, ustride, apply_chirp ? 1 : 0);
+    SFFT_CHECK_LAUNCH();
+  } else {
+    cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    sample_poly_kernel<false><<<ctas, 256, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+                                                       ustride, apply_chirp ? 1 : 0, nullptr, 0);
+    SFFT_CHECK_LAUNCH();
+  }
   return 0;
 }
 

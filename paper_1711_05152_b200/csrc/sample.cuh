@@ -14,11 +14,15 @@ struct AnchorTable {
 struct PolyPlan {
   int nunits;
   int s;
+  int bl;    // low bits of the two-level twiddle tables
+  int ks;    // term slices per tile (K split)
+  int kper;  // terms per slice (multiple of 16)
   int unit_lat[SFFT_UMAX];
   int unit_it[SFFT_UMAX];
-  int tile_start[SFFT_UMAX + 1];
+  int tile_start[SFFT_UMAX + 1];  // CTA prefix over units (tiles * ks)
   int J1[SFFT_LMAX];
   int nt1[SFFT_LMAX];
+  uint64_t mu[SFFT_LMAX];         // Barrett constants floor((2^64-1) / M_l)
 };
 
 // B-spline test function: groups of (order, component slots)
@@ -34,10 +38,12 @@ struct BsplineSpec {
 int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, const LatTable& lt,
                         const PolyPlan& pp, const AnchorTable& at, double2* cprime, int32_t* rres,
                         int32_t* rj, cudaStream_t st);
-int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
-                       const int32_t* rres, const int32_t* rj, const double2* tw,
-                       const double2* chirp, double2* buf, int64_t ustride, bool fast,
-                       bool apply_chirp, cudaStream_t st);
+int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& ut,
+                       const double2* cprime, const int32_t* rres, const int32_t* rj,
+                       const double2* tw, const double2* chirp, double2* buf, int64_t ustride,
+                       bool apply_chirp, double2* part, int64_t pstride, int num_sms,
+                       cudaStream_t st);
+size_t sample_poly_smem(int bl, int64_t mmax);
 int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
                           const AnchorTable& at, const double2* chirp, double2* buf,
                           int64_t ustride, bool fast, bool apply_chirp, int num_sms,

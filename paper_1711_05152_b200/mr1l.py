@@ -244,9 +244,12 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
             cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
             rres = dev.empty((L, max(s, 1)), torch.int32)
             rj = dev.empty((L, max(s, 1)), torch.int32)
+            need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s))
+            part = dev.empty((max(need, 1), 2), torch.float64)
             dev.call("sfft_sample_poly", dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
                      hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
-                     dptr(tabs.chirp), dptr(buf), P, chirp_now, ctx=f"sampling, step {step}")
+                     dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0),
+                     ctx=f"sampling, step {step}")
         else:
             order, start, comps, scale = base.host_spec()
             dev.call("sfft_sample_bspline", len(base.groups), hptr(order), hptr(start), hptr(comps),
