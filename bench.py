@@ -271,15 +271,27 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = world * n / (ms_step * 1e-3)
 
-    # per-stage breakdown + roofline of the dominant kernel (sampling, FP64-bound)
+    # per-stage breakdown + per-kernel-class device times (CUDA events recorded
+    # by the library around each class on the launching stream)
+    import ctypes
     timer = StageTimer(dev)
-    for _ in range(3):
+    _native.query("sfft_profile_enable", 1)
+    nprof = 3
+    for _ in range(nprof):
         flush.zero_()
         sch, res = step(timer)
+    dev.sync()
+    kernels = {}
+    for cls, name in enumerate(("sample_poly", "bluestein_fft", "alias", "gather")):
+        tot = ctypes.c_double(0.0)
+        cnt = ctypes.c_int(0)
+        _native.call("sfft_profile_collect", cls, ctypes.addressof(tot), ctypes.addressof(cnt))
+        kernels[name] = tot.value / max(cnt.value, 1)
+    _native.query("sfft_profile_enable", 0)
     stages = {k: float(np.mean(v)) for k, v in timer.totals_ms().items()}
     s_terms = wl.oracle.s
     flops = 8.0 * s_terms * sch.total_size
-    achieved = flops / (stages["sample"] * 1e-3) / 1e12
+    achieved = flops / (kernels["sample_poly"] * 1e-3) / 1e12
     traffic = load_traffic()
 
     # end to end through the public API with host buffers
@@ -337,7 +349,11 @@ def run_ours(args):
                    "l2": "flushed (256 MB write) before every timed step",
                    "parallelism": f"{world} independent step streams (weak scaling)" if world > 1 else "1 GPU"},
         "stages_ms": stages,
-        "roofline": {"bound": "fp64", "kernel": "sample_poly (K1, GEMM-factored DFMA)",
+        "kernels_ms": kernels,
+        "kernel_share_of_step": kernels["sample_poly"] / ms_step,
+        "roofline": {"bound": "fp64", "kernel": "sample_poly_kernel (K1, GEMM-factored DFMA)",
+                     "timing": "CUDA events around the kernel launch on its stream (sfft_profile_*), "
+                               f"mean of {nprof} launches",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": "measured in this run: register-resident DFMA loop (sfft_fp64_peak)",
                      "algorithmic": f"8 flop x {s_terms} terms x {sch.total_size} nodes per launch",

@@ -38,6 +38,13 @@ extern "C" {
 int sfft_abi_version(void);
 /* kernels launched by this library since load (all devices, all streams) */
 long long sfft_launch_count(void);
+/* CUDA-event timing of kernel classes on their launching stream:
+ * 0 = polynomial sampling GEMM (K1), 1 = Bluestein FFT passes (K2),
+ * 2 = alias histogram + masks (K3), 3 = gather/average/threshold (K4).
+ * enable(1) clears the record; collect() synchronises and returns the summed
+ * device time and launch count of one class since the last collect. */
+int sfft_profile_enable(int on);
+int sfft_profile_collect(int cls, double* total_ms, int* count);
 const char* sfft_error_string(int code);
 /* number of SMs and compute capability of the current device */
 int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);

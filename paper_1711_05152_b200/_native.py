@@ -20,6 +20,8 @@ _int = C.c_int
 _SIGS = {
     "sfft_abi_version": (_int, []),
     "sfft_launch_count": (C.c_longlong, []),
+    "sfft_profile_enable": (_int, [_int]),
+    "sfft_profile_collect": (_int, [_int, _vp, _vp]),
     "sfft_error_string": (C.c_char_p, [_int]),
     "sfft_device_info": (_int, [_vp, _vp, _vp]),
     "sfft_alias_scratch_words": (_i64, [_vp, _int]),

@@ -109,8 +109,10 @@ template <int DM, bool FAST>
 static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
                            int64_t words, uint64_t* masks, int32_t* stats, int blocks,
                            cudaStream_t st) {
+  prof_mark(PROF_ALIAS, true, st);
   alias_mark_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits, bits + words / 2, words);
   alias_mask_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits + words / 2, masks, stats);
+  prof_mark(PROF_ALIAS, false, st);
 }
 
 int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,

@@ -3,6 +3,9 @@
 #include <math.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "../../include/sfft_b200.h"
 #include "common.cuh"
 #include "gather.cuh"
@@ -21,6 +24,47 @@ int launch_add_noise(double2* x, const double2* e, int64_t n, double scale, int 
 }
 
 using namespace sfft;
+
+// ---------------------------------------------------------------------------
+// kernel-class event profiling
+namespace {
+constexpr int PROF_RING = 4096;
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  cudaEvent_t ev[PROF_NCLASS][PROF_RING][2];
+  bool made[PROF_NCLASS][PROF_RING];
+  int n[PROF_NCLASS];
+  int open[PROF_NCLASS];
+};
+ProfState& prof() {
+  static ProfState* p = [] {
+    auto* q = new ProfState;
+    memset(q->made, 0, sizeof(q->made));
+    memset(q->n, 0, sizeof(q->n));
+    memset(q->open, 0, sizeof(q->open));
+    return q;
+  }();
+  return *p;
+}
+}  // namespace
+
+namespace sfft {
+void prof_mark(int cls, bool begin, cudaStream_t st) {
+  ProfState& p = prof();
+  if (!p.on) return;
+  std::lock_guard<std::mutex> g(p.mu);
+  int i = p.n[cls];
+  if (i >= PROF_RING) return;
+  if (!p.made[cls][i]) {
+    cudaEventCreate(&p.ev[cls][i][0]);
+    cudaEventCreate(&p.ev[cls][i][1]);
+    p.made[cls][i] = true;
+  }
+  cudaEventRecord(p.ev[cls][i][begin ? 0 : 1], st);
+  if (!begin) p.n[cls] = i + 1;
+}
+}  // namespace sfft
 
 namespace {
 
@@ -118,8 +162,31 @@ int fill_bspline(BsplineSpec& bs, int ngroups, const int32_t* h_order, const int
   return 0;
 }
 
-// J1 (multiple of 64) minimising the padded tile count J1 * 64 * ceil(J2 / 64)
+// J1 (multiple of 64) minimising the padded tile count J1 * 64 * ceil(J2 / 64);
+// memoised per M (the same primes recur across steps and calls)
+void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2);
+
 void choose_j1(int64_t m, int& j1, int& nt1, int& nt2) {
+  static std::mutex mu;
+  static std::unordered_map<int64_t, int> memo;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto itr = memo.find(m);
+    if (itr != memo.end()) {
+      j1 = itr->second;
+      nt1 = j1 / 64;
+      const int64_t J2 = (m + j1 - 1) / j1;
+      nt2 = (int)((J2 + 63) / 64);
+      return;
+    }
+  }
+  choose_j1_search(m, j1, nt1, nt2);
+  std::lock_guard<std::mutex> g(mu);
+  if (memo.size() > 65536) memo.clear();
+  memo[m] = j1;
+}
+
+void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2) {
   int64_t best = -1;
   int bj = 64;
   const int64_t amax = (m + 63) / 64;
@@ -158,7 +225,10 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int 
   pp->bl = bl;
   const size_t smem = sample_poly_smem(bl, mmax);
   if (smem > 227 * 1024) return E_2BIG;
-  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  // resident CTAs per SM: 3 by registers (128 threads x <= 168 regs), fewer if smem-bound
+  int per_sm = (int)((228 * 1024) / (smem + 1024));
+  if (per_sm > 3) per_sm = 3;
+  if (per_sm < 1) per_sm = 1;
   int64_t tiles_l[SFFT_LMAX];
   int64_t tiles_total = 0;
   for (int l = 0; l < L; ++l) {
@@ -209,6 +279,33 @@ extern "C" {
 int sfft_abi_version(void) { return SFFT_B200_ABI_VERSION; }
 
 long long sfft_launch_count(void) { return g_launches.load(); }
+
+int sfft_profile_enable(int on) {
+  ProfState& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.on = on != 0;
+  memset(p.n, 0, sizeof(p.n));
+  return 0;
+}
+
+int sfft_profile_collect(int cls, double* total_ms, int* count) {
+  if (cls < 0 || cls >= PROF_NCLASS) return E_INVAL;
+  ProfState& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  double tot = 0.0;
+  for (int i = 0; i < p.n[cls]; ++i) {
+    cudaError_t e = cudaEventSynchronize(p.ev[cls][i][1]);
+    if (e != cudaSuccess) return (int)e;
+    float ms = 0.f;
+    e = cudaEventElapsedTime(&ms, p.ev[cls][i][0], p.ev[cls][i][1]);
+    if (e != cudaSuccess) return (int)e;
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = p.n[cls];
+  p.n[cls] = 0;
+  return 0;
+}
 
 const char* sfft_error_string(int code) {
   if (code == 0) return "ok";

@@ -20,6 +20,11 @@ namespace sfft {
 // number of kernels this library has launched (reported by sfft_launch_count)
 inline std::atomic<long long> g_launches{0};
 
+// Optional CUDA-event brackets around kernel classes (sfft_profile_enable):
+// the bench reads each class's device time on the launching stream.
+enum ProfClass { PROF_SAMPLE = 0, PROF_FFT = 1, PROF_ALIAS = 2, PROF_GATHER = 3, PROF_NCLASS = 4 };
+void prof_mark(int cls, bool begin, cudaStream_t st);  // no-op unless enabled
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }

@@ -325,6 +325,7 @@ int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ft
                      const double2* bhat, const double2* chirp, cudaStream_t st) {
   const FftGeom g = fft_geom(p);
   const int64_t P = g.P;
+  prof_mark(PROF_FFT, true, st);
   int rc = run_forward_cols(buf, P, ut, p, 1, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.P2);
@@ -338,6 +339,7 @@ int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ft
     dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
     rc = launch_col<true>(g.p1, grid, smc, st, buf, P, ut, p, 0, ftab, chirp);
   }
+  prof_mark(PROF_FFT, false, st);
   return rc;
 }
 

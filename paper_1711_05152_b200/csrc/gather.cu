@@ -102,6 +102,7 @@ static int launch_gather_t(const int32_t* freqs, int64_t n, const LatTable& lt,
                            const uint64_t* masks, const double2* buf, int64_t ustride, int rb,
                            int it0, double delta, double2* coef, uint8_t* keep, int32_t* counts,
                            int blocks, cudaStream_t st) {
+  prof_mark(PROF_GATHER, true, st);
   if (rb <= 1)
     gather_kernel<DM, FAST, 1><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf, ustride, rb, it0,
                                                        delta, coef, keep, counts);
@@ -113,6 +114,7 @@ static int launch_gather_t(const int32_t* freqs, int64_t n, const LatTable& lt,
                                                        delta, coef, keep, counts);
   else
     return -22;
+  prof_mark(PROF_GATHER, false, st);
   SFFT_CHECK_LAUNCH();
   return 0;
 }

@@ -59,6 +59,7 @@ __global__ void poly_residue_kernel(const int32_t* __restrict__ hf, int s, LatTa
 
 constexpr int PT = 64;  // output tile edge (j1 and j2)
 constexpr int KC = 16;  // terms per shared-memory stage
+constexpr int SP_T = 256;  // threads per sampling CTA
 
 // (x mod m) for any x < 2^64 by Barrett reduction with mu = floor((2^64-1)/m):
 // the quotient estimate is low by at most one, so one correction is exact.
@@ -77,22 +78,23 @@ __device__ __forceinline__ double2 tw2(const double2* __restrict__ tlo, const do
   return cmul(thi[n >> bl], tlo[n & ((1u << bl) - 1u)]);
 }
 
-// One CTA = one 64 x 64 tile (j1, j2) of one unit and one slice of the terms.
-// Warp w covers j1 in [8 (w & 1), +8) + 16 a and j2 in [4 (w >> 1), +4) + 16 b
-// so every shared-memory operand load of a warp is served by one wavefront.
+// One CTA (256 threads) = one 64 x 64 tile (j1, j2) of one unit and one
+// slice of the terms; thread tile 4 x 4 complex (j1 = tx + 16 i, j2 = ty + 16 j).
+// Operand tiles are double-buffered in shared memory: each stage is generated
+// (integer Barrett, two-level table lookups, recurrences) while the other is
+// contracted, with one barrier per stage.
 // SPLIT: write the unchirped partial sum of this term slice to `part`
 // (reduced in slice order by poly_split_reduce_kernel, deterministic).
 template <bool SPLIT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(SP_T, 2)
 sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
                    const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
                    const double2* __restrict__ tw, const double2* __restrict__ chirp,
                    double2* __restrict__ buf, int64_t ustride, int apply_chirp,
                    double2* __restrict__ part, int64_t pstride) {
   extern __shared__ double2 sm[];
-  double2* As = sm;                  // [KC][PT]
-  double2* Bs = sm + KC * PT;        // [KC][PT]
-  double2* tlo = sm + 2 * KC * PT;   // [2^bl]
+  // two stages of operand tiles: stage b at sm + b * 2 * KC * PT = {A[KC][PT], B[KC][PT]}
+  double2* tlo = sm + 4 * KC * PT;   // [2^bl]
   double2* thi = tlo + (1 << pp.bl); // [nhi]
   const int bid = blockIdx.x;
   int lo = 0, hi = pp.nunits - 1;
@@ -124,8 +126,8 @@ sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
   // stage this lattice's two-level twiddle tables
   const int nlo = 1 << bl;
   const int nhi = (int)((M + nlo - 1) >> bl);
-  for (int i = threadIdx.x; i < nlo; i += 256) tlo[i] = __ldg(&twl[i < M ? i : 0]);
-  for (int i = threadIdx.x; i < nhi; i += 256) thi[i] = __ldg(&twl[(int64_t)i << bl]);
+  for (int i = threadIdx.x; i < nlo; i += SP_T) tlo[i] = __ldg(&twl[i < M ? i : 0]);
+  for (int i = threadIdx.x; i < nhi; i += SP_T) thi[i] = __ldg(&twl[(int64_t)i << bl]);
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tx = (lane & 7) + 8 * (w & 1);
@@ -137,26 +139,73 @@ sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
 
-  for (int k0 = h_begin; k0 < h_end; k0 += KC) {
-    __syncthreads();  // tables staged / previous stage consumed
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = threadIdx.x + e * 256;
-      const int kk = idx >> 6, jj = idx & 63;
-      const int h = k0 + kk;
-      double2 a = make_double2(0.0, 0.0), b = make_double2(1.0, 0.0);
-      if (h < h_end) {
-        const uint32_t r = (uint32_t)__ldg(&rr[h]);
-        const uint32_t na = mod_barrett((uint64_t)r * (j1_0 + jj), M32, mu);
-        a = cmul(__ldg(&cp[h]), tw2(tlo, thi, na, bl));
-        const uint32_t qq = (uint32_t)__ldg(&rj[h]);
-        const uint32_t nb = mod_barrett((uint64_t)qq * (j2_0 + jj), M32, mu);
-        b = tw2(tlo, thi, nb, bl);
-      }
-      As[kk * PT + jj] = a;
-      Bs[kk * PT + jj] = b;
+  // Operand generation, term-major: the 16 threads of term gh produce rows
+  // gt + 16 i of A and B from one table lookup each plus a recurrence by
+  // w^{16 r} (3 complex multiplications, a few ulp).
+  const int gh = threadIdx.x >> 4, gt = threadIdx.x & 15;
+  uint32_t pr = 0, pq = 0;
+  double2 pc = make_double2(0.0, 0.0);
+  auto fetch = [&](int k0) {
+    const int h = k0 + gh;
+    if (h < h_end) {
+      pr = (uint32_t)__ldg(&rr[h]);
+      pq = (uint32_t)__ldg(&rj[h]);
+      pc = __ldg(&cp[h]);
     }
-    __syncthreads();
+  };
+  // generation state of the stage being produced
+  double2 gv = make_double2(0.0, 0.0), ge = make_double2(1.0, 0.0);
+  auto gen_start_a = [&](bool live) {
+    gv = make_double2(0.0, 0.0);
+    ge = make_double2(1.0, 0.0);
+    if (live) {
+      gv = cmul(pc, tw2(tlo, thi, mod_barrett((uint64_t)pr * (j1_0 + gt), M32, mu), bl));
+      ge = tw2(tlo, thi, mod_barrett((uint64_t)pr * 16u, M32, mu), bl);
+    }
+  };
+  auto gen_start_b = [&](bool live) {
+    gv = make_double2(1.0, 0.0);
+    ge = make_double2(1.0, 0.0);
+    if (live) {
+      gv = tw2(tlo, thi, mod_barrett((uint64_t)pq * (j2_0 + gt), M32, mu), bl);
+      ge = tw2(tlo, thi, mod_barrett((uint64_t)pq * 16u, M32, mu), bl);
+    }
+  };
+  auto gen_put = [&](double2* dst, int i) {
+    dst[gh * PT + gt + 16 * i] = gv;
+    if (i < 3) gv = cmul(gv, ge);
+  };
+
+  int stage = 0;
+  fetch(h_begin);
+  __syncthreads();  // tables staged
+  if (h_begin < h_end) {
+    const bool live = h_begin + gh < h_end;
+    gen_start_a(live);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gen_put(sm, i);
+    gen_start_b(live);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gen_put(sm + KC * PT, i);
+  }
+  fetch(h_begin + KC);
+  for (int k0 = h_begin; k0 < h_end; k0 += KC) {
+    __syncthreads();  // stage `stage` complete; the other stage is free
+    const double2* As = sm + stage * 2 * KC * PT;
+    const double2* Bs = As + KC * PT;
+    double2* An = sm + (stage ^ 1) * 2 * KC * PT;
+    double2* Bn = An + KC * PT;
+    const bool more = k0 + KC < h_end;
+    const bool live = more && (k0 + KC + gh < h_end);
+    if (more) {
+      gen_start_a(live);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gen_put(An, i);
+      gen_start_b(live);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gen_put(Bn, i);
+      fetch(k0 + 2 * KC);
+    }
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
       double2 b[4];
@@ -174,6 +223,7 @@ sample_poly_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
         }
       }
     }
+    stage ^= 1;
   }
   const double2* ch = chirp + lt.off[l];
   double2* ub = SPLIT ? part + ((int64_t)q * pp.nunits + u) * pstride : buf + (int64_t)u * ustride;
@@ -342,7 +392,7 @@ int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, co
 size_t sample_poly_smem(int bl, int64_t mmax) {
   const int64_t nlo = (int64_t)1 << bl;
   const int64_t nhi = (mmax + nlo - 1) / nlo;
-  return (size_t)(2 * KC * PT + nlo + nhi) * sizeof(double2);
+  return (size_t)(4 * KC * PT + nlo + nhi) * sizeof(double2);
 }
 
 int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& ut,
@@ -359,8 +409,10 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
     cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    sample_poly_kernel<true><<<ctas, 256, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+    prof_mark(PROF_SAMPLE, true, st);
+    sample_poly_kernel<true><<<ctas, SP_T, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
                                                       ustride, apply_chirp ? 1 : 0, part, pstride);
+    prof_mark(PROF_SAMPLE, false, st);
     SFFT_CHECK_LAUNCH();
     int bx = (int)((mmax + 255) / 256);
     const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
@@ -372,8 +424,10 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
     cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    sample_poly_kernel<false><<<ctas, 256, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
+    prof_mark(PROF_SAMPLE, true, st);
+    sample_poly_kernel<false><<<ctas, SP_T, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
                                                        ustride, apply_chirp ? 1 : 0, nullptr, 0);
+    prof_mark(PROF_SAMPLE, false, st);
     SFFT_CHECK_LAUNCH();
   }
   return 0;

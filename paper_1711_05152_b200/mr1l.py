@@ -197,19 +197,67 @@ class LatticeTables:
         return 1 << self.p
 
 
-def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str = "") -> LatticeTables:
+class _TableCache:
+    """LRU of per-size tables (twiddles, chirps, transformed Bluestein kernels).
+
+    They depend only on the lattice sizes M_l — like FFT plans (the
+    reference's scipy/pocketfft keeps an LRU plan cache too) — and consecutive
+    steps of a run, or repeated steps on sets of equal size, reuse the same
+    primes.  Bounded by SFFT_B200_TABLE_CACHE_BYTES (default 8 GiB per device).
+    """
+
+    def __init__(self):
+        import os
+        from collections import OrderedDict
+        self.cap = int(os.environ.get("SFFT_B200_TABLE_CACHE_BYTES", 8 << 30))
+        self.entries: "OrderedDict[tuple, tuple]" = OrderedDict()
+        self.bytes = 0
+        self.hits = 0
+        self.misses = 0
+
+    def get(self, key):
+        got = self.entries.get(key)
+        if got is not None:
+            self.entries.move_to_end(key)
+            self.hits += 1
+        return got
+
+    def put(self, key, val, nbytes: int):
+        self.misses += 1
+        if nbytes > self.cap:
+            return
+        while self.entries and self.bytes + nbytes > self.cap:
+            _, old = self.entries.popitem(last=False)
+            self.bytes -= old[-1]
+        self.entries[key] = val + (nbytes,)
+        self.bytes += nbytes
+
+
+_TABLES: dict[int, _TableCache] = {}
+
+
+def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str = "",
+                   cache: bool = True) -> LatticeTables:
     torch = dev.torch
     ms = np.ascontiguousarray(np.asarray(ms, dtype=np.int64))
     L = len(ms)
     p = fft_exponent(int(ms.max()))
+    key = (p,) + tuple(int(m) for m in ms)
+    tc = _TABLES.setdefault(dev.index, _TableCache())
+    got = tc.get(key) if cache else None
+    ftab = dev.fft_tables(p)
+    if got is not None:
+        tw, chirp, bhat, _ = got
+        return LatticeTables(ms, zs, p, tw, chirp, bhat, ftab)
     P = 1 << p
     tot = int(ms.sum())
     tw = dev.empty((tot, 2), torch.float64)
     chirp = dev.empty((tot, 2), torch.float64)
     dev.call("sfft_lattice_tables", hptr(ms), L, dptr(tw), dptr(chirp), ctx=ctx)
-    ftab = dev.fft_tables(p)
     bhat = dev.empty((L, P, 2), torch.float64)
     dev.call("sfft_bluestein_bhat", hptr(ms), L, p, dptr(ftab), dptr(chirp), dptr(bhat), ctx=ctx)
+    if cache:
+        tc.put(key, (tw, chirp, bhat), 32 * tot + 16 * L * P)
     return LatticeTables(ms, zs, p, tw, chirp, bhat, ftab)
 
 
