@@ -79,7 +79,12 @@ int sfft_fft_tables(int p, double* d_ftab, void* stream);
 int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
                         const double* d_chirp, double* d_bhat, void* stream);
 int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
-                   const double* d_bhat, const double* d_chirp, double* d_buf, void* stream);
+                   const double* d_bhat, const double* d_chirp, double* d_buf,
+                   const int32_t* h_units, int nunits, void* stream);
+
+/* Unit lists: functions taking (h_units, nunits) process the explicit units
+ * h_units[j] = it * L + l (it < rb), unit j in buffer slot j; h_units = NULL
+ * means all rb * L units in order. */
 
 /* ---- K1: sampling at lattice nodes ----------------------------------------
  * Sparse polynomial oracle (testbed.py:116-127) on the nodes of
@@ -91,14 +96,16 @@ int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_fta
  * partial sums; sfft_sample_poly_scratch() gives the size for the best
  * split, a smaller buffer selects a smaller split, 0 disables it).
  * apply_chirp = 0 leaves the raw samples. */
-int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s);
+int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s, const int32_t* h_units,
+                                 int nunits);
 int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
                      const int64_t* h_m, const int32_t* h_z, int L,
                      const double* h_anchor, int rb,
                      double* d_cprime, int32_t* d_rres, int32_t* d_rj,
                      const double* d_tw, const double* d_chirp,
                      double* d_buf, int64_t P, int apply_chirp,
-                     double* d_partial, int64_t partial_len, void* stream);
+                     double* d_partial, int64_t partial_len,
+                     const int32_t* h_units, int nunits, void* stream);
 /* B-spline oracle (testbed.py:198-244): ngroups tensor-product terms; group g
  * has spline order h_order[g] (<= 8), scale h_scale[g] = C_m * m, and the
  * component slots h_comps[h_start[g] .. h_start[g+1]). */
@@ -106,16 +113,17 @@ int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_st
                         const int32_t* h_comps, const double* h_scale, int d, int t1,
                         const int64_t* h_m, const int32_t* h_z, int L,
                         const double* h_anchor, int rb, const double* d_chirp,
-                        double* d_buf, int64_t P, int apply_chirp, void* stream);
+                        double* d_buf, int64_t P, int apply_chirp,
+                        const int32_t* h_units, int nunits, void* stream);
 /* Host-callback / noisy oracles: d_buf holds raw samples; adds
  * d_sigma[u] * d_noise[u * nstride + n] when d_noise != NULL (NoisyOracle,
  * testbed.py:100-106), then applies the pre-chirp. */
 int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp,
                         double* d_buf, int64_t P, const double* d_noise, int64_t nstride,
-                        const double* d_sigma, void* stream);
+                        const double* d_sigma, const int32_t* h_units, int nunits, void* stream);
 /* sum_n |x_n|^2 per unit over n < M (relative-SNR noise calibration). */
 int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
-                    double* d_out, void* stream);
+                    double* d_out, const int32_t* h_units, int nunits, void* stream);
 /* Node coordinates of lattice l (lattice.py:505-508 + anchor tail,
  * detect.py:294-297): d_pts is M_l x d row-major float64. */
 int sfft_lattice_nodes(const int64_t* h_m, const int32_t* h_z, int L, int t1, int l, int d,
@@ -129,6 +137,17 @@ int sfft_gather_select(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax,
                        const int64_t* h_m, const int32_t* h_z, int L,
                        const uint64_t* d_masks, const double* d_buf, int64_t P,
                        int rb, int it0, double delta,
+                       double* d_coef, uint8_t* d_keep, int32_t* d_counts, void* stream);
+/* Sharded step: per-unit dense rows of alias-free bins (out[j*n + k] =
+ * X_j[res] / M, 0 where lattice of unit j is not alias-free for k), and their
+ * lattice-ordered combination after an all-gather (h_rows[i*L + l] = row of
+ * unit (i, l) in d_vals), bit-identical to sfft_gather_select. */
+int sfft_gather_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                      const int32_t* h_z, int L, const uint64_t* d_masks, const double* d_buf,
+                      int64_t P, int rb, const int32_t* h_units, int nunits, double* d_out,
+                      void* stream);
+int sfft_combine_units(int64_t n, int L, const uint64_t* d_masks, const double* d_vals,
+                       const int32_t* h_rows, int r_total, int rb, int it0, double delta,
                        double* d_coef, uint8_t* d_keep, int32_t* d_counts, void* stream);
 /* cap selection of one iteration (detect.py:205-211) */
 int64_t sfft_select_scratch_bytes(int64_t n);

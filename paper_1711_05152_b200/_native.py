@@ -30,17 +30,19 @@ _SIGS = {
     "sfft_fft_table_len": (_i64, [_int]),
     "sfft_fft_tables": (_int, [_int, _vp, _vp]),
     "sfft_bluestein_bhat": (_int, [_vp, _int, _int, _vp, _vp, _vp, _vp]),
-    "sfft_bluestein": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
-    "sfft_sample_poly_scratch": (_i64, [_vp, _int, _int, _int]),
+    "sfft_bluestein": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp]),
+    "sfft_sample_poly_scratch": (_i64, [_vp, _int, _int, _int, _vp, _int]),
     "sfft_sample_poly": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int,
-                                _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp]),
+                                _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _vp]),
     "sfft_sample_bspline": (_int, [_int, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp, _int, _vp, _int,
-                                   _vp, _vp, _i64, _int, _vp]),
-    "sfft_finish_samples": (_int, [_vp, _int, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp]),
-    "sfft_unit_norm2": (_int, [_vp, _int, _int, _vp, _i64, _vp, _vp]),
+                                   _vp, _vp, _i64, _int, _vp, _int, _vp]),
+    "sfft_finish_samples": (_int, [_vp, _int, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _int, _vp]),
+    "sfft_unit_norm2": (_int, [_vp, _int, _int, _vp, _i64, _vp, _vp, _int, _vp]),
     "sfft_lattice_nodes": (_int, [_vp, _vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "sfft_gather_select": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp, _i64, _int, _int,
                                   _dbl, _vp, _vp, _vp, _vp]),
+    "sfft_gather_units": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _vp]),
+    "sfft_combine_units": (_int, [_i64, _int, _vp, _vp, _vp, _int, _int, _int, _dbl, _vp, _vp, _vp, _vp]),
     "sfft_select_scratch_bytes": (_i64, [_i64]),
     "sfft_select_cap": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
     "sfft_scan_scratch_len": (_i64, [_i64]),

@@ -232,10 +232,10 @@ def dft_1d(values, direction: str = "forward") -> np.ndarray:
     inv = direction == "inverse"
     if inv:
         dev.call("sfft_cscale", dptr(buf), K, 1.0, 1, ctx="dft_1d conj")
-    dev.call("sfft_finish_samples", hptr(tabs.ms), 1, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0,
+    dev.call("sfft_finish_samples", hptr(tabs.ms), 1, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="dft_1d pre-chirp")
     dev.call("sfft_bluestein", hptr(tabs.ms), 1, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
-             dptr(tabs.chirp), dptr(buf), ctx="dft_1d")
+             dptr(tabs.chirp), dptr(buf), 0, 0, ctx="dft_1d")
     if inv:
         dev.call("sfft_cscale", dptr(buf), K, 1.0 / K, 1, ctx="dft_1d scale")
     out = dev.download(buf[0, :K])
@@ -271,10 +271,10 @@ def invert_multiple(samples: Sequence[LatticeSamples], ml: MultipleRank1Lattice)
         host[l, : got.lattice.m] = _c2(got.values)
     with torch.cuda.stream(dev.stream):
         buf[:, : host.shape[1]].copy_(torch.from_numpy(host))
-    dev.call("sfft_finish_samples", hptr(ms), L, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0,
+    dev.call("sfft_finish_samples", hptr(ms), L, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="invert_multiple pre-chirp")
     dev.call("sfft_bluestein", hptr(ms), L, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
-             dptr(buf), ctx="invert_multiple FFT")
+             dptr(buf), 0, 0, ctx="invert_multiple FFT")
     cand = DeviceFreqs.from_host(dev, target.freqs)
     d_masks = dev.upload(words.view(np.int64))
     coef = dev.empty((1, n, 2), torch.float64)

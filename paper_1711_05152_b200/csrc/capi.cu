@@ -109,10 +109,16 @@ int fill_lat(LatTable& lt, const int64_t* h_m, const int32_t* h_z, int L, int t1
   return 0;
 }
 
-int fill_units(UnitTable& ut, const int64_t* h_m, int L, int rb) {
-  if (L < 1 || L > SFFT_LMAX || rb < 1 || (int64_t)rb * L > SFFT_UMAX) return E_2BIG;
+// Units of a launch: all rb x L (iteration, lattice) pairs in order
+// (h_units == NULL), or the explicit list h_units[j] = it * L + l (it < rb),
+// buffer slot j holding unit h_units[j] (the sharded engine's local units).
+int fill_units(UnitTable& ut, const int64_t* h_m, int L, int rb, const int32_t* h_units = nullptr,
+               int nunits = 0) {
+  if (L < 1 || L > SFFT_LMAX || rb < 1) return E_2BIG;
+  const int nu = h_units ? nunits : rb * L;
+  if (nu < 1 || nu > SFFT_UMAX) return E_2BIG;
   memset(&ut, 0, sizeof(UnitTable));
-  ut.nunits = rb * L;
+  ut.nunits = nu;
   ut.nlat = L;
   int64_t off = 0;
   for (int l = 0; l < L; ++l) {
@@ -120,11 +126,12 @@ int fill_units(UnitTable& ut, const int64_t* h_m, int L, int rb) {
     ut.off[l] = off;
     off += h_m[l];
   }
-  for (int i = 0; i < rb; ++i)
-    for (int l = 0; l < L; ++l) {
-      ut.lat[i * L + l] = l;
-      ut.it[i * L + l] = i;
-    }
+  for (int j = 0; j < nu; ++j) {
+    const int g = h_units ? h_units[j] : j;
+    if (g < 0 || g >= rb * L) return E_INVAL;
+    ut.lat[j] = g % L;
+    ut.it[j] = g / L;
+  }
   return 0;
 }
 
@@ -212,11 +219,11 @@ void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2) {
 // The K split (term slices reduced in order by a second kernel) is chosen to
 // maximise the fraction of the last wave that is busy; `need` = partial-sum
 // scratch in complex elements (0 without a split).  partial_cap < 0: unlimited.
-int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int num_sms,
-                    int64_t partial_cap, int64_t* need) {
-  if (L < 1 || L > SFFT_LMAX || rb < 1 || (int64_t)rb * L > SFFT_UMAX || s < 0) return E_2BIG;
+int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut, int rb_hint, int s,
+                    int num_sms, int64_t partial_cap, int64_t* need) {
+  if (L < 1 || L > SFFT_LMAX || ut.nunits < 1 || ut.nunits > SFFT_UMAX || s < 0) return E_2BIG;
   memset(pp, 0, sizeof(PolyPlan));
-  pp->nunits = rb * L;
+  pp->nunits = ut.nunits;
   pp->s = s;
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
@@ -225,9 +232,9 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int 
   pp->bl = bl;
   const size_t smem = sample_poly_smem(bl, mmax);
   if (smem > 227 * 1024) return E_2BIG;
-  // resident CTAs per SM: 3 by registers (128 threads x <= 168 regs), fewer if smem-bound
+  // resident CTAs per SM: 2 by registers (256 threads x 128 regs), fewer if smem-bound
   int per_sm = (int)((228 * 1024) / (smem + 1024));
-  if (per_sm > 3) per_sm = 3;
+  if (per_sm > 2) per_sm = 2;
   if (per_sm < 1) per_sm = 1;
   int64_t tiles_l[SFFT_LMAX];
   int64_t tiles_total = 0;
@@ -237,9 +244,15 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int 
     pp->J1[l] = j1;
     pp->nt1[l] = nt1;
     tiles_l[l] = (int64_t)nt1 * nt2;
-    tiles_total += (int64_t)rb * tiles_l[l];
     pp->mu[l] = ~0ull / (uint64_t)h_m[l];
   }
+  // The K split is chosen for the full chunk of rb x L units even when this
+  // launch holds a subset (sharded step): the term slicing, and so every
+  // rounding, is then independent of the number of GPUs.
+  int rb_nominal = 1;
+  for (int u = 0; u < ut.nunits; ++u) rb_nominal = ut.it[u] + 1 > rb_nominal ? ut.it[u] + 1 : rb_nominal;
+  if (rb_hint > rb_nominal) rb_nominal = rb_hint;
+  for (int l = 0; l < L; ++l) tiles_total += (int64_t)rb_nominal * tiles_l[l];
   const int64_t slots = (int64_t)per_sm * num_sms;
   int best_ks = 1, best_kper = ((s + 15) / 16) * 16;
   double best_eff = -1.0;
@@ -258,15 +271,13 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, int rb, int s, int 
   pp->ks = best_ks;
   pp->kper = best_kper;
   int64_t acc = 0;
-  for (int i = 0; i < rb; ++i)
-    for (int l = 0; l < L; ++l) {
-      const int u = i * L + l;
-      pp->unit_lat[u] = l;
-      pp->unit_it[u] = i;
-      pp->tile_start[u] = (int)acc;
-      acc += tiles_l[l] * best_ks;
-    }
-  pp->tile_start[rb * L] = (int)acc;
+  for (int u = 0; u < ut.nunits; ++u) {
+    pp->unit_lat[u] = ut.lat[u];
+    pp->unit_it[u] = ut.it[u];
+    pp->tile_start[u] = (int)acc;
+    acc += tiles_l[ut.lat[u]] * best_ks;
+  }
+  pp->tile_start[ut.nunits] = (int)acc;
   if (acc > 0x7fffffffLL) return E_2BIG;
   *need = best_ks > 1 ? (int64_t)best_ks * pp->nunits * mmax : 0;
   return 0;
@@ -375,10 +386,11 @@ int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
 }
 
 int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
-                   const double* d_bhat, const double* d_chirp, double* d_buf, void* stream) {
+                   const double* d_bhat, const double* d_chirp, double* d_buf,
+                   const int32_t* h_units, int nunits, void* stream) {
   if (p < 4 || p > 24) return E_INVAL;
   UnitTable ut;
-  int rc = fill_units(ut, h_m, L, rb);
+  int rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   for (int l = 0; l < L; ++l)
     if (2 * h_m[l] - 1 > ((int64_t)1 << p)) return E_INVAL;
@@ -390,12 +402,15 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
                      const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
                      double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
                      const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
-                     double* d_partial, int64_t partial_len, void* stream) {
-  if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX) return E_INVAL;
+                     double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
+                     void* stream) {
+  if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX || rb < 1) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
   if (rc) return rc;
-  if ((int64_t)rb * L > SFFT_UMAX || rb < 1) return E_2BIG;
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb, h_units, nunits);
+  if (rc) return rc;
   const int tail = d - t1;
   if ((int64_t)rb * tail > 1024) return E_2BIG;
   AnchorTable at;
@@ -404,10 +419,7 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
   for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
   PolyPlan* pp = new PolyPlan;
   int64_t need = 0;
-  rc = build_poly_plan(pp, h_m, L, rb, s, num_sms_current(), partial_len, &need);
-  if (rc) { delete pp; return rc; }
-  UnitTable ut;
-  rc = fill_units(ut, h_m, L, rb);
+  rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), partial_len, &need);
   if (rc) { delete pp; return rc; }
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
@@ -422,10 +434,13 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
   return rc;
 }
 
-int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s) {
+int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s, const int32_t* h_units,
+                                 int nunits) {
+  UnitTable ut;
+  if (fill_units(ut, h_m, L, rb, h_units, nunits)) return -1;
   PolyPlan* pp = new PolyPlan;
   int64_t need = 0;
-  int rc = build_poly_plan(pp, h_m, L, rb, s, num_sms_current(), -1, &need);
+  int rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), -1, &need);
   delete pp;
   return rc ? -1 : need;
 }
@@ -434,13 +449,13 @@ int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_st
                         const int32_t* h_comps, const double* h_scale, int d, int t1,
                         const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor,
                         int rb, const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
-                        void* stream) {
+                        const int32_t* h_units, int nunits, void* stream) {
   if (ngroups < 0 || ngroups > 8 || d < 1 || d > SFFT_DMAX || t1 < 1 || t1 > d) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
   if (rc) return rc;
   UnitTable ut;
-  rc = fill_units(ut, h_m, L, rb);
+  rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   BsplineSpec bs;
   rc = fill_bspline(bs, ngroups, h_order, h_start, h_comps, h_scale, d);
@@ -458,9 +473,9 @@ int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_st
 
 int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp, double* d_buf,
                         int64_t P, const double* d_noise, int64_t nstride, const double* d_sigma,
-                        void* stream) {
+                        const int32_t* h_units, int nunits, void* stream) {
   UnitTable ut;
-  int rc = fill_units(ut, h_m, L, rb);
+  int rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   return launch_finish_samples(ut, (const double2*)d_chirp, (double2*)d_buf, P,
                                (const double2*)d_noise, nstride, d_sigma, num_sms_current(),
@@ -468,9 +483,9 @@ int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp
 }
 
 int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
-                    double* d_out, void* stream) {
+                    double* d_out, const int32_t* h_units, int nunits, void* stream) {
   UnitTable ut;
-  int rc = fill_units(ut, h_m, L, rb);
+  int rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   return launch_unit_norm2(ut, (const double2*)d_buf, P, d_out, num_sms_current(), S(stream));
 }
@@ -499,6 +514,33 @@ int sfft_gather_select(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, 
   return launch_gather(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, rb, it0, delta,
                        (double2*)d_coef, d_keep, d_counts, residue_fast(t1, kmax, h_m, L),
                        num_sms_current(), S(stream));
+}
+
+int sfft_gather_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                      const int32_t* h_z, int L, const uint64_t* d_masks, const double* d_buf,
+                      int64_t P, int rb, const int32_t* h_units, int nunits, double* d_out,
+                      void* stream) {
+  if (n < 0 || !h_units) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb, h_units, nunits);
+  if (rc) return rc;
+  return launch_gather_units(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, ut, (double2*)d_out,
+                             residue_fast(t1, kmax, h_m, L), num_sms_current(), S(stream));
+}
+
+int sfft_combine_units(int64_t n, int L, const uint64_t* d_masks, const double* d_vals,
+                       const int32_t* h_rows, int r_total, int rb, int it0, double delta,
+                       double* d_coef, uint8_t* d_keep, int32_t* d_counts, void* stream) {
+  if (n < 0 || L < 1 || L > SFFT_LMAX || rb < 1 || rb > 8 || it0 < 0 || it0 + rb > r_total)
+    return E_INVAL;
+  if ((int64_t)r_total * L > SFFT_UMAX) return E_2BIG;
+  RowMap rm;
+  for (int u = 0; u < r_total * L; ++u) rm.row[u] = h_rows[u];
+  return launch_combine_units(n, L, d_masks, (const double2*)d_vals, rm, rb, it0, delta,
+                              (double2*)d_coef, d_keep, d_counts, num_sms_current(), S(stream));
 }
 
 int64_t sfft_select_scratch_bytes(int64_t n) { return select_scratch_bytes(n); }

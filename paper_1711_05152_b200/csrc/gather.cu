@@ -56,9 +56,11 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
           if (i < rb) {
+            // spectrum_hat = X / M rounded, then accumulated (no FMA contraction),
+            // exactly the numpy sequence of transform.py:121-123
             const double2 v = __ldg(&buf[(int64_t)(i * L + l) * ustride + r]);
-            sums[i].x += v.x * invm;
-            sums[i].y += v.y * invm;
+            sums[i].x = __dadd_rn(sums[i].x, __dmul_rn(v.x, invm));
+            sums[i].y = __dadd_rn(sums[i].y, __dmul_rn(v.y, invm));
           }
         }
       }
@@ -67,7 +69,7 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
       if (i < rb) {
-        double2 c = make_double2(sums[i].x * invc, sums[i].y * invc);
+        double2 c = make_double2(__dmul_rn(sums[i].x, invc), __dmul_rn(sums[i].y, invc));
         uint8_t kf = 0;
         if (cnt) {
           const double mag = hypot(c.x, c.y);
@@ -140,6 +142,146 @@ int launch_gather(const int32_t* freqs, int64_t n, const LatTable& lt, const uin
   SFFT_G_CASE(64)
 #undef SFFT_G_CASE
   return -22;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded step (several GPUs): each rank gathers the alias-free bins of its
+// own (iteration, lattice) units into dense per-unit rows
+//     out[j][k] = bit l(j) of mask_k ? X_j[k.z_l mod M_l] * (1/M_l) : 0,
+// the rows of all ranks are all-gathered (NCCL), and every rank combines them
+// in lattice order with the same rounding sequence as gather_kernel, so the
+// result is bit-identical for any number of GPUs.
+
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+gather_units_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+                    const uint64_t* __restrict__ masks, const double2* __restrict__ buf,
+                    int64_t ustride, UnitTable ut, double2* __restrict__ out) {
+  const int d = lt.d;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t mask = masks[k];
+    int32_t kv[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) kv[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + k]) : 0;
+    for (int j = 0; j < ut.nunits; ++j) {
+      const int l = ut.lat[j];
+      double2 t = make_double2(0.0, 0.0);
+      if ((mask >> l) & 1ull) {
+        const int64_t r = residue<DM, FAST>(kv, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+        const double invm = 1.0 / (double)lt.m[l];
+        const double2 v = __ldg(&buf[(int64_t)j * ustride + r]);
+        t = make_double2(__dmul_rn(v.x, invm), __dmul_rn(v.y, invm));
+      }
+      out[(int64_t)j * n + k] = t;
+    }
+  }
+}
+
+template <int RB>
+__global__ void __launch_bounds__(256)
+combine_units_kernel(int64_t n, int L, const uint64_t* __restrict__ masks,
+                     const double2* __restrict__ vals, RowMap rm, int rb, int it0, double delta,
+                     double2* __restrict__ coef, uint8_t* __restrict__ keep,
+                     int32_t* __restrict__ counts) {
+  __shared__ int red[RB][8];
+  const uint64_t lmask = (L >= 64) ? ~0ull : ((1ull << L) - 1ull);
+  int kept[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) kept[i] = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t mm = masks[k] & lmask;
+    double2 sums[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) sums[i] = make_double2(0.0, 0.0);
+    int cnt = 0;
+    while (mm) {
+      const int l = __ffsll((long long)mm) - 1;
+      mm &= mm - 1;
+      ++cnt;
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        if (i < rb) {
+          const double2 t = vals[(int64_t)rm.row[(it0 + i) * L + l] * n + k];
+          sums[i].x = __dadd_rn(sums[i].x, t.x);
+          sums[i].y = __dadd_rn(sums[i].y, t.y);
+        }
+      }
+    }
+    const double invc = cnt ? 1.0 / (double)cnt : 0.0;
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      if (i < rb) {
+        double2 c = make_double2(__dmul_rn(sums[i].x, invc), __dmul_rn(sums[i].y, invc));
+        uint8_t kf = 0;
+        if (cnt) kf = (hypot(c.x, c.y) >= delta) ? 1 : 0;
+        else c = make_double2(0.0, 0.0);
+        coef[(int64_t)(it0 + i) * n + k] = c;
+        keep[(int64_t)(it0 + i) * n + k] = kf;
+        kept[i] += kf;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    int v = kept[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[i][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < RB && threadIdx.x < rb) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+    if (t) atomicAdd(&counts[it0 + threadIdx.x], t);
+  }
+}
+
+int launch_gather_units(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
+                        const double2* buf, int64_t ustride, const UnitTable& ut, double2* out,
+                        bool fast, int num_sms, cudaStream_t st) {
+  if (n == 0 || ut.nunits == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  const int blocks = (int)(want < cap ? want : cap);
+  const int d = lt.d;
+#define SFFT_GU_CASE(DMV)                                                                      \
+  if (d <= DMV) {                                                                              \
+    if (fast) gather_units_kernel<DMV, true><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf, \
+                                                                     ustride, ut, out);        \
+    else gather_units_kernel<DMV, false><<<blocks, 256, 0, st>>>(freqs, n, lt, masks, buf,     \
+                                                                 ustride, ut, out);            \
+    SFFT_CHECK_LAUNCH();                                                                       \
+    return 0;                                                                                  \
+  }
+  SFFT_GU_CASE(4)
+  SFFT_GU_CASE(8)
+  SFFT_GU_CASE(16)
+  SFFT_GU_CASE(32)
+  SFFT_GU_CASE(64)
+#undef SFFT_GU_CASE
+  return -22;
+}
+
+int launch_combine_units(int64_t n, int L, const uint64_t* masks, const double2* vals,
+                         const RowMap& rm, int rb, int it0, double delta, double2* coef,
+                         uint8_t* keep, int32_t* counts, int num_sms, cudaStream_t st) {
+  if (n == 0) return 0;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  const int blocks = (int)(want < cap ? want : cap);
+  if (rb <= 1)
+    combine_units_kernel<1><<<blocks, 256, 0, st>>>(n, L, masks, vals, rm, rb, it0, delta, coef, keep, counts);
+  else if (rb <= 4)
+    combine_units_kernel<4><<<blocks, 256, 0, st>>>(n, L, masks, vals, rm, rb, it0, delta, coef, keep, counts);
+  else if (rb <= 8)
+    combine_units_kernel<8><<<blocks, 256, 0, st>>>(n, L, masks, vals, rm, rb, it0, delta, coef, keep, counts);
+  else
+    return -22;
+  SFFT_CHECK_LAUNCH();
+  return 0;
 }
 
 // ---------------------------------------------------------------------------

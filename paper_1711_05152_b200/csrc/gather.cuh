@@ -10,6 +10,12 @@ int64_t alias_scratch_words(const LatTable& lt);
 int launch_gather(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
                   const double2* buf, int64_t ustride, int rb, int it0, double delta, double2* coef,
                   uint8_t* keep, int32_t* counts, bool fast, int num_sms, cudaStream_t st);
+int launch_gather_units(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
+                        const double2* buf, int64_t ustride, const UnitTable& ut, double2* out,
+                        bool fast, int num_sms, cudaStream_t st);
+int launch_combine_units(int64_t n, int L, const uint64_t* masks, const double2* vals,
+                         const RowMap& rm, int rb, int it0, double delta, double2* coef,
+                         uint8_t* keep, int32_t* counts, int num_sms, cudaStream_t st);
 int64_t scan_scratch_len(int64_t n);
 int launch_flag_indices(const uint8_t* flags, int64_t n, int nrows, int32_t* idx_out,
                         int32_t* total, int32_t* scratch, cudaStream_t st);

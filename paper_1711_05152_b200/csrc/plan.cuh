@@ -29,6 +29,11 @@ struct UnitTable {
   int64_t off[SFFT_LMAX];
 };
 
+// row of the all-gathered per-unit buffer holding global unit u = it * L + l
+struct RowMap {
+  int row[SFFT_UMAX];
+};
+
 // Power-of-two FFT geometry: P = P1 * P2, P2 = 2^min(12, p).
 struct FftGeom {
   int p, p1, p2, P1, P2, qlo, nlo;

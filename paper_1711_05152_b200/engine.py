@@ -179,7 +179,7 @@ def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarra
         if oracle.needs_norm():
             nrm = dev.empty((r,), torch.float64)
             km = np.array([K], dtype=np.int64)
-            dev.call("sfft_unit_norm2", hptr(km), 1, r, dptr(vals), K, dptr(nrm), ctx="line noise norm")
+            dev.call("sfft_unit_norm2", hptr(km), 1, r, dptr(vals), K, dptr(nrm), 0, 0, ctx="line noise norm")
             norms = dev.download(nrm)
         for i in range(r):
             e = dev.upload(np.ascontiguousarray(oracle.draw(K)))
@@ -243,10 +243,18 @@ def detect_component(oracle, t: int, cfg: DetectionConfig, rng: np.random.Genera
 # ---------------------------------------------------------------------------
 # the engine
 
-def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None) -> DetectionReport:
+def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
+               group=None, shard: bool | None = None) -> DetectionReport:
     """Reconstruct support and coefficients of a sparse periodic signal
-    (reference detect.py:305-423) on the GPU."""
+    (reference detect.py:305-423) on the GPU.
+
+    Under torch.distributed (one process per GPU) the units of every MR1L step
+    are sharded over the ranks of ``group`` (parallel.py) unless
+    ``shard=False``; every rank returns the same, bit-identical report."""
+    from .parallel import Shard, run_step_sharded
     start = time.perf_counter()
+    sh = Shard(group)
+    sharded = sh.active and shard is not False
     if getattr(oracle, "dim", cfg.box.dim) != cfg.box.dim:
         raise ValueError("oracle dimension does not match the search box")
     if cfg.lattice_kind != "multiple":
@@ -320,7 +328,10 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None) ->
         anchor_rng = np.random.default_rng(anchor_streams[t])
         tail = d - (t + 1)
         tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
-        res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t)
+        if sharded:
+            res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
+        else:
+            res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t)
         if last:
             rows_d, coef_d = compact(dev, cand, res.keep[0], 1, res.coef[0])
             final_rows = rows_d.to_host(dev)

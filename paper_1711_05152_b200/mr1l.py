@@ -270,9 +270,20 @@ class StepResult:
     timings: dict = field(default_factory=dict)
 
 
+def _unit_arg(units):
+    """(host int32 array or None, count) for the C ABI's unit lists."""
+    if units is None:
+        return None, 0
+    arr = np.ascontiguousarray(np.asarray(units, dtype=np.int32))
+    return arr, len(arr)
+
+
 def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
-                  tails: list[np.ndarray], buf, step: int, it0: int):
-    """Fill buf[u] (u = i*L + l) with pre-chirped samples of the chunk's units."""
+                  tails: list[np.ndarray], buf, step: int, it0: int, units=None):
+    """Fill buffer slot j with the pre-chirped samples of unit units[j]
+    (global id i * L + l within this chunk of iterations; all rb * L units in
+    order when ``units`` is None).  Noise streams are consumed for every unit
+    of the chunk in the reference's call order, whichever units are local."""
     torch = dev.torch
     L = len(tabs.ms)
     rb = len(tails)
@@ -280,7 +291,10 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
     tail = d - t1
     anchor = np.ascontiguousarray(np.asarray(tails, dtype=np.float64).reshape(rb, tail)) \
         if tail else np.zeros(1, dtype=np.float64)
-    nodes = rb * int(tabs.ms.sum())
+    ulist = list(range(rb * L)) if units is None else [int(u) for u in units]
+    uarr, nu = _unit_arg(units)
+    up = hptr(uarr) if uarr is not None else 0
+    nodes = sum(int(tabs.ms[u % L]) for u in ulist)
     base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
     device_inner = isinstance(base, (SparsePolynomialOracle, BSplineOracle))
     noisy = isinstance(oracle, NoisyOracle)
@@ -292,67 +306,73 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
             cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
             rres = dev.empty((L, max(s, 1)), torch.int32)
             rj = dev.empty((L, max(s, 1)), torch.int32)
-            need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s))
+            need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
             part = dev.empty((max(need, 1), 2), torch.float64)
             dev.call("sfft_sample_poly", dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
                      hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
-                     dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0),
+                     dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0), up, nu,
                      ctx=f"sampling, step {step}")
         else:
             order, start, comps, scale = base.host_spec()
             dev.call("sfft_sample_bspline", len(base.groups), hptr(order), hptr(start), hptr(comps),
                      hptr(scale), d, t1, hptr(tabs.ms), hptr(tabs.zs), L, hptr(anchor), rb,
-                     dptr(tabs.chirp), dptr(buf), P, chirp_now, ctx=f"sampling, step {step}")
+                     dptr(tabs.chirp), dptr(buf), P, chirp_now, up, nu, ctx=f"sampling, step {step}")
         if noisy:
-            _add_lattice_noise(dev, oracle, tabs, rb, buf)
+            _add_lattice_noise(dev, oracle, tabs, rb, buf, ulist, uarr)
         else:
             base.count_samples(nodes)
         return nodes
     # host callback: nodes on the device, values from the callback
     pts = dev.empty((int(tabs.ms.max()), d), torch.float64)
-    for i in range(rb):
+    for j, u in enumerate(ulist):
+        i, l = divmod(u, L)
+        m = int(tabs.ms[l])
         tail_i = np.ascontiguousarray(anchor[i] if tail else np.zeros(1))
-        for l in range(L):
-            m = int(tabs.ms[l])
-            dev.call("sfft_lattice_nodes", hptr(tabs.ms), hptr(tabs.zs), L, t1, l, d, hptr(tail_i),
-                     dptr(pts), ctx=f"lattice nodes, step {step}")
-            host_pts = dev.download(pts[:m])
-            vals = evaluate_callback(oracle, host_pts, step, it0 + i)
-            v2 = np.ascontiguousarray(np.stack([vals.real, vals.imag], axis=1))
-            u = i * L + l
-            with torch.cuda.stream(dev.stream):
-                buf[u, :m].copy_(torch.from_numpy(v2), non_blocking=False)
-    dev.call("sfft_finish_samples", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P, 0, 0, 0,
+        dev.call("sfft_lattice_nodes", hptr(tabs.ms), hptr(tabs.zs), L, t1, l, d, hptr(tail_i),
+                 dptr(pts), ctx=f"lattice nodes, step {step}")
+        host_pts = dev.download(pts[:m])
+        vals = evaluate_callback(oracle, host_pts, step, it0 + i)
+        v2 = np.ascontiguousarray(np.stack([vals.real, vals.imag], axis=1))
+        with torch.cuda.stream(dev.stream):
+            buf[j, :m].copy_(torch.from_numpy(v2), non_blocking=False)
+    dev.call("sfft_finish_samples", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P, 0, 0, 0, up, nu,
              ctx=f"pre-chirp, step {step}")
     return nodes
 
 
-def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb: int, buf):
+def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb: int, buf,
+                       ulist: list[int], uarr):
     """Noise in the reference's call order (iteration-major, then lattice),
-    drawn from the oracle's numpy stream, added on the device with the
-    pre-chirp."""
+    drawn from the oracle's numpy stream for every unit of the chunk, added on
+    the device (local units only) together with the pre-chirp."""
     torch = dev.torch
     L = len(tabs.ms)
     P = tabs.P
     mmax = int(tabs.ms.max())
-    norms = None
+    nu = len(ulist)
+    up = hptr(uarr) if uarr is not None else 0
+    nuarg = len(uarr) if uarr is not None else 0
+    norms = {}
     if oracle.needs_norm():
-        nrm = dev.empty((rb * L,), torch.float64)
-        dev.call("sfft_unit_norm2", hptr(tabs.ms), L, rb, dptr(buf), P, dptr(nrm), ctx="noise norm")
-        norms = dev.download(nrm)
-    noise = np.zeros((rb * L, mmax, 2), dtype=np.float64)
-    sig = np.zeros(rb * L, dtype=np.float64)
-    for i in range(rb):
-        for l in range(L):
-            u = i * L + l
-            m = int(tabs.ms[l])
-            noise[u, :m] = oracle.draw(m)
-            sig[u] = oracle.scale_for(float(norms[u]) if norms is not None else 0.0, m)
-            oracle.count_samples(m)
+        nrm = dev.empty((nu,), torch.float64)
+        dev.call("sfft_unit_norm2", hptr(tabs.ms), L, rb, dptr(buf), P, dptr(nrm), up, nuarg,
+                 ctx="noise norm")
+        norms = dict(zip(ulist, dev.download(nrm).tolist()))
+    slot = {u: j for j, u in enumerate(ulist)}
+    noise = np.zeros((nu, mmax, 2), dtype=np.float64)
+    sig = np.zeros(nu, dtype=np.float64)
+    for u in range(rb * L):
+        m = int(tabs.ms[u % L])
+        e = oracle.draw(m)
+        oracle.count_samples(m)
+        j = slot.get(u)
+        if j is not None:
+            noise[j, :m] = e
+            sig[j] = oracle.scale_for(norms.get(u, 0.0), m)
     d_noise = dev.upload(noise)
     d_sig = dev.upload(sig)
     dev.call("sfft_finish_samples", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P,
-             dptr(d_noise), mmax, dptr(d_sig), ctx="noisy samples")
+             dptr(d_noise), mmax, dptr(d_sig), up, nuarg, ctx="noisy samples")
 
 
 class StageTimer:
@@ -419,7 +439,7 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
             nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0)
         with tm.span("fft"):
             dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
-                     dptr(tabs.chirp), dptr(buf), ctx=f"Bluestein FFT, step {step}")
+                     dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")
         with tm.span("gather"):
             dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
                      dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),

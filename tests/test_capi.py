@@ -1,0 +1,75 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU, and exports every
+entry point include/sfft_b200.h declares (no compute calls here)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "sfft_b200.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sfft_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1711_05152_b200 import _native
+    return _native.load()
+
+
+def test_header_symbols_exported(lib):
+    names = _declared()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_table_matches_header():
+    from paper_1711_05152_b200 import _native
+    assert sorted(_native.EXPORTED) == _declared()
+
+
+def test_sm100a_cubin_embedded():
+    import subprocess
+    so = ROOT / "paper_1711_05152_b200" / "libsfft_b200.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_size_queries_without_gpu(lib):
+    from paper_1711_05152_b200 import _native
+    import numpy as np
+    assert _native.query("sfft_abi_version") == 1
+    assert _native.query("sfft_fft_table_len", 3) == -1
+    n18 = _native.query("sfft_fft_table_len", 18)
+    # [P1 | P2 | 2^9 | 2^9] with P = 2^18 = 2^6 * 2^12
+    assert n18 == 64 + 4096 + 512 + 512
+    ms = np.array([7, 64, 65], dtype=np.int64)
+    assert _native.query("sfft_alias_scratch_words", ms.ctypes.data, 3) == 2 * (1 + 2 + 3)
+    assert _native.query("sfft_scan_scratch_len", 0) == 1
+    assert _native.query("sfft_scan_scratch_len", 2049) == 3
+    assert _native.query("sfft_select_scratch_bytes", 100) > 500
+
+
+def test_error_strings(lib):
+    assert lib.sfft_error_string(0) == b"ok"
+    assert lib.sfft_error_string(-22) == b"invalid argument"
+    assert lib.sfft_error_string(-7).startswith(b"argument exceeds")
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    from paper_1711_05152_b200.device import get_device
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        get_device()
+    import paper_1711_05152_b200 as P
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.dft_1d([1.0, 2.0, 3.0])
