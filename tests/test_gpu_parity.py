@@ -261,6 +261,23 @@ def test_zero_signal(P):
     assert rep.oracle_calls == oracle.call_count
 
 
+def test_config2_full_size_matches_reference_run(P):
+    """BASELINE config 2 at full size on the instance the survey ran through the
+    unmodified reference (seed 42 / rng_seed 43, r = 5; SURVEY §6.3 and
+    BASELINE.md §3.1: 3127.5 s on the CPU).  Every per-step candidate count,
+    every scheme size and the total oracle-call audit are the reference's."""
+    truth, oracle = P.gen_random_sparse_poly(10, 32, 1000, "box", seed=42)
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(10, 32), delta=1e-12, s=1000, r=5, b=10, rng_seed=43)
+    rep = P.sparse_fft(oracle, cfg)
+    assert rep.candidate_counts == [65, 4225, 58370, 64935] + [65000] * 6
+    assert rep.scheme_sizes == [0, 16928, 1284863, 1689355, 1040344, 1821004, 1430609, 1170423, 1170423,
+                                1560730]
+    assert rep.lattice_attempts == [0] + [1] * 9
+    assert rep.oracle_calls == 49_683_725
+    assert rep.detected.support() == truth.support()
+    assert P.relative_spectrum_l2_error(rep.detected, truth) <= 1e-14
+
+
 def test_config1_full_size(P):
     """BASELINE config 1 at full size: |J| = 100000, d = 10, 2000 nonzero.
     Masks bit-exact against the CPU oracle; coefficients against the truth."""
