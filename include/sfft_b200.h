@@ -190,6 +190,11 @@ int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,
 int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, void* stream);
 
 /* ---- utilities ---------------------------------------------------------------- */
+/* numpy rows (n x d int64, row-major) -> component-major int32 candidates;
+ * d_minmax (2d + 1 int32): per-component min, max, and an out-of-range flag
+ * (|k| > 2^31 - 1, lattice.py:36-38). */
+int sfft_pack_rows(const int64_t* d_rows, int64_t n, int d, int32_t* d_out, int32_t* d_minmax,
+                   void* stream);
 int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream);
 /* FP64 roofline probe: blocks x 256 threads x iters x 16 DFMA */
 int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream);

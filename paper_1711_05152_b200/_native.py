@@ -55,6 +55,7 @@ _SIGS = {
     "sfft_eval_poly_points": (_int, [_vp, _i64, _int, _vp, _vp, _int, _vp, _vp]),
     "sfft_eval_bspline_points": (_int, [_vp, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sfft_add_noise": (_int, [_vp, _vp, _i64, _dbl, _vp]),
+    "sfft_pack_rows": (_int, [_vp, _i64, _int, _vp, _vp, _vp]),
     "sfft_cscale": (_int, [_vp, _i64, _dbl, _int, _vp]),
     "sfft_fp64_peak": (_int, [_vp, _int, _int, _vp]),
 }

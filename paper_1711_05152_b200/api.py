@@ -102,12 +102,12 @@ def build_multiple_lattice(I: FrequencyIndexSet, cfg: MLConfig,
     l_max = cfg.max_lattices(n)
     primes = candidate_primes(I, cfg.size_lower_bound(n), l_max)
     saved = rng.bit_generator.state
-    z = np.stack([rng.integers(0, m, size=I.dim, dtype=np.int64) for m in primes])
+    ms = np.asarray(primes, dtype=np.int64)
+    z = rng.integers(0, ms[:, None], size=(len(ms), I.dim), dtype=np.int64)
     cand = DeviceFreqs.from_host(dev, I.freqs)
     sch = _masks_for(dev, cand, primes, z)
     rng.bit_generator.state = saved
-    for m in primes[: sch.L]:
-        rng.integers(0, m, size=I.dim, dtype=np.int64)
+    rng.integers(0, ms[: sch.L, None], size=(sch.L, I.dim), dtype=np.int64)
     return scheme_to_host(dev, I.freqs, sch)
 
 
@@ -166,32 +166,36 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     -> oracle(lattice nodes) -> invert_multiple -> _select of the reference
     (construct.py:185-206, detect.py:290-299, transform.py:99-127,
     detect.py:197-212) as one device pipeline."""
-    from .mr1l import compact, run_step
-    rows = np.asarray(candidates, dtype=np.int64)
-    if rows.ndim != 2 or not len(rows):
-        raise ValueError("candidates must be a nonempty (n, d) integer array")
+    from .mr1l import run_step
     dev = device or get_device()
-    n, t1 = rows.shape
+    torch = dev.torch
+    if isinstance(candidates, torch.Tensor):
+        host_rows = candidates.to(torch.int64) if candidates.dtype != torch.int64 else candidates
+    else:
+        host_rows = torch.from_numpy(np.ascontiguousarray(np.asarray(candidates, dtype=np.int64)))
+    if host_rows.dim() != 2 or not host_rows.shape[0]:
+        raise ValueError("candidates must be a nonempty (n, d) integer array")
+    n, t1 = (int(x) for x in host_rows.shape)
     d = oracle.dim
     tail = np.zeros(d - t1) if anchor_tail is None else np.asarray(anchor_tail, dtype=np.float64)
     if seed_seq is None:
         seed_seq = np.random.SeedSequence(0)
     elif not isinstance(seed_seq, np.random.SeedSequence):
         seed_seq = np.random.SeedSequence(seed_seq)
-    cand = DeviceFreqs.from_host(dev, rows)
-    h2d = cand.n * cand.ncomp * 4
+    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows)
+    h2d = n * t1 * 8
     if hasattr(oracle, "device_terms"):
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
-    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((rows.max(0) - rows.min(0)).max()))
+    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()))
     res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap))
-    coef = dev.download(res.coef[0])
-    keep = dev.download(res.keep[0]).astype(bool)
-    words = dev.download(sch.masks).view(np.uint64)
+    coef, keep, words = dev.download_many(res.coef[0], res.keep[0], sch.masks)
     d2h = coef.nbytes + keep.nbytes + words.nbytes
-    return StepReport(coef[:, 0] + 1j * coef[:, 1], words != 0, keep, sch.primes[: sch.L], sch.z[: sch.L],
-                      sch.attempts, res.nodes, h2d, d2h)
+    # the pinned staging buffers are reused by the next call: own the results
+    coef = coef.view(np.complex128).reshape(n).copy()
+    return StepReport(coef, words.view(np.uint64) != 0, keep.view(bool).copy(),
+                      sch.primes[: sch.L], sch.z[: sch.L], sch.attempts, res.nodes, h2d, d2h)
 
 
 # ---------------------------------------------------------------------------

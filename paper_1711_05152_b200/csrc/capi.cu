@@ -621,6 +621,12 @@ int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, 
                           S(stream));
 }
 
+int sfft_pack_rows(const int64_t* d_rows, int64_t n, int d, int32_t* d_out, int32_t* d_minmax,
+                   void* stream) {
+  if (n < 0) return E_INVAL;
+  return launch_pack_rows(d_rows, n, d, d_out, d_minmax, num_sms_current(), S(stream));
+}
+
 int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream) {
   return launch_cscale((double2*)d_x, n, scale, conj, num_sms_current(), S(stream));
 }

@@ -612,6 +612,55 @@ int launch_residues(const int32_t* freqs, int64_t n, const LatTable& lt, int64_t
   return -22;
 }
 
+// Host rows (n x d int64, row-major, as numpy hands them over) -> the
+// component-major int32 device layout, with per-component min / max
+// (minmax[c] = min, minmax[d + c] = max) and an out-of-range flag
+// (minmax[2d] = 1 if some |k| > 2^31 - 1, lattice.py:36-38).
+__global__ void pack_rows_init_kernel(int d, int32_t* __restrict__ minmax) {
+  const int c = threadIdx.x;
+  if (c < d) { minmax[c] = INT32_MAX; minmax[d + c] = INT32_MIN; }
+  if (c == 0) minmax[2 * d] = 0;
+}
+
+__global__ void pack_rows_kernel(const int64_t* __restrict__ rows, int64_t n, int d,
+                                 int32_t* __restrict__ out, int32_t* __restrict__ minmax) {
+  __shared__ int smin[SFFT_DMAX], smax[SFFT_DMAX];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) { smin[c] = INT32_MAX; smax[c] = INT32_MIN; }
+  __syncthreads();
+  const int64_t total = n * d;
+  int bad = 0;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = rows[f];
+    const int64_t i = f / d;
+    const int c = (int)(f - i * d);
+    if (v > 2147483647LL || v < -2147483647LL) bad = 1;
+    const int32_t w = (int32_t)v;
+    out[(int64_t)c * n + i] = w;
+    atomicMin(&smin[c], w);
+    atomicMax(&smax[c], w);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    atomicMin(&minmax[c], smin[c]);
+    atomicMax(&minmax[d + c], smax[c]);
+  }
+  if (bad) atomicOr(&minmax[2 * d], 1);
+}
+
+int launch_pack_rows(const int64_t* rows, int64_t n, int d, int32_t* out, int32_t* minmax,
+                     int num_sms, cudaStream_t st) {
+  if (d < 1 || d > SFFT_DMAX) return -22;
+  pack_rows_init_kernel<<<1, 64, 0, st>>>(d, minmax);
+  SFFT_CHECK_LAUNCH();
+  if (n == 0) return 0;
+  int64_t want = (n * d + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  pack_rows_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(rows, n, d, out, minmax);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
 __global__ void cscale_kernel(double2* __restrict__ x, int64_t n, double scale, int conj) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {

@@ -29,6 +29,8 @@ int launch_product(const int32_t* pref, int64_t np, int t, const int32_t* comp, 
                    int32_t* out, int num_sms, cudaStream_t st);
 int launch_residues(const int32_t* freqs, int64_t n, const LatTable& lt, int64_t* out, bool fast,
                     int num_sms, cudaStream_t st);
+int launch_pack_rows(const int64_t* rows, int64_t n, int d, int32_t* out, int32_t* minmax,
+                     int num_sms, cudaStream_t st);
 int launch_cscale(double2* x, int64_t n, double scale, int conj, int num_sms, cudaStream_t st);
 
 }  // namespace sfft

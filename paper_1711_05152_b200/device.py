@@ -54,6 +54,7 @@ class Device:
         self.num_sms = sms.value
         self.cc = (maj.value, mnr.value)
         self._ftab: dict[int, object] = {}
+        self._pinned: dict[int, object] = {}
 
     # -- raw handles ------------------------------------------------------
     @property
@@ -83,6 +84,37 @@ class Device:
     def download(self, t) -> np.ndarray:
         with self.torch.cuda.stream(self.stream):
             return t.detach().to("cpu").numpy()
+
+    def download_many(self, *tensors) -> list[np.ndarray]:
+        """Copy several device tensors to host with asynchronous DMA into
+        pinned buffers (reused across calls, one per slot) and one stream
+        synchronisation; returns uint8 numpy views to reinterpret."""
+        torch = self.torch
+        outs = []
+        for k, t in enumerate(tensors):
+            nbytes = t.numel() * t.element_size()
+            key = ("many", k)
+            buf = self._pinned.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty((max(nbytes, 1),), dtype=torch.uint8, pin_memory=True)
+                self._pinned[key] = buf
+            with torch.cuda.stream(self.stream):
+                buf[:nbytes].copy_(t.detach().contiguous().reshape(-1).view(torch.uint8), non_blocking=True)
+            outs.append(buf[:nbytes].numpy())
+        self.stream.synchronize()
+        return outs
+
+    def download_small(self, t) -> np.ndarray:
+        """Copy of a small device tensor through a reusable pinned buffer."""
+        nbytes = t.numel() * t.element_size()
+        buf = self._pinned.get(nbytes)
+        if buf is None:
+            buf = self.torch.empty((nbytes,), dtype=self.torch.uint8, pin_memory=True)
+            self._pinned[nbytes] = buf
+        with self.torch.cuda.stream(self.stream):
+            buf.copy_(t.detach().reshape(-1).view(self.torch.uint8), non_blocking=True)
+        self.stream.synchronize()
+        return buf.numpy().view(np.dtype(str(t.dtype).replace("torch.", ""))).reshape(t.shape).copy()
 
     def sync(self):
         self.stream.synchronize()

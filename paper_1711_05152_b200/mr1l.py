@@ -81,6 +81,25 @@ class DeviceFreqs:
         t = dev.upload(np.ascontiguousarray(rows.T.astype(np.int32)))
         return cls(t, rows.shape[0], kmax)
 
+    @classmethod
+    def from_rows_tensor(cls, dev: Device, rows) -> tuple["DeviceFreqs", np.ndarray, np.ndarray]:
+        """Upload (n, d) int64 rows (a CPU tensor; pinned memory makes the copy
+        asynchronous DMA) and pack them on the device; also returns the
+        per-component minima and maxima."""
+        torch = dev.torch
+        n, d = (int(x) for x in rows.shape)
+        with torch.cuda.stream(dev.stream):
+            d_rows = rows.to(dev.device, non_blocking=bool(rows.is_pinned()))
+        out = dev.empty((d, n), torch.int32)
+        mm = dev.empty((2 * d + 1,), torch.int32)
+        dev.call("sfft_pack_rows", dptr(d_rows), n, d, dptr(out), dptr(mm), ctx="pack rows")
+        mmh = dev.download_small(mm).astype(np.int64)
+        if mmh[2 * d]:
+            raise ValueError("frequency components must satisfy |k_t| <= 2147483647")
+        lo, hi = mmh[:d], mmh[d:2 * d]
+        kmax = int(max(np.abs(lo).max(), np.abs(hi).max())) if n else 0
+        return cls(out, n, kmax), lo, hi
+
     def to_host(self, dev: Device) -> np.ndarray:
         return dev.download(self.data).T.astype(np.int64)
 
@@ -147,11 +166,13 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     attempt = 0
     for attempt, child in enumerate(seed_seq.spawn(b), start=1):
         rng = np.random.default_rng(child)
-        z = np.stack([rng.integers(0, m, size=t1, dtype=np.int64) for m in primes])
+        # one vectorised draw with per-row bounds == the reference's per-prime
+        # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
+        z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
         zh = np.ascontiguousarray(z.astype(np.int32))
         dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
-        stats_h = dev.download(stats)
+        stats_h = dev.download_small(stats)
         if int(stats_h[1]) == 0:
             return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0)
     return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]))
@@ -444,7 +465,7 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
             dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
                      dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
                      dptr(counts), ctx=f"gather/select, step {step}")
-    counts_h = dev.download(counts).astype(np.int64)
+    counts_h = dev.download_small(counts).astype(np.int64)
     over = [i for i in range(r) if counts_h[i] > cap]
     if over:
         sbytes = int(_native.query("sfft_select_scratch_bytes", n))
@@ -466,7 +487,7 @@ def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):
     sl = int(_native.query("sfft_scan_scratch_len", n))
     scr = dev.empty((max(sl, 1),), torch.int32)
     dev.call("sfft_flag_indices", dptr(flags), n, nrows, dptr(idx), dptr(total), dptr(scr), ctx="compaction")
-    cnt = int(dev.download(total)[0])
+    cnt = int(dev.download_small(total)[0])
     out = dev.empty((cand.ncomp, max(cnt, 1)), torch.int32)
     cout = dev.empty((max(cnt, 1), 2), torch.float64) if coef is not None else None
     dev.call("sfft_gather_rows", dptr(cand.data), n, cand.ncomp, dptr(idx), dptr(total), cnt, dptr(out),

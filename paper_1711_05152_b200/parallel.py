@@ -134,7 +134,7 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
         dev.call("sfft_combine_units", n, L, dptr(sch.masks), dptr(allrows), hptr(rmap), rb, rb, 0,
                  float(delta), dptr(coef[i0]), dptr(keep[i0]), dptr(counts[i0:]),
                  ctx=f"combine, step {step}")
-    counts_h = dev.download(counts).astype(np.int64)
+    counts_h = dev.download_small(counts).astype(np.int64)
     over = [i for i in range(r) if counts_h[i] > cap]
     if over:
         sbytes = int(_native.query("sfft_select_scratch_bytes", n))

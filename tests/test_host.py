@@ -148,6 +148,19 @@ class TestWorkloadsAndRng:
         one = [seq[1].integers(0, m, size=10, dtype=np.int64) for m in primes[:7]]
         assert all(np.array_equal(a, b) for a, b in zip(pre, one))
 
+    def test_vectorised_bounded_draw_is_stream_identical(self):
+        # build_scheme draws rng.integers(0, M[:, None], (L, d)) in one call; it
+        # must equal the reference's per-prime rng.integers(0, m, size=d) loop
+        for ms in ([2, 3, 5, 7, 11, 13], O.primes_above(100, 20), [2**31 - 1, 2**31 - 19, 2**30 + 3]):
+            ms = np.asarray(ms, dtype=np.int64)
+            for seed in range(3):
+                a = np.random.default_rng(seed)
+                b = np.random.default_rng(seed)
+                loop = np.stack([a.integers(0, m, size=7, dtype=np.int64) for m in ms])
+                vec = b.integers(0, ms[:, None], size=(len(ms), 7), dtype=np.int64)
+                assert np.array_equal(loop, vec)
+                assert a.random() == b.random()
+
     def test_spawn_is_stateful(self):
         ss = np.random.SeedSequence(1)
         a = ss.spawn(2)
