@@ -42,7 +42,7 @@ alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
 #pragma unroll
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
     for (int l = 0; l < lt.nlat; ++l) {
-      const int64_t r = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+      const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
       const int64_t w = bw[l] + (r >> 5);
       const uint32_t bit = 1u << (r & 31);
       const uint32_t old = atomicOr(&seen1[w], bit);
@@ -74,7 +74,7 @@ alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
     uint64_t mask = 0;
     for (int l = 0; l < lt.nlat; ++l) {
-      const int64_t r = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+      const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
       const uint32_t wv = __ldg(&seen2[bw[l] + (r >> 5)]);
       if (!((wv >> (r & 31)) & 1u)) mask |= (1ull << l);
     }

@@ -142,6 +142,23 @@ bool residue_fast(int t1, int64_t kmax, const int64_t* h_m, int L) {
   return bound < 4.0e15;  // < 2^52 with margin
 }
 
+// Enable the int32 residue path when every |k . z| < d * kmax * M < 2^31.
+void set_i32(LatTable& lt, int64_t kmax) {
+  int64_t mmax = 1;
+  for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
+  const double bound = (double)lt.d * (double)(kmax < 0 ? -kmax : kmax) * (double)mmax;
+  lt.i32 = bound < 2147483647.0 ? 1 : 0;
+  for (int l = 0; l < lt.nlat; ++l) {
+    lt.mu32[l] = (uint32_t)(0xFFFFFFFFull / (uint64_t)lt.m[l]);
+    lt.off32[l] = lt.i32 ? (uint32_t)(lt.m[l] * (int64_t)lt.d * (kmax < 0 ? -kmax : kmax)) : 0u;
+  }
+}
+
+bool fast_i32(LatTable& lt, int t1, int64_t kmax, const int64_t* h_m, int L) {
+  set_i32(lt, kmax);
+  return residue_fast(t1, kmax, h_m, L);
+}
+
 bool mulmod_fast(const int64_t* h_m, int L) {
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
@@ -173,27 +190,31 @@ int fill_bspline(BsplineSpec& bs, int ngroups, const int32_t* h_order, const int
 // memoised per M (the same primes recur across steps and calls)
 void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2);
 
-void choose_j1(int64_t m, int& j1, int& nt1, int& nt2) {
+void choose_j1_search(int64_t m, int tw2, int& j1, int& nt1, int& nt2);
+
+// tiles are 64 (j1) x tw2 (j2), tw2 = 64 (classic kernel) or 128 (warp-specialised)
+void choose_j1(int64_t m, int tw2, int& j1, int& nt1, int& nt2) {
   static std::mutex mu;
   static std::unordered_map<int64_t, int> memo;
+  const int64_t key = m * 2 + (tw2 == 128 ? 1 : 0);
   {
     std::lock_guard<std::mutex> g(mu);
-    auto itr = memo.find(m);
+    auto itr = memo.find(key);
     if (itr != memo.end()) {
       j1 = itr->second;
       nt1 = j1 / 64;
       const int64_t J2 = (m + j1 - 1) / j1;
-      nt2 = (int)((J2 + 63) / 64);
+      nt2 = (int)((J2 + tw2 - 1) / tw2);
       return;
     }
   }
-  choose_j1_search(m, j1, nt1, nt2);
+  choose_j1_search(m, tw2, j1, nt1, nt2);
   std::lock_guard<std::mutex> g(mu);
   if (memo.size() > 65536) memo.clear();
-  memo[m] = j1;
+  memo[key] = j1;
 }
 
-void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2) {
+void choose_j1_search(int64_t m, int tw2, int& j1, int& nt1, int& nt2) {
   int64_t best = -1;
   int bj = 64;
   const int64_t amax = (m + 63) / 64;
@@ -202,7 +223,7 @@ void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2) {
   for (int64_t a = 1; a <= alim; ++a) {
     const int64_t J1 = 64 * a;
     const int64_t J2 = (m + J1 - 1) / J1;
-    const int64_t padded = J1 * 64 * ((J2 + 63) / 64);
+    const int64_t padded = J1 * tw2 * ((J2 + tw2 - 1) / tw2);
     if (best < 0 || padded < best ||
         (padded == best && fabs((double)J1 - root) < fabs((double)bj - root))) {
       best = padded;
@@ -212,7 +233,17 @@ void choose_j1_search(int64_t m, int& j1, int& nt1, int& nt2) {
   j1 = bj;
   nt1 = bj / 64;
   const int64_t J2 = (m + bj - 1) / bj;
-  nt2 = (int)((J2 + 63) / 64);
+  nt2 = (int)((J2 + tw2 - 1) / tw2);
+}
+
+// polynomial sampling kernel: SFFT_B200_SAMPLE_KERNEL=classic|ws (default ws)
+int sample_kind() {
+  static int kind = [] {
+    const char* e = getenv("SFFT_B200_SAMPLE_KERNEL");
+    if (e && strcmp(e, "classic") == 0) return 0;
+    return 1;
+  }();
+  return kind;
 }
 
 // Tiles, K split and table split of the GEMM-factored polynomial sampling.
@@ -230,17 +261,22 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
   int bl = 1;
   while (((int64_t)1 << (2 * bl)) < mmax) ++bl;
   pp->bl = bl;
-  const size_t smem = sample_poly_smem(bl, mmax);
+  pp->kind = sample_kind();
+  if (pp->kind == 1 && sample_poly_ws_smem(bl, mmax) > 227 * 1024) pp->kind = 0;
+  const size_t smem = pp->kind == 1 ? sample_poly_ws_smem(bl, mmax) : sample_poly_smem(bl, mmax);
   if (smem > 227 * 1024) return E_2BIG;
-  // resident CTAs per SM: 2 by registers (256 threads x 128 regs), fewer if smem-bound
+  // resident CTAs per SM: classic 2 by registers (256 threads x 128 regs),
+  // warp-specialised 1 (384 threads x 168 regs); fewer if shared-memory-bound
+  const int reg_cap = pp->kind == 1 ? 1 : 2;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
-  if (per_sm > 2) per_sm = 2;
+  if (per_sm > reg_cap) per_sm = reg_cap;
   if (per_sm < 1) per_sm = 1;
+  const int tw2 = pp->kind == 1 ? 128 : 64;
   int64_t tiles_l[SFFT_LMAX];
   int64_t tiles_total = 0;
   for (int l = 0; l < L; ++l) {
     int j1, nt1, nt2;
-    choose_j1(h_m[l], j1, nt1, nt2);
+    choose_j1(h_m[l], tw2, j1, nt1, nt2);
     pp->J1[l] = j1;
     pp->nt1[l] = nt1;
     tiles_l[l] = (int64_t)nt1 * nt2;
@@ -352,7 +388,7 @@ int sfft_alias_masks(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, co
   const int64_t need = sfft_alias_scratch_words(h_m, L);
   if (scratch_words < need) return E_INVAL;
   return launch_alias(d_freqs, n, lt, d_scratch, need, d_masks, d_stats,
-                      residue_fast(t1, kmax, h_m, L), num_sms_current(), S(stream));
+                      fast_i32(lt, t1, kmax, h_m, L), num_sms_current(), S(stream));
 }
 
 int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp, void* stream) {
@@ -512,7 +548,7 @@ int sfft_gather_select(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, 
   int rc = fill_lat(lt, h_m, h_z, L, t1);
   if (rc) return rc;
   return launch_gather(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, rb, it0, delta,
-                       (double2*)d_coef, d_keep, d_counts, residue_fast(t1, kmax, h_m, L),
+                       (double2*)d_coef, d_keep, d_counts, fast_i32(lt, t1, kmax, h_m, L),
                        num_sms_current(), S(stream));
 }
 
@@ -528,7 +564,7 @@ int sfft_gather_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, c
   rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   return launch_gather_units(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, ut, (double2*)d_out,
-                             residue_fast(t1, kmax, h_m, L), num_sms_current(), S(stream));
+                             fast_i32(lt, t1, kmax, h_m, L), num_sms_current(), S(stream));
 }
 
 int sfft_combine_units(int64_t n, int L, const uint64_t* d_masks, const double* d_vals,
@@ -579,7 +615,7 @@ int sfft_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
   if (rc) return rc;
-  return launch_residues(d_freqs, n, lt, d_out, residue_fast(t1, kmax, h_m, L), num_sms_current(),
+  return launch_residues(d_freqs, n, lt, d_out, fast_i32(lt, t1, kmax, h_m, L), num_sms_current(),
                          S(stream));
 }
 

@@ -62,11 +62,27 @@ __device__ __forceinline__ int64_t mulmod(int64_t a, int64_t b, int64_t m, doubl
 }
 
 // Residue k . z mod M of one candidate (components in registers).
-// FAST requires sum_c |k_c| * z_c < 2^52 (host-checked).  Matches
-// reference lattice.py:511-517 (componentwise-reduced inner product).
+// FAST requires sum_c |k_c| * z_c < 2^52 (host-checked); with i32 != 0 the
+// host has also checked d * kmax * M < 2^31, and the sum runs in int32 plus a
+// 32-bit Barrett reduction of acc + off32 (off32 = M * d * kmax, a multiple of
+// M making the argument non-negative and < 2^32; mu32 = floor((2^32-1)/M),
+// quotient low by at most one).  Matches reference lattice.py:511-517
+// (componentwise-reduced inner product) exactly in every mode.
 template <int DM, bool FAST>
 __device__ __forceinline__ int64_t residue(const int32_t (&k)[DM], int d, const int32_t* z,
-                                           int64_t m, double inv_m) {
+                                           int64_t m, double inv_m, int i32 = 0,
+                                           uint32_t off32 = 0, uint32_t mu32 = 0) {
+  if (FAST && i32) {
+    int32_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < DM; ++c)
+      if (c < d) acc += k[c] * z[c];
+    const uint32_t x = (uint32_t)acc + off32;
+    const uint32_t mm = (uint32_t)m;
+    uint32_t r = x - __umulhi(x, mu32) * mm;
+    if (r >= mm) r -= mm;
+    return (int64_t)r;
+  }
   if (FAST) {
     int64_t acc = 0;
 #pragma unroll

@@ -50,7 +50,7 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
       while (mm) {
         const int l = __ffsll((long long)mm) - 1;
         mm &= mm - 1;
-        const int64_t r = residue<DM, FAST>(kv, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+        const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
         const double invm = 1.0 / (double)lt.m[l];
         ++cnt;
 #pragma unroll
@@ -168,7 +168,7 @@ gather_units_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
       const int l = ut.lat[j];
       double2 t = make_double2(0.0, 0.0);
       if ((mask >> l) & 1ull) {
-        const int64_t r = residue<DM, FAST>(kv, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+        const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
         const double invm = 1.0 / (double)lt.m[l];
         const double2 v = __ldg(&buf[(int64_t)j * ustride + r]);
         t = make_double2(__dmul_rn(v.x, invm), __dmul_rn(v.y, invm));
@@ -585,7 +585,7 @@ __global__ void residues_kernel(const int32_t* __restrict__ freqs, int64_t n, La
 #pragma unroll
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
     for (int l = 0; l < lt.nlat; ++l)
-      out[(int64_t)l * n + i] = residue<DM, FAST>(k, d, lt.z + l * d, lt.m[l], lt.inv_m[l]);
+      out[(int64_t)l * n + i] = SFFT_RES(DM, FAST, k, lt, l);
   }
 }
 

@@ -13,11 +13,19 @@ namespace sfft {
 struct LatTable {
   int nlat;
   int d;                      // length of each z (the candidates' dimension t+1)
+  int i32;                    // residues fit the int32 path (d * kmax * M < 2^31)
   int64_t m[SFFT_LMAX];
   double inv_m[SFFT_LMAX];
   int64_t off[SFFT_LMAX];     // offset of lattice l in the per-lattice tw/chirp tables
+  uint32_t off32[SFFT_LMAX];  // int32 path: M_l * d * kmax (non-negative shift, multiple of M_l)
+  uint32_t mu32[SFFT_LMAX];   // int32 path: floor((2^32 - 1) / M_l)
   int32_t z[SFFT_ZMAX];       // z[l * d + c], canonicalised into [0, M_l)
 };
+
+// residue of candidate k on lattice l of a LatTable (every exact mode)
+#define SFFT_RES(DM, FAST, k, lt, l)                                                       \
+  residue<DM, FAST>(k, (lt).d, (lt).z + (l) * (lt).d, (lt).m[l], (lt).inv_m[l], (lt).i32, \
+                    (lt).off32[l], (lt).mu32[l])
 
 // (iteration, lattice) work units of one step.
 struct UnitTable {

@@ -405,6 +405,20 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
   int64_t mmax = 1;
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
   const size_t smem = sample_poly_smem(pp.bl, mmax);
+  if (pp.kind == 1) {
+    int rc = launch_sample_poly_ws(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride, apply_chirp,
+                                   part, pstride, st);
+    if (rc) return rc;
+    if (pp.ks > 1) {
+      int bx = (int)((mmax + 255) / 256);
+      const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
+      if (bx > cap) bx = cap;
+      poly_split_reduce_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, pp.ks, part, pstride, chirp,
+                                                                    buf, ustride, apply_chirp ? 1 : 0);
+      SFFT_CHECK_LAUNCH();
+    }
+    return 0;
+  }
   if (pp.ks > 1) {
     cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

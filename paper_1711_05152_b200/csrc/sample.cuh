@@ -14,6 +14,7 @@ struct AnchorTable {
 struct PolyPlan {
   int nunits;
   int s;
+  int kind;  // 0: classic 64x64 tiles (sample.cu), 1: warp-specialised 64x128 tiles (sample_ws.cu)
   int bl;    // low bits of the two-level twiddle tables
   int ks;    // term slices per tile (K split)
   int kper;  // terms per slice (multiple of 16)
@@ -44,6 +45,11 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
                        bool apply_chirp, double2* part, int64_t pstride, int num_sms,
                        cudaStream_t st);
 size_t sample_poly_smem(int bl, int64_t mmax);
+size_t sample_poly_ws_smem(int bl, int64_t mmax);
+int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
+                          const int32_t* rres, const int32_t* rj, const double2* tw,
+                          const double2* chirp, double2* buf, int64_t ustride, bool apply_chirp,
+                          double2* part, int64_t pstride, cudaStream_t st);
 int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
                           const AnchorTable& at, const double2* chirp, double2* buf,
                           int64_t ustride, bool fast, bool apply_chirp, int num_sms,
