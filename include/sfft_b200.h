@@ -121,6 +121,16 @@ int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_st
 int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp,
                         double* d_buf, int64_t P, const double* d_noise, int64_t nstride,
                         const double* d_sigma, const int32_t* h_units, int nunits, void* stream);
+/* Device-generated noise (statistically equivalent to NoisyOracle; realisation
+ * from Philox4x32-10 keyed by seed, counter (n, oracle-call index), so it is
+ * reproducible and independent of launch splits / GPU counts): unit u (global
+ * id g = it * L + l) is oracle call call_base + g; its samples get
+ * s_u * (N(0,1) + i N(0,1)) with s_u = sigma / sqrt(2), or, when d_norm2 is
+ * given, rel * sqrt(d_norm2[u] / M_l) / sqrt(2); then the optional pre-chirp. */
+int sfft_finish_devnoise(const int64_t* h_m, int L, int rb, const double* d_chirp, double* d_buf,
+                         int64_t P, const double* d_norm2, double rel, double sigma, uint64_t seed,
+                         uint64_t call_base, int apply_chirp, const int32_t* h_units, int nunits,
+                         void* stream);
 /* sum_n |x_n|^2 per unit over n < M (relative-SNR noise calibration). */
 int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
                     double* d_out, const int32_t* h_units, int nunits, void* stream);

@@ -38,6 +38,8 @@ _SIGS = {
                                    _vp, _vp, _i64, _int, _vp, _int, _vp]),
     "sfft_finish_samples": (_int, [_vp, _int, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _int, _vp]),
     "sfft_unit_norm2": (_int, [_vp, _int, _int, _vp, _i64, _vp, _vp, _int, _vp]),
+    "sfft_finish_devnoise": (_int, [_vp, _int, _int, _vp, _vp, _i64, _vp, _dbl, _dbl, C.c_uint64, C.c_uint64,
+                                    _int, _vp, _int, _vp]),
     "sfft_lattice_nodes": (_int, [_vp, _vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "sfft_gather_select": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp, _i64, _int, _int,
                                   _dbl, _vp, _vp, _vp, _vp]),

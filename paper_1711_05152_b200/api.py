@@ -178,17 +178,16 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     n, t1 = (int(x) for x in host_rows.shape)
     d = oracle.dim
     tail = np.zeros(d - t1) if anchor_tail is None else np.asarray(anchor_tail, dtype=np.float64)
-    if seed_seq is None:
-        seed_seq = np.random.SeedSequence(0)
-    elif not isinstance(seed_seq, np.random.SeedSequence):
-        seed_seq = np.random.SeedSequence(seed_seq)
+    fresh = not isinstance(seed_seq, np.random.SeedSequence)
+    if fresh:
+        seed_seq = np.random.SeedSequence(0 if seed_seq is None else seed_seq)
     cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows)
     h2d = n * t1 * 8
     if hasattr(oracle, "device_terms"):
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
-    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()))
+    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh)
     res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap))
     coef, keep, words = dev.download_many(res.coef[0], res.keep[0], sch.masks)
     d2h = coef.nbytes + keep.nbytes + words.nbytes

@@ -518,6 +518,17 @@ int sfft_finish_samples(const int64_t* h_m, int L, int rb, const double* d_chirp
                                S(stream));
 }
 
+int sfft_finish_devnoise(const int64_t* h_m, int L, int rb, const double* d_chirp, double* d_buf,
+                         int64_t P, const double* d_norm2, double rel, double sigma, uint64_t seed,
+                         uint64_t call_base, int apply_chirp, const int32_t* h_units, int nunits,
+                         void* stream) {
+  UnitTable ut;
+  int rc = fill_units(ut, h_m, L, rb, h_units, nunits);
+  if (rc) return rc;
+  return launch_finish_devnoise(ut, (const double2*)d_chirp, (double2*)d_buf, P, d_norm2, rel, sigma,
+                                seed, call_base, apply_chirp != 0, num_sms_current(), S(stream));
+}
+
 int sfft_unit_norm2(const int64_t* h_m, int L, int rb, const double* d_buf, int64_t P,
                     double* d_out, const int32_t* h_units, int nunits, void* stream) {
   UnitTable ut;

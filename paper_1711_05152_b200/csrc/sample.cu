@@ -330,6 +330,75 @@ __global__ void finish_samples_kernel(UnitTable ut, const double2* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device noise (counter-based, reproducible for any launch split / GPU count):
+// Philox4x32-10 keyed by the oracle seed, counter (sample n, oracle-call
+// index); Box-Muller gives one complex N(0,1) + i N(0,1) sample per counter.
+// The call index is the position of the oracle call in the reference's call
+// order (testbed.py:100-106 draws per call), so unit u of a chunk is call
+// call_base + (global unit id).
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ double2 normal2(uint64_t seed, uint64_t call, uint64_t n) {
+  uint32_t c[4] = {(uint32_t)n, (uint32_t)(n >> 32), (uint32_t)call, (uint32_t)(call >> 32)};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t a = ((uint64_t)c[0] << 32 | c[1]) >> 11;
+  const uint64_t b = ((uint64_t)c[2] << 32 | c[3]) >> 11;
+  const double u1 = ((double)a + 1.0) * 0x1.0p-53;  // (0, 1]
+  const double u2 = (double)b * 0x1.0p-53;          // [0, 1)
+  const double rad = sqrt(-2.0 * log(u1));
+  double s, co;
+  sincospi(2.0 * u2, &s, &co);
+  return make_double2(rad * co, rad * s);
+}
+
+// x_n <- (x_n + s_u * (g_re + i g_im)) * chirp_n: s_u = sigma / sqrt(2) (fixed) or
+// rel * sqrt(norm2_u / M) / sqrt(2) (relative to the noise-free vector)
+__global__ void finish_devnoise_kernel(UnitTable ut, const double2* __restrict__ chirp,
+                                       double2* __restrict__ buf, int64_t ustride,
+                                       const double* __restrict__ norm2, double rel, double sigma,
+                                       uint64_t seed, uint64_t call_base, int apply_chirp) {
+  const int u = blockIdx.y;
+  const int l = ut.lat[u];
+  const int64_t M = ut.m[l];
+  const double2* ch = chirp + ut.off[l];
+  double2* ub = buf + (int64_t)u * ustride;
+  const uint64_t call = call_base + (uint64_t)(ut.it[u] * ut.nlat + l);
+  const double sg = (norm2 ? rel * sqrt(norm2[u] / (double)M) : sigma) * 0.70710678118654752440;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const double2 e = normal2(seed, call, (uint64_t)n);
+    double2 v = ub[n];
+    v = make_double2(v.x + sg * e.x, v.y + sg * e.y);
+    ub[n] = apply_chirp ? cmul(v, __ldg(&ch[n])) : v;
+  }
+}
+
+int launch_finish_devnoise(const UnitTable& ut, const double2* chirp, double2* buf, int64_t ustride,
+                           const double* norm2, double rel, double sigma, uint64_t seed,
+                           uint64_t call_base, bool apply_chirp, int num_sms, cudaStream_t st) {
+  int64_t mmax = 1;
+  for (int l = 0; l < ut.nlat; ++l) mmax = ut.m[l] > mmax ? ut.m[l] : mmax;
+  int bx = (int)((mmax + 255) / 256);
+  const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
+  if (bx > cap) bx = cap;
+  finish_devnoise_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, chirp, buf, ustride, norm2, rel, sigma,
+                                                              seed, call_base, apply_chirp ? 1 : 0);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
 // squared 2-norm of each unit's first M samples (for relative-noise oracles)
 __global__ void unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf, int64_t ustride,
                                   double* __restrict__ out) {

@@ -57,6 +57,9 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
 int launch_finish_samples(const UnitTable& ut, const double2* chirp, double2* buf, int64_t ustride,
                           const double2* noise, int64_t nstride, const double* sigma, int num_sms,
                           cudaStream_t st);
+int launch_finish_devnoise(const UnitTable& ut, const double2* chirp, double2* buf, int64_t ustride,
+                           const double* norm2, double rel, double sigma, uint64_t seed,
+                           uint64_t call_base, bool apply_chirp, int num_sms, cudaStream_t st);
 int launch_unit_norm2(const UnitTable& ut, const double2* buf, int64_t ustride, double* out,
                       int num_sms, cudaStream_t st);
 int launch_lattice_nodes(const LatTable& lt, int l, int d, const AnchorTable& at, int it,

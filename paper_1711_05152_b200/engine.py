@@ -174,7 +174,18 @@ def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarra
         with torch.cuda.stream(dev.stream):
             vals.copy_(torch.from_numpy(host))
         return vals
-    if noisy:
+    if noisy and oracle.device_rng:
+        km = np.array([K], dtype=np.int64)
+        base_call = oracle.reserve_calls(r)
+        nrm = None
+        if oracle.needs_norm():
+            nrm = dev.empty((r,), torch.float64)
+            dev.call("sfft_unit_norm2", hptr(km), 1, r, dptr(vals), K, dptr(nrm), 0, 0, ctx="line noise norm")
+        dev.call("sfft_finish_devnoise", hptr(km), 1, r, dptr(vals), dptr(vals), K,
+                 dptr(nrm) if nrm is not None else 0, getattr(oracle, "rel", 0.0), oracle.sigma,
+                 oracle.device_key, base_call, 0, 0, 0, ctx="line device noise")
+        oracle.count_samples(r * K)
+    elif noisy:
         norms = None
         if oracle.needs_norm():
             nrm = dev.empty((r,), torch.float64)
@@ -315,8 +326,8 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             rep.prefix_counts[t] = 0
             rep.step_times.append(time.perf_counter() - t_step)
             continue
-        sch = build_scheme(dev, cand, cfg.b, lattice_streams[t],
-                           box_extent=int(extents[: t + 1].max()), ctx=f"lattice search, step {t}")
+        sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
+                           ctx=f"lattice search, step {t}", lazy_streams=True)
         rep.scheme_sizes[t] = sch.total_size
         rep.lattice_attempts[t] = sch.attempts
         rep.inversion_calls[t] = r_tilde * sch.total_size

@@ -132,9 +132,25 @@ def _spread_bound(cand: DeviceFreqs, box_extent: int | None) -> int:
     return 2 * cand.kmax
 
 
+def _attempt_streams(seed_seq: np.random.SeedSequence, b: int, lazy: bool):
+    """The b child streams of construct.py:202 (``seed_seq.spawn(b)``).
+
+    ``lazy``: build each child only when its attempt runs (identical streams;
+    ~10x cheaper, since one attempt is the norm) without advancing
+    ``seed_seq``'s spawn counter — for parents that are never spawned again
+    (the engine's per-step lattice streams, fresh per-call seeds)."""
+    if not lazy:
+        yield from seed_seq.spawn(b)
+        return
+    base = seed_seq.n_children_spawned
+    for i in range(b):
+        yield np.random.SeedSequence(seed_seq.entropy, spawn_key=seed_seq.spawn_key + (base + i,),
+                                     pool_size=seed_seq.pool_size)
+
+
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
-                 ctx: str = "") -> DeviceScheme:
+                 ctx: str = "", lazy_streams: bool = False) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -164,7 +180,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     z = None
     stats_h = None
     attempt = 0
-    for attempt, child in enumerate(seed_seq.spawn(b), start=1):
+    for attempt, child in enumerate(_attempt_streams(seed_seq, b, lazy_streams), start=1):
         rng = np.random.default_rng(child)
         # one vectorised draw with per-row bounds == the reference's per-prime
         # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
@@ -373,6 +389,18 @@ def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb
     nu = len(ulist)
     up = hptr(uarr) if uarr is not None else 0
     nuarg = len(uarr) if uarr is not None else 0
+    if oracle.device_rng:
+        base = oracle.reserve_calls(rb * L)
+        nrm = None
+        if oracle.needs_norm():
+            nrm = dev.empty((nu,), torch.float64)
+            dev.call("sfft_unit_norm2", hptr(tabs.ms), L, rb, dptr(buf), P, dptr(nrm), up, nuarg,
+                     ctx="noise norm")
+        dev.call("sfft_finish_devnoise", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P,
+                 dptr(nrm) if nrm is not None else 0, getattr(oracle, "rel", 0.0), oracle.sigma,
+                 oracle.device_key, base, 1, up, nuarg, ctx="device noise")
+        oracle.count_samples(sum(int(tabs.ms[u % L]) for u in ulist))
+        return
     norms = {}
     if oracle.needs_norm():
         nrm = dev.empty((nu,), torch.float64)

@@ -302,7 +302,12 @@ class NoisyOracle:
 
     kind = "noisy"
 
-    def __init__(self, inner, sigma: float, seed=0):
+    def __init__(self, inner, sigma: float, seed=0, *, device_rng: bool = False):
+        """``device_rng=True`` generates the noise on the GPU (Philox keyed by
+        the seed and the call index) instead of drawing the numpy stream: the
+        same distribution, a different realisation, no host RNG or upload —
+        for runs whose sample counts make the host stream the bottleneck
+        (BASELINE config 3: 1.4e9 samples)."""
         if sigma < 0:
             raise ValueError("sigma must be >= 0")
         self.inner = inner
@@ -312,6 +317,17 @@ class NoisyOracle:
         self._rng = np.random.default_rng(seed)
         self._lock = threading.Lock()
         self._counter = _Counter()
+        self.device_rng = bool(device_rng)
+        ss = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+        self.device_key = int(ss.generate_state(1, np.uint64)[0])
+        self._next_call = 0
+
+    def reserve_calls(self, n: int) -> int:
+        """Index of the first of the next n oracle calls (device-noise counter)."""
+        with self._lock:
+            base = self._next_call
+            self._next_call += int(n)
+        return base
 
     @property
     def call_count(self) -> int:
@@ -354,8 +370,8 @@ class RelativeNoisyOracle(NoisyOracle):
     in expectation, per oracle call (BASELINE config 3: rel = 1e-2):
     sigma_call = rel * ||p(X)||_2 / sqrt(n)."""
 
-    def __init__(self, inner, rel: float = 1e-2, seed=0):
-        super().__init__(inner, 0.0, seed)
+    def __init__(self, inner, rel: float = 1e-2, seed=0, *, device_rng: bool = False):
+        super().__init__(inner, 0.0, seed, device_rng=device_rng)
         if rel < 0:
             raise ValueError("rel must be >= 0")
         self.rel = float(rel)

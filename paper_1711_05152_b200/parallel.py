@@ -90,9 +90,12 @@ def _local_rows(dev, oracle, cand, sch, tabs, tails_chunk, d, step, i0, world, r
                  dptr(sch.masks), dptr(buf), P, rb, hptr(uarr), len(mine), dptr(rows),
                  ctx=f"unit gather, step {step}")
     elif isinstance(oracle, NoisyOracle):
-        # keep this rank's copy of the noise stream aligned with the others
-        for u in range(U):
-            oracle.draw(int(tabs.ms[u % L]))
+        # keep this rank's copy of the noise stream / call counter aligned
+        if oracle.device_rng:
+            oracle.reserve_calls(U)
+        else:
+            for u in range(U):
+                oracle.draw(int(tabs.ms[u % L]))
     return rows, nodes
 
 

@@ -88,10 +88,13 @@ def config2(seed: int = 0, trial: int = 0, r: int = 5) -> Workload:
     return Workload(f"config2 d=10 N=32 s=1000 r={r}", oracle, cfg, truth)
 
 
-def config3(seed: int = 0, trial: int = 0, d: int = 20, s: int = 10_000, r: int = 5) -> Workload:
+def config3(seed: int = 0, trial: int = 0, d: int = 20, s: int = 10_000, r: int = 5,
+            device_rng: bool = False) -> Workload:
+    """``device_rng``: GPU-generated noise (same distribution, not the numpy
+    realisation); the default draws the reference-compatible numpy stream."""
     ts, rs, ns = seeds_for(seed, 3, trial)
     truth, poly = gen_random_sparse_poly(d, 32, s, "polar", seed=ts)
-    oracle = RelativeNoisyOracle(poly, 1e-2, seed=ns)
+    oracle = RelativeNoisyOracle(poly, 1e-2, seed=ns, device_rng=device_rng)
     box = SearchBox.centered(d, 32, check_cardinality=False)
     cfg = DetectionConfig(box=box, delta=1e-1, s=s, r=r, b=10, rng_seed=rs)
     return Workload(f"config3 d={d} N=32 s={s} r={r} noisy 1e-2", oracle, cfg, truth)

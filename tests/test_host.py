@@ -161,6 +161,14 @@ class TestWorkloadsAndRng:
                 assert np.array_equal(loop, vec)
                 assert a.random() == b.random()
 
+    def test_lazy_attempt_streams_equal_spawn(self):
+        from paper_1711_05152_b200.mr1l import _attempt_streams
+        for parent in (np.random.SeedSequence(7), np.random.SeedSequence(3).spawn(4)[2]):
+            eager = [np.random.default_rng(c).integers(0, 1 << 40, 5) for c in
+                     np.random.SeedSequence(parent.entropy, spawn_key=parent.spawn_key).spawn(10)]
+            lazy = [np.random.default_rng(c).integers(0, 1 << 40, 5) for c in _attempt_streams(parent, 10, True)]
+            assert all(np.array_equal(a, b) for a, b in zip(eager, lazy))
+
     def test_spawn_is_stateful(self):
         ss = np.random.SeedSequence(1)
         a = ss.spawn(2)

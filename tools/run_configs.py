@@ -29,6 +29,8 @@ def main():
             wl = workloads.Workload("config2 survey instance (seed 42 / 43)", oracle, cfg, truth)
         elif c == "3":
             wl = workloads.config3()
+        elif c == "3d":  # device-generated noise
+            wl = workloads.config3(device_rng=True)
         elif c == "4":
             wl = workloads.config4()
         else:
