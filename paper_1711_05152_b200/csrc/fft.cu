@@ -108,7 +108,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   double2* ub = buf + (int64_t)u * ustride;
 
   // load (coalesced along columns), transpose into rows of length P1
-#pragma unroll 4
+#pragma unroll
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int c = f % C, n1 = f / C;
     const int64_t n = (int64_t)n1 * P2 + c0 + c;
@@ -120,7 +120,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   __syncthreads();
   block_fft<LOG1, INV>(s, ftab + g.off_p1);
   if (!INV) {
-#pragma unroll 4
+#pragma unroll
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int c = f % C, k1 = f / C;
       const int64_t n2 = c0 + c;
@@ -130,7 +130,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     }
   } else {
     const double2* ch = chirp + ut.off[lat];
-#pragma unroll 4
+#pragma unroll
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int c = f % C, n1 = f / C;
       const int64_t n = (int64_t)n1 * P2 + c0 + c;
@@ -158,7 +158,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   const int g0 = blockIdx.x * rows;
   const bool single = (P1 == 1);
 
-#pragma unroll 4
+#pragma unroll
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
@@ -175,7 +175,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   block_fft<LOG2, false>(s, ftab + g.off_p2);
   if (MODE == 1) {
     const double scale = 1.0 / (double)g.P;  // exact: P is a power of two
-#pragma unroll 4
+#pragma unroll
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int r = f / P2, i = f % P2;
       const int grow = g0 + r;
@@ -188,7 +188,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     return;
   }
   // pointwise product with Bhat (same layout)
-#pragma unroll 4
+#pragma unroll
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
@@ -202,7 +202,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   }
   __syncthreads();
   block_fft<LOG2, true>(s, ftab + g.off_p2);
-#pragma unroll 4
+#pragma unroll
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;

@@ -91,7 +91,7 @@ def main():
                                              "dram_pct": float(dram) if dram else None})
         summary["full_capture"] = per
         for name, lst in per.items():
-            if "sample_poly_kernel" in name:
+            if name.startswith("sample_poly") and "reduce" not in name:
                 summary["sample_poly_dram_bytes"] = lst[0]["dram_bytes"]
         print(json.dumps(per, indent=1))
     summary_path.write_text(json.dumps(summary, indent=1))
