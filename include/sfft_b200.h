@@ -199,6 +199,17 @@ int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,
 /* d_x[i] += scale * d_noise[i] (complex; NoisyOracle update, testbed.py:104-106) */
 int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, void* stream);
 
+/* ---- single rank-1 lattice (Algorithm 5; construct.py:212-278, transform.py:67-96)
+ * CBC scan: d_dup[j] = 1 iff (prefix_res_i + col_i * (z0 + j)) mod m has a
+ * repeated value over i < n (d_bits: Z * words scratch, words >= ceil(m/32)).
+ * prefix_flags: first row of every distinct t1-prefix of a sorted set.
+ * scatter_residues: acc[k . z mod m] += coef_k (eval_on_lattice). */
+int sfft_cbc_scan(const int64_t* d_prefix_res, const int32_t* d_col, int64_t n, int64_t m, int64_t z0,
+                  int Z, uint32_t* d_bits, int64_t words, int32_t* d_dup, void* stream);
+int sfft_prefix_flags(const int32_t* d_freqs, int64_t n, int t1, uint8_t* d_flags, void* stream);
+int sfft_scatter_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t m, const int32_t* h_z,
+                          const double* d_coef, double* d_acc, void* stream);
+
 /* ---- utilities ---------------------------------------------------------------- */
 /* numpy rows (n x d int64, row-major) -> component-major int32 candidates;
  * d_minmax (2d + 1 int32): per-component min, max, and an out-of-range flag

@@ -135,6 +135,49 @@ def build_with_retries(freqs: np.ndarray, b: int, seed_seq: np.random.SeedSequen
 
 
 # ---------------------------------------------------------------------------
+# single lattice, component by component (construct.py:212-278)
+
+
+def cbc(freqs: np.ndarray) -> tuple[np.ndarray, int]:
+    """Smallest odd M >= |I| and smallest z_t per component separating all
+    distinct prefixes (construct.py:254-278); freqs lexicographically sorted."""
+    n, d = freqs.shape
+    if n == 1:
+        return np.zeros(d, dtype=np.int64), 1
+    m = n if n % 2 == 1 else n + 1
+    while True:
+        z = np.zeros(d, dtype=np.int64)
+        z[0] = 1 % m
+        ok = True
+        if d == 1:
+            ok = len(np.unique(freqs[:, 0] % m)) == n
+        for t in range(1, d):
+            rows = np.unique(freqs[:, :t + 1], axis=0)
+            pres = residues(rows[:, :t], z[:t], m)
+            col = rows[:, t] % m
+            found = None
+            for start in range(0, m, 4096):
+                cand = np.arange(start, min(start + 4096, m), dtype=np.int64)
+                res = np.sort((pres[:, None] + col[:, None] * cand[None, :]) % m, axis=0)
+                good = np.flatnonzero(np.all(res[1:] != res[:-1], axis=0))
+                if len(good):
+                    found = int(cand[good[0]])
+                    break
+            if found is None:
+                ok = False
+                break
+            z[t] = found
+        if ok:
+            return z, m
+        m += 2
+
+
+def invert_single(freqs: np.ndarray, z: np.ndarray, m: int, values: np.ndarray) -> np.ndarray:
+    """transform.py:83-96: X[k.z mod M] / M for every k."""
+    return (np.fft.fft(values) / m)[residues(freqs, z, m)]
+
+
+# ---------------------------------------------------------------------------
 # inversion (transform.py:99-127) and selection (detect.py:197-212)
 
 
@@ -292,7 +335,8 @@ class Report:
 
 
 def sparse_fft(fn, lows, highs, delta: float, s: int, r: int = 1, b: int = 1, rng_seed: int = 0,
-               s_local: int | None = None, zero_anchor: bool = False, component_delta: float | None = None):
+               s_local: int | None = None, zero_anchor: bool = False, component_delta: float | None = None,
+               single: bool = False):
     """Algorithm 3 with the reference's RNG-stream contract (detect.py:305-423)."""
     t0 = time.perf_counter()
     lows = np.asarray(lows, dtype=np.int64)
@@ -336,7 +380,11 @@ def sparse_fft(fn, lows, highs, delta: float, s: int, r: int = 1, b: int = 1, rn
         if not len(cand):
             prefixes = cand
             continue
-        sch = build_with_retries(cand, b, lat_s[t])
+        if single:
+            zc, mc = cbc(cand)
+            sch = Scheme([mc], [zc], [np.ones(len(cand), dtype=bool)])
+        else:
+            sch = build_with_retries(cand, b, lat_s[t])
         rep.schemes.append(sch)
         rep.scheme_sizes[t] = sch.total_size
         rep.attempts[t] = sch.attempts

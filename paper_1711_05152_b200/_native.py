@@ -57,6 +57,9 @@ _SIGS = {
     "sfft_eval_poly_points": (_int, [_vp, _i64, _int, _vp, _vp, _int, _vp, _vp]),
     "sfft_eval_bspline_points": (_int, [_vp, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sfft_add_noise": (_int, [_vp, _vp, _i64, _dbl, _vp]),
+    "sfft_cbc_scan": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp, _i64, _vp, _vp]),
+    "sfft_prefix_flags": (_int, [_vp, _i64, _int, _vp, _vp]),
+    "sfft_scatter_residues": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _vp, _vp]),
     "sfft_pack_rows": (_int, [_vp, _i64, _int, _vp, _vp, _vp]),
     "sfft_cscale": (_int, [_vp, _i64, _dbl, _int, _vp]),
     "sfft_fp64_peak": (_int, [_vp, _int, _int, _vp]),

@@ -14,6 +14,12 @@
 #include "sample.cuh"
 
 namespace sfft {
+int launch_cbc_scan(const int64_t* prefix_res, const int32_t* col, int64_t n, int64_t m, int64_t z0,
+                    int Z, uint32_t* bits, int64_t words, int32_t* dup, int num_sms, cudaStream_t st);
+int launch_prefix_flags(const int32_t* freqs, int64_t n, int t1, uint8_t* flags, int num_sms,
+                        cudaStream_t st);
+int launch_scatter_residues(const int32_t* freqs, int64_t n, const LatTable& lt, const double2* coef,
+                            double2* acc, int num_sms, cudaStream_t st);
 int launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t st);
 int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* hf,
                             const double2* coef, int s, double2* out, cudaStream_t st);
@@ -666,6 +672,28 @@ int sfft_add_noise(double* d_x, const double* d_noise, int64_t n, double scale, 
   if (n < 0) return E_INVAL;
   return launch_add_noise((double2*)d_x, (const double2*)d_noise, n, scale, num_sms_current(),
                           S(stream));
+}
+
+int sfft_cbc_scan(const int64_t* d_prefix_res, const int32_t* d_col, int64_t n, int64_t m, int64_t z0,
+                  int Z, uint32_t* d_bits, int64_t words, int32_t* d_dup, void* stream) {
+  if (n < 0 || m < 1 || m > 2147483647LL || Z < 0 || words < (m + 31) / 32) return E_INVAL;
+  return launch_cbc_scan(d_prefix_res, d_col, n, m, z0, Z, d_bits, words, d_dup, num_sms_current(),
+                         S(stream));
+}
+
+int sfft_prefix_flags(const int32_t* d_freqs, int64_t n, int t1, uint8_t* d_flags, void* stream) {
+  if (n < 0 || t1 < 1) return E_INVAL;
+  return launch_prefix_flags(d_freqs, n, t1, d_flags, num_sms_current(), S(stream));
+}
+
+int sfft_scatter_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t m, const int32_t* h_z,
+                          const double* d_coef, double* d_acc, void* stream) {
+  if (n < 0 || t1 < 1) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, &m, h_z, 1, t1);
+  if (rc) return rc;
+  return launch_scatter_residues(d_freqs, n, lt, (const double2*)d_coef, (double2*)d_acc,
+                                 num_sms_current(), S(stream));
 }
 
 int sfft_pack_rows(const int64_t* d_rows, int64_t n, int d, int32_t* d_out, int32_t* d_minmax,

@@ -268,10 +268,6 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
     sharded = sh.active and shard is not False
     if getattr(oracle, "dim", cfg.box.dim) != cfg.box.dim:
         raise ValueError("oracle dimension does not match the search box")
-    if cfg.lattice_kind != "multiple":
-        raise NotImplementedError(
-            "lattice_kind='single' (Algorithm 5, CBC single lattice) is outside the B200 MR1L path"
-        )
     dev = device or get_device()
     box = cfg.box
     order = cfg.dimension_order
@@ -326,8 +322,12 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             rep.prefix_counts[t] = 0
             rep.step_times.append(time.perf_counter() - t_step)
             continue
-        sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
-                           ctx=f"lattice search, step {t}", lazy_streams=True)
+        if cfg.lattice_kind == "single":
+            from .single import single_scheme
+            sch = single_scheme(dev, cand)  # CBC (reference detect.py:269-271), no RNG consumed
+        else:
+            sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
+                               ctx=f"lattice search, step {t}", lazy_streams=True)
         rep.scheme_sizes[t] = sch.total_size
         rep.lattice_attempts[t] = sch.attempts
         rep.inversion_calls[t] = r_tilde * sch.total_size

@@ -197,8 +197,34 @@ def bspline_fixture(out):
     out["bsv_cm"] = np.array([sfft.bspline_l2_constant(m) for m in (2, 4, 6)])
 
 
+def single_fixture(out):
+    """Algorithm 5 path: CBC lattices, invert_single / eval_on_lattice, a run."""
+    rng = np.random.default_rng(8)
+    for i, (n, d, N) in enumerate(((1, 3, 4), (7, 1, 20), (40, 2, 6), (90, 3, 5), (60, 4, 3))):
+        rows = np.unique(rng.integers(-N, N + 1, size=(n, d)), axis=0)
+        lat = sfft.build_single_lattice_cbc(sfft.FrequencyIndexSet(rows))
+        out[f"cbc{i}_rows"] = rows
+        out[f"cbc{i}_z"] = lat.z
+        out[f"cbc{i}_m"] = np.array([lat.m])
+    rows = out["cbc3_rows"]
+    lat = sfft.Rank1Lattice(out["cbc3_z"], int(out["cbc3_m"][0]))
+    coef = rng.normal(size=len(rows)) + 1j * rng.normal(size=len(rows))
+    spec = sfft.SparseSpectrum(rows, coef)
+    samples = sfft.eval_on_lattice(spec, lat)
+    out["single_eval"] = samples.values
+    out["single_inv"] = sfft.invert_single(samples, spec.support()).coeffs
+    out["single_coef"] = spec.coeffs
+    rng = np.random.default_rng(45)
+    truth, _ = sfft.gen_random_sparse_poly(3, 8, 15, "box", seed=rng)
+    out.update(sk_hf=truth.freqs, sk_hc=truth.coeffs)
+    run_fixture(out, "sk", _poly_signal(truth.freqs, truth.coeffs),
+                sfft.DetectionConfig(box=sfft.SearchBox.centered(3, 8), delta=1e-12, s=15, r=1, b=10, rng_seed=9,
+                                     lattice_kind="single"))
+
+
 def main():
     out: dict = {}
+    single_fixture(out)
     residues_fixture(out)
     primes_fixture(out)
     transform_fixture(out)

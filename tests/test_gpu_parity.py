@@ -220,6 +220,27 @@ def test_sparse_fft_bspline(P, golden):
     assert abs(err - float(golden["bs_l2err"][0])) <= 1e-4 * float(golden["bs_l2err"][0])
 
 
+def test_single_lattice_path(P, golden):
+    """Algorithm 5: CBC lattices bit-exact, eval_on_lattice / invert_single,
+    and a lattice_kind='single' run (reference construct.py:212-278,
+    transform.py:67-96, detect.py:269-271)."""
+    for i in range(5):
+        lat = P.build_single_lattice_cbc(P.FrequencyIndexSet(golden[f"cbc{i}_rows"]))
+        assert lat.m == int(golden[f"cbc{i}_m"][0]) and np.array_equal(lat.z, golden[f"cbc{i}_z"])
+    rows = golden["cbc3_rows"]
+    lat = P.Rank1Lattice(golden["cbc3_z"], int(golden["cbc3_m"][0]))
+    spec = P.SparseSpectrum(rows, golden["single_coef"])
+    samples = P.eval_on_lattice(spec, lat)
+    ref = golden["single_eval"]
+    assert np.abs(samples.values - ref).max() <= 1e-12 * np.abs(ref).max()
+    inv = P.invert_single(P.LatticeSamples(lat, ref), spec.support())
+    assert np.abs(inv.coeffs - golden["single_inv"]).max() <= 1e-12
+    oracle = P.SparsePolynomialOracle(golden["sk_hf"], golden["sk_hc"])
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(3, 8), delta=1e-12, s=15, r=1, b=10, rng_seed=9,
+                            lattice_kind="single")
+    _check_report(golden, "sk", P.sparse_fft(oracle, cfg))
+
+
 def test_bspline_points(P, golden):
     f = P.bspline_test_function()
     got = f(golden["bsv_pts"])

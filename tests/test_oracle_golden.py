@@ -130,6 +130,19 @@ def test_engine_caps_zero_anchor_1d(golden):
     _check_run(golden, "one", rep)
 
 
+def test_cbc_and_single_path(golden):
+    for i in range(5):
+        z, m = O.cbc(golden[f"cbc{i}_rows"])
+        assert m == int(golden[f"cbc{i}_m"][0]) and np.array_equal(z, golden[f"cbc{i}_z"])
+    rows = golden["cbc3_rows"]
+    got = O.invert_single(rows, golden["cbc3_z"], int(golden["cbc3_m"][0]), golden["single_eval"])
+    assert np.abs(got - golden["single_inv"]).max() <= 1e-13
+    f, c = golden["sk_hf"], golden["sk_hc"]
+    rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-8] * 3, [8] * 3, 1e-12, 15, r=1, b=10, rng_seed=9,
+                       single=True)
+    _check_run(golden, "sk", rep)
+
+
 def test_engine_noisy(golden):
     f, c = golden["noisy_hf"], golden["noisy_hc"]
     rng = np.random.default_rng(123)
