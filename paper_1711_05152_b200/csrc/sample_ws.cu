@@ -167,22 +167,25 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
     const double2* Bs = As + KC * TJ1;
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
-      double2 a[4];
+      double2 a[4], b[8];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = As[kk * TJ1 + tx + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double2 b = Bs[kk * TJ2 + ty + 16 * j];
-        // two half-passes so that dependent DFMAs on one accumulator are 8 apart
+      for (int j = 0; j < 8; ++j) b[j] = Bs[kk * TJ2 + ty + 16 * j];
+      // row-major order: 16 consecutive DFMAs share one A component (operand
+      // reuse; measured +9% DFMA issue rate over column order, tools/mb_dfma.cu),
+      // dependent DFMAs on one accumulator are 16 apart
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][j].x = fma(a[i].x, b.x, acc[i][j].x);
-          acc[i][j].y = fma(a[i].x, b.y, acc[i][j].y);
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[i][j].x = fma(a[i].x, b[j].x, acc[i][j].x);
+          acc[i][j].y = fma(a[i].x, b[j].y, acc[i][j].y);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][j].x = fma(-a[i].y, b.y, acc[i][j].x);
-          acc[i][j].y = fma(a[i].y, b.x, acc[i][j].y);
+        for (int j = 0; j < 8; ++j) {
+          acc[i][j].x = fma(-a[i].y, b[j].y, acc[i][j].x);
+          acc[i][j].y = fma(a[i].y, b[j].x, acc[i][j].y);
         }
       }
     }
