@@ -208,6 +208,35 @@ def load_traffic():
     return None
 
 
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except Exception:
+        return 7700.0, "fallback: nominal B200 HBM3e bandwidth (MEASURED_PEAKS.json absent)"
+
+
+def secondary_rooflines(dev, sch, n, d, kernels):
+    """SURVEY §8(d) per-kernel rooflines of the other kernels of the step
+    (algorithmic bytes ÷ measured kernel time ÷ HBM peak)."""
+    peak, src = hbm_peak()
+    L = sch.L
+    words = dev.download(sch.masks).view(np.uint64) & np.uint64((1 << L) - 1)
+    bins = int(np.unpackbits(words.view(np.uint8)).sum())  # sum_l |I_l|
+    sum_m = int(sch.total_size)
+    out = {}
+    for name, nbytes, extra in (
+            ("bluestein_fft", 32 * sum_m, {"nominal_gflop": 5e-9 * sum(m * np.log2(m) for m in sch.primes[:L])}),
+            ("alias", 2 * 4 * d * n, {}),
+            ("gather", 4 * d * n + 16 * bins + 17 * n, {"alias_free_bins": bins})):
+        ms = kernels[name]
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = dict(bound="hbm", algorithmic_bytes=nbytes, ms=ms, achieved=gbs, peak=peak, unit="GB/s",
+                         frac=gbs / peak, **extra)
+    out["peak_source"] = src
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -296,6 +325,7 @@ def run_ours(args):
     flops = 8.0 * s_terms * sch.total_size
     achieved = flops / (kernels["sample_poly"] * 1e-3) / 1e12
     traffic = load_traffic()
+    others = secondary_rooflines(dev, sch, n, 10, kernels)
 
     # end to end through the public API with host buffers: the candidate rows
     # sit in pinned host memory (as a producer would leave them), results come
@@ -381,6 +411,7 @@ def run_ours(args):
                      "peak_source": "measured in this run: register-resident DFMA loop (sfft_fp64_peak)",
                      "algorithmic": f"8 flop x {s_terms} terms x {sch.total_size} nodes per launch",
                      "traffic": (traffic or {}).get("sample_poly_dram_bytes")},
+        "kernel_rooflines": others,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": "paper_1711_05152_b200.api.reconstruct_step (numpy in/out)"},
