@@ -119,7 +119,23 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   }
   __syncthreads();
   block_fft<LOG1, INV>(s, ftab + g.off_p1);
-  if (!INV) {
+  if (!INV && C <= FFT_T) {
+    // this thread's elements share the column n2 and step k1 by FFT_T / C:
+    // twiddles e^{-2 pi i n2 k1 / P} by a short recurrence from two table
+    // lookups (the per-element two-level lookups were the LSU's largest
+    // global-load consumer)
+    const int c = threadIdx.x % C;
+    const int64_t n2 = c0 + c;
+    double2 w = twP(g, ftab, n2 * (int64_t)(threadIdx.x / C));
+    const double2 step = twP(g, ftab, n2 * (int64_t)(FFT_T / C));
+#pragma unroll
+    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+      const int k1 = f / C;
+      const double2 v = cmul(s[c * rstride + fpad(k1)], w);
+      ub[(int64_t)k1 * P2 + n2] = v;
+      w = cmul(w, step);
+    }
+  } else if (!INV) {
 #pragma unroll
     for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
       const int c = f % C, k1 = f / C;
@@ -129,12 +145,23 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
       ub[(int64_t)k1 * P2 + n2] = v;
     }
   } else {
+    // post-chirp: all chirp loads first, then multiply + store (one exposed
+    // latency instead of one per group of four)
     const double2* ch = chirp + ut.off[lat];
+    constexpr int Q = FFT_E / FFT_T;
+    double2 cv[Q];
 #pragma unroll
-    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    for (int q = 0; q < Q; ++q) {
+      const int f = threadIdx.x + q * FFT_T;
+      const int64_t n = (int64_t)(f / C) * P2 + c0 + f % C;
+      cv[q] = n < m ? __ldg(&ch[n]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int f = threadIdx.x + q * FFT_T;
       const int c = f % C, n1 = f / C;
       const int64_t n = (int64_t)n1 * P2 + c0 + c;
-      if (n < m) ub[n] = cmul(s[c * rstride + fpad(n1)], __ldg(&ch[n]));
+      if (n < m) ub[n] = cmul(s[c * rstride + fpad(n1)], cv[q]);
     }
   }
 }
@@ -158,18 +185,27 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   const int g0 = blockIdx.x * rows;
   const bool single = (P1 == 1);
 
+  // all loads first, then the shared-memory stores: keeps the 16 loads of a
+  // thread in flight together (interleaved, ptxas serialised them)
+  constexpr int Q = FFT_E / FFT_T;
+  double2 v[Q];
 #pragma unroll
-  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+  for (int q = 0; q < Q; ++q) {
+    const int f = threadIdx.x + q * FFT_T;
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
-    double2 v = make_double2(0.0, 0.0);
+    v[q] = make_double2(0.0, 0.0);
     if (grow < total_rows) {
       const int u = grow / P1, k1 = grow - u * P1;
       const int lat = ut.lat[u];
       if (!(MODE == 0 && single && i >= ut.m[lat]))
-        v = buf[(int64_t)u * ustride + (int64_t)k1 * P2 + i];
+        v[q] = __ldcs(&buf[(int64_t)u * ustride + (int64_t)k1 * P2 + i]);
     }
-    s[r * rstride + fpad(i)] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int f = threadIdx.x + q * FFT_T;
+    s[(f / P2) * rstride + fpad(f % P2)] = v[q];
   }
   __syncthreads();
   block_fft<LOG2, false>(s, ftab + g.off_p2);
@@ -187,21 +223,41 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     }
     return;
   }
-  // pointwise product with Bhat (same layout)
+  // pointwise product with Bhat (same layout); loads first (see above)
 #pragma unroll
-  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+  for (int q = 0; q < Q; ++q) {
+    const int f = threadIdx.x + q * FFT_T;
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
+    v[q] = make_double2(0.0, 0.0);
     if (grow < total_rows) {
       const int u = grow / P1, k1 = grow - u * P1;
-      const int lat = ut.lat[u];
-      const double2 b = __ldg(&bhat[(int64_t)lat * ustride + (int64_t)k1 * P2 + i]);
-      const int si = r * rstride + fpad(i);
-      s[si] = cmul(s[si], b);
+      v[q] = __ldg(&bhat[(int64_t)ut.lat[u] * ustride + (int64_t)k1 * P2 + i]);
     }
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int f = threadIdx.x + q * FFT_T;
+    const int si = (f / P2) * rstride + fpad(f % P2);
+    s[si] = cmul(s[si], v[q]);
   }
   __syncthreads();
   block_fft<LOG2, true>(s, ftab + g.off_p2);
+  if (rows == 1 && !single) {
+    // one row k1 per CTA: e^{+2 pi i i k1 / P} for i = tid + FFT_T q by a short
+    // recurrence from two table lookups (see the column pass)
+    if (g0 >= total_rows) return;
+    const int u = g0 / P1, k1 = g0 - u * P1;
+    double2* ub = buf + (int64_t)u * ustride + (int64_t)k1 * P2;
+    double2 w = twP(g, ftab, (int64_t)threadIdx.x * k1);
+    const double2 step = twP(g, ftab, (int64_t)FFT_T * k1);
+#pragma unroll
+    for (int i = threadIdx.x; i < P2; i += FFT_T) {
+      ub[i] = cmulc(s[fpad(i)], w);
+      w = cmul(w, step);
+    }
+    return;
+  }
 #pragma unroll
   for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
     const int r = f / P2, i = f % P2;
