@@ -201,3 +201,30 @@ extern "C" int mb_info(int id, int* w, int* ti, int* tj) {
   *w = tab[id][0]; *ti = tab[id][1]; *tj = tab[id][2];
   return 0;
 }
+
+// launch cost vs kernel-parameter size (host time per launch)
+template <int BYTES>
+struct Blob { char b[BYTES]; };
+template <int BYTES>
+__global__ void param_kernel(Blob<BYTES> p, int* out) {
+  if (threadIdx.x == 0 && p.b[BYTES - 1] == 123) out[0] = 1;
+}
+#include <chrono>
+extern "C" double mb_launch_us(int bytes, int reps, void* st) {
+  int* out = nullptr;
+  cudaMalloc(&out, 64);
+  auto run = [&](auto blob) {
+    auto t0 = std::chrono::high_resolution_clock::now();
+    for (int i = 0; i < reps; ++i) param_kernel<<<1, 32, 0, (cudaStream_t)st>>>(blob, out);
+    auto t1 = std::chrono::high_resolution_clock::now();
+    cudaStreamSynchronize((cudaStream_t)st);
+    return std::chrono::duration<double, std::micro>(t1 - t0).count() / reps;
+  };
+  double r = -1;
+  if (bytes == 256) { Blob<256> b{}; run(b); r = run(b); }
+  if (bytes == 4096) { Blob<4096> b{}; run(b); r = run(b); }
+  if (bytes == 16384) { Blob<16384> b{}; run(b); r = run(b); }
+  if (bytes == 30000) { Blob<30000> b{}; run(b); r = run(b); }
+  cudaFree(out);
+  return r;
+}

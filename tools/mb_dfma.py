@@ -46,3 +46,8 @@ for id_ in range(20):
     flops = sms * 32 * w.value * chunks * 16 * ti.value * tj.value * 8.0
     print(f"id {id_:2d} W={w.value:2d} tile {ti.value}x{tj.value} {'smem' if id_ % 2 == 0 or id_ >= 18 else 'reg '} "
           f"order{[0, 0, 1, 1, 2, 2, 0, 0, 1, 1, 0, 0, 0, 0, 3, 3, 3, 3, 4, 1][id_]}: {flops / ms / 1e9:7.2f} TFLOP/s")
+
+lib.mb_launch_us.restype = ctypes.c_double
+for nb in (256, 4096, 16384, 30000):
+    us = lib.mb_launch_us(nb, 2000, ctypes.c_void_p(st.cuda_stream))
+    print(f"launch with {nb:6d} B of kernel parameters: {us:6.2f} us host time per launch")

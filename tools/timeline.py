@@ -52,6 +52,36 @@ for _ in range(5):
     step()
 dev.sync()
 Device.call, Device.download_small = call, dls
+
+import paper_1711_05152_b200.mr1l as _m  # noqa: E402
+import paper_1711_05152_b200._native as _n  # noqa: E402
+
+
+def _wrap(mod, name):
+    fn = getattr(mod, name)
+
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        out = fn(*a, **k)
+        rec.append((f"[host] {name}", t0, time.perf_counter(), None))
+        return out
+    setattr(mod, name, w)
+
+
+for mod, name in ((_m, "lattice_tables"), (_m, "_sample_units"), (_m, "candidate_primes"), (_n, "query"),
+                  (_m, "_attempt_streams")):
+    _wrap(mod, name)
+_empty = Device.empty
+
+
+def empty(self, *a, **k):
+    t0 = time.perf_counter()
+    out = _empty(self, *a, **k)
+    rec.append(("[host] empty", t0, time.perf_counter(), None))
+    return out
+
+
+Device.empty = empty
 for it in range(3):
     rec.clear()
     dev.sync()
@@ -65,7 +95,10 @@ for it in range(3):
     dev.sync()
     print(f"--- step {it}: device {e0.elapsed_time(e1):.3f} ms, host {1e3 * (h1 - h0):.3f} ms")
     prev_gpu = 0.0
-    for name, t0, t1, ev in rec:
+    for name, t0, t1, ev in sorted(rec, key=lambda x: x[1]):
+        if ev is None:
+            print(f"  {name:28s} host@{1e3 * (t0 - h0):7.3f} dur {1e3 * (t1 - t0):6.3f}")
+            continue
         g = e0.elapsed_time(ev)
         print(f"  {name:28s} host@{1e3 * (t0 - h0):7.3f} dur {1e3 * (t1 - t0):6.3f}  gpu@{g:7.3f} "
               f"(+{g - prev_gpu:6.3f})")
