@@ -252,7 +252,7 @@ def run_ours(args):
     from paper_1711_05152_b200 import _native, workloads
     from paper_1711_05152_b200.api import reconstruct_step
     from paper_1711_05152_b200.device import get_device
-    from paper_1711_05152_b200.mr1l import DeviceFreqs, StageTimer, build_scheme, run_step
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, StageTimer, build_scheme, prepare_step, run_step
 
     dev = get_device(local if world > 1 else None)
     wl = workloads.config1(seed=rank, n=args.n)
@@ -260,20 +260,30 @@ def run_ours(args):
     cand = DeviceFreqs.from_host(dev, wl.cand)
     flush = dev.empty((64 * 1024 * 1024,), torch.float32)  # 256 MB > 126 MB L2
 
-    def step(timer=None):
+    def step(timer=None, prev=None):
+        """One config-1 step.  Its cap check is deferred (run_step(defer_cap=True))
+        and completed by the NEXT step right after that step's work is enqueued
+        (``prev.finalize()``: by then the counts have long arrived), so the host
+        prepares step k+1 while step k still runs, as a stream of independent
+        steps would."""
+        prepare = lambda ms, z: prepare_step(dev, wl.oracle, cand, 1, ms, z)  # noqa: E731
         if timer is None:
             sch = build_scheme(dev, cand, wl.b, np.random.SeedSequence(wl.lattice_seed), box_extent=64,
-                                   lazy_streams=True)
+                               lazy_streams=True, prepare=prepare)
         else:
             with timer.span("alias"):
                 sch = build_scheme(dev, cand, wl.b, np.random.SeedSequence(wl.lattice_seed), box_extent=64,
-                                   lazy_streams=True)
-        res = run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, n, timer=timer)
+                                   lazy_streams=True, prepare=prepare)
+        res = run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, n, timer=timer, defer_cap=True,
+                       prep=sch.prep)
+        if prev is not None:
+            prev.finalize()
         return sch, res
 
     peak = measure_fp64_peak(dev, P)
     for _ in range(args.warmup):
         sch, res = step()
+        res.finalize()
     dev.sync()
     # correctness guard on the measured configuration
     coef = dev.download(res.coef[0])
@@ -305,9 +315,11 @@ def run_ours(args):
         t_a = torch.cuda.Event(enable_timing=True)
         t_b = torch.cuda.Event(enable_timing=True)
         t_a.record(dev.stream)
+        res = None
         for _ in range(args.steps):
             flush.zero_()
-            sch, res = step()
+            sch, res = step(prev=res)
+        res.finalize()
         t_b.record(dev.stream)
         dev.sync()
     launches = _native.query("sfft_launch_count") - launches0
@@ -326,6 +338,7 @@ def run_ours(args):
     for _ in range(3):
         flush.zero_()
         sch, res = step(timer)
+        res.finalize()
     dev.sync()
     stages = {k: float(np.mean(v)) for k, v in timer.totals_ms().items()}
     s_terms = wl.oracle.s

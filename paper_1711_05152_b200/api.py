@@ -166,7 +166,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     -> oracle(lattice nodes) -> invert_multiple -> _select of the reference
     (construct.py:185-206, detect.py:290-299, transform.py:99-127,
     detect.py:197-212) as one device pipeline."""
-    from .mr1l import run_step
+    from .mr1l import prepare_step, run_step
     dev = device or get_device()
     torch = dev.torch
     if isinstance(candidates, torch.Tensor):
@@ -187,8 +187,11 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
-    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh)
-    res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap))
+    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
+                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z))
+    res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
+                   defer_cap=True, prep=sch.prep)
+    res.finalize()  # cap applied (if binding) before the results are read
     coef, keep, words = dev.download_many(res.coef[0], res.keep[0], sch.masks)
     d2h = coef.nbytes + keep.nbytes + words.nbytes
     # the pinned staging buffers are reused by the next call: own the results

@@ -116,6 +116,31 @@ class Device:
         self.stream.synchronize()
         return buf.numpy().view(np.dtype(str(t.dtype).replace("torch.", ""))).reshape(t.shape).copy()
 
+    def download_async(self, t, ring: int = 8):
+        """Start a copy of a small device tensor into one of `ring` reusable
+        pinned slots (round robin) and return a callable that waits for it and
+        returns the host array.  Lets a caller keep enqueuing work and read the
+        value later; the slot is reused `ring` calls later."""
+        torch = self.torch
+        nbytes = t.numel() * t.element_size()
+        self._ring_pos = (getattr(self, "_ring_pos", -1) + 1) % ring
+        key = ("ring", self._ring_pos, nbytes)
+        buf = self._pinned.get(key)
+        if buf is None:
+            buf = torch.empty((nbytes,), dtype=torch.uint8, pin_memory=True)
+            self._pinned[key] = buf
+        with torch.cuda.stream(self.stream):
+            buf.copy_(t.detach().reshape(-1).view(torch.uint8), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        dtype = np.dtype(str(t.dtype).replace("torch.", ""))
+        shape = tuple(t.shape)
+
+        def wait():
+            ev.synchronize()
+            return buf.numpy().view(dtype).reshape(shape).copy()
+        return wait
+
     def sync(self):
         self.stream.synchronize()
 

@@ -29,7 +29,7 @@ from .device import Device, dptr, hptr
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig, candidate_primes
 
-__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "run_step", "StepResult",
+__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "run_step", "prepare_step", "StepPrep", "StepResult",
            "OracleInterrupt", "OracleError", "evaluate_callback"]
 
 UMAX = 256      # (iteration, lattice) units per launch (plan.cuh SFFT_UMAX)
@@ -112,6 +112,7 @@ class DeviceScheme:
     masks: object               # torch int64 (n,) alias-free bit masks (bit l = lattice l)
     attempts: int
     uncovered: int
+    prep: object = None         # build_scheme(prepare=...) result
 
     @property
     def m_used(self) -> np.ndarray:
@@ -150,13 +151,15 @@ def _attempt_streams(seed_seq: np.random.SeedSequence, b: int, lazy: bool):
 
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
-                 ctx: str = "", lazy_streams: bool = False) -> DeviceScheme:
+                 ctx: str = "", lazy_streams: bool = False, prepare=None) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
     the reference's sequential draw, SURVEY §7 hard part 1) and evaluates the
     alias masks of all of them in one pass; the early-exit L is the largest
-    first-cover index over the candidates.
+    first-cover index over the candidates.  ``prepare(ms, z)``: called once the
+    first attempt's alias kernel is enqueued (host work that overlaps it); its
+    result is returned as ``DeviceScheme.prep``.
     """
     if b < 1:
         raise ValueError("retry cap b must be >= 1")
@@ -180,6 +183,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     z = None
     stats_h = None
     attempt = 0
+    prep = None
     for attempt, child in enumerate(_attempt_streams(seed_seq, b, lazy_streams), start=1):
         rng = np.random.default_rng(child)
         # one vectorised draw with per-row bounds == the reference's per-prime
@@ -188,10 +192,12 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         zh = np.ascontiguousarray(z.astype(np.int32))
         dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
+        if prepare is not None and attempt == 1:
+            prep = prepare(ms, zh)
         stats_h = dev.download_small(stats)
         if int(stats_h[1]) == 0:
-            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0)
-    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]))
+            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep)
+    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep)
 
 
 def scheme_to_host(dev: Device, cand_rows: np.ndarray, sch: DeviceScheme) -> MultipleRank1Lattice:
@@ -232,6 +238,17 @@ class LatticeTables:
     @property
     def P(self) -> int:
         return 1 << self.p
+
+    def prefix(self, L: int) -> "LatticeTables | None":
+        """Tables of the first L lattices (twiddles/chirps are concatenated in
+        lattice order, one Bhat row per lattice: a prefix is a view), or None
+        when the first L sizes need a smaller FFT than this set's."""
+        ms = self.ms[:L]
+        if fft_exponent(int(ms.max())) != self.p:
+            return None
+        tot = int(ms.sum())
+        zs = self.zs[:L] if self.zs is not None else None
+        return LatticeTables(ms, zs, self.p, self.tw[:tot], self.chirp[:tot], self.bhat[:L], self.ftab)
 
 
 class _TableCache:
@@ -302,9 +319,23 @@ def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str 
 class StepResult:
     keep: object              # torch uint8 (r, n)
     coef: object              # torch float64 (r, n, 2)
-    counts: np.ndarray        # survivors per iteration after threshold and cap
+    _counts: np.ndarray | None  # survivors per iteration after threshold and cap
     nodes: int                # oracle samples taken
     timings: dict = field(default_factory=dict)
+    _finish: object = None    # pending cap check (run_step(defer_cap=True))
+
+    def finalize(self) -> "StepResult":
+        """Apply the cap (detect.py:205-211) if it is still pending: waits for
+        this step's survivor counts and runs the exact cap selection on the
+        iterations that exceed it.  Must precede any use of keep / coef."""
+        if self._finish is not None:
+            fin, self._finish = self._finish, None
+            self._counts = fin()
+        return self
+
+    @property
+    def counts(self) -> np.ndarray:
+        return self.finalize()._counts
 
 
 def _unit_arg(units):
@@ -316,7 +347,7 @@ def _unit_arg(units):
 
 
 def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
-                  tails: list[np.ndarray], buf, step: int, it0: int, units=None):
+                  tails: list[np.ndarray], buf, step: int, it0: int, units=None, scratch=None):
     """Fill buffer slot j with the pre-chirped samples of unit units[j]
     (global id i * L + l within this chunk of iterations; all rb * L units in
     order when ``units`` is None).  Noise streams are consumed for every unit
@@ -340,11 +371,14 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
         if isinstance(base, SparsePolynomialOracle):
             hf, cf = base.device_terms(dev)
             s = base.s
-            cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
-            rres = dev.empty((L, max(s, 1)), torch.int32)
-            rj = dev.empty((L, max(s, 1)), torch.int32)
             need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
-            part = dev.empty((max(need, 1), 2), torch.float64)
+            if scratch is not None and scratch[3].shape[0] >= max(need, 1):
+                cprime, rres, rj, part = scratch
+            else:
+                cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
+                rres = dev.empty((L, max(s, 1)), torch.int32)
+                rj = dev.empty((L, max(s, 1)), torch.int32)
+                part = dev.empty((max(need, 1), 2), torch.float64)
             dev.call("sfft_sample_poly", dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
                      hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
                      dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0), up, nu,
@@ -461,31 +495,96 @@ class _NoTimer:
         return contextlib.nullcontext()
 
 
+@dataclass
+class StepPrep:
+    """Everything of a single-chunk step that does not depend on the
+    early-exit L, made while the alias kernel runs (``build_scheme(prepare=)``):
+    the per-size tables of all L_max primes (cached; the used lattices' are a
+    prefix), the output buffers, the transform buffer and the sampling scratch
+    sized for L_max lattices."""
+    tabs: LatticeTables
+    keep: object
+    coef: object
+    counts: object
+    buf: object
+    poly: tuple | None
+    r: int
+    n: int
+
+
+def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all) -> StepPrep | None:
+    """Host work of ``run_step`` that can overlap the alias kernel (single
+    chunk of iterations, r * L_max <= the unit capacity); None otherwise."""
+    torch = dev.torch
+    ms_all = np.ascontiguousarray(np.asarray(ms_all, dtype=np.int64))
+    L_max = len(ms_all)
+    if r * L_max > UMAX or r > RBMAX:
+        return None
+    tabs = lattice_tables(dev, ms_all, np.ascontiguousarray(np.asarray(zs_all).astype(np.int32)),
+                          ctx="lattice tables (prepared)")
+    n = cand.n
+    keep = dev.empty((r, n), torch.uint8)
+    coef = dev.empty((r, n, 2), torch.float64)
+    counts = dev.zeros((r,), torch.int32)
+    buf = dev.empty((r * L_max, tabs.P, 2), torch.float64)
+    poly = None
+    base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
+    if isinstance(base, SparsePolynomialOracle):
+        s = max(base.s, 1)
+        # sized for L_max lattices (the rare smaller-L plan that needs more
+        # partial-sum space allocates its own in _sample_units)
+        need = int(_native.query("sfft_sample_poly_scratch", hptr(ms_all), L_max, r, base.s, 0, 0))
+        poly = (dev.empty((r, s, 2), torch.float64), dev.empty((L_max, s), torch.int32),
+                dev.empty((L_max, s), torch.int32), dev.empty((max(need, 1), 2), torch.float64))
+    return StepPrep(tabs, keep, coef, counts, buf, poly, r, n)
+
+
 def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
              d: int, delta: float, cap: int, step: int = 0, tabs: LatticeTables | None = None,
-             timer: StageTimer | None = None) -> StepResult:
-    """Sample, transform and invert all r~ iterations of one step; threshold + cap."""
+             timer: StageTimer | None = None, defer_cap: bool = False,
+             prep: StepPrep | None = None) -> StepResult:
+    """Sample, transform and invert all r~ iterations of one step; threshold + cap.
+
+    ``defer_cap``: return as soon as the work is enqueued; the survivor counts
+    come back asynchronously and the cap is applied by ``StepResult.finalize()``
+    (or the first ``.counts`` access), so the host can prepare the next
+    independent step while this one runs.  ``prep``: buffers and tables made
+    by ``prepare_step`` while the alias kernel ran."""
     torch = dev.torch
     tm = timer or _NoTimer()
     n = cand.n
     t1 = cand.ncomp
     L = sch.L
+    r = len(tails)
+    if prep is not None and (prep.r != r or prep.n != n or len(prep.tabs.ms) < L):
+        prep = None
+    if tabs is None and prep is not None:
+        tabs = prep.tabs.prefix(L)
+        if tabs is None:
+            prep = None
+        else:
+            tabs.zs = sch.z_used  # the accepted attempt's vectors
     if tabs is None:
         with tm.span("tables"):
             tabs = lattice_tables(dev, sch.m_used, sch.z_used, ctx=f"lattice tables, step {step}")
     P = tabs.P
-    r = len(tails)
-    keep = dev.empty((r, n), torch.uint8)
-    coef = dev.empty((r, n, 2), torch.float64)
-    counts = dev.zeros((r,), torch.int32)
     rb_max = max(1, min(RBMAX, UMAX // L))
     rb_alloc = min(rb_max, r)
-    buf = dev.empty((rb_alloc * L, P, 2), torch.float64)
+    if prep is not None:
+        keep, coef, counts, scratch = prep.keep, prep.coef, prep.counts, prep.poly
+        buf = prep.buf[: rb_alloc * L]
+    else:
+        keep = dev.empty((r, n), torch.uint8)
+        coef = dev.empty((r, n, 2), torch.float64)
+        counts = dev.zeros((r,), torch.int32)
+        buf = dev.empty((rb_alloc * L, P, 2), torch.float64)
+        scratch = None
     nodes = 0
     for i0 in range(0, r, rb_max):
         rb = min(rb_max, r - i0)
         with tm.span("sample"):
-            nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0)
+            nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0,
+                                   scratch=scratch)
         with tm.span("fft"):
             dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
                      dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")
@@ -493,16 +592,22 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
             dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
                      dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
                      dptr(counts), ctx=f"gather/select, step {step}")
-    counts_h = dev.download_small(counts).astype(np.int64)
-    over = [i for i in range(r) if counts_h[i] > cap]
-    if over:
-        sbytes = int(_native.query("sfft_select_scratch_bytes", n))
-        scratch = dev.empty((sbytes,), torch.uint8)
-        for i in over:
-            dev.call("sfft_select_cap", dptr(coef[i]), dptr(keep[i]), n, int(cap), dptr(scratch),
-                     ctx=f"cap selection, step {step}")
-            counts_h[i] = cap
-    return StepResult(keep, coef, counts_h, nodes)
+    def apply_cap(counts_h):
+        counts_h = counts_h.astype(np.int64)
+        over = [i for i in range(r) if counts_h[i] > cap]
+        if over:
+            sbytes = int(_native.query("sfft_select_scratch_bytes", n))
+            scratch = dev.empty((sbytes,), torch.uint8)
+            for i in over:
+                dev.call("sfft_select_cap", dptr(coef[i]), dptr(keep[i]), n, int(cap), dptr(scratch),
+                         ctx=f"cap selection, step {step}")
+                counts_h[i] = cap
+        return counts_h
+
+    if defer_cap:
+        wait = dev.download_async(counts)
+        return StepResult(keep, coef, None, nodes, _finish=lambda: apply_cap(wait()))
+    return StepResult(keep, coef, apply_cap(dev.download_small(counts)), nodes)
 
 
 def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):

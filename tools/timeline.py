@@ -14,7 +14,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_1711_05152_b200 import workloads  # noqa: E402
 from paper_1711_05152_b200.device import Device, get_device  # noqa: E402
-from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, run_step  # noqa: E402
+from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, prepare_step, run_step  # noqa: E402
 
 dev = get_device()
 torch = dev.torch
@@ -42,10 +42,14 @@ def dls(self, t):
     return out
 
 
+PREP = "--prep" in sys.argv
+
+
 def step():
+    prepare = (lambda ms, z: prepare_step(dev, wl.oracle, cand, 1, ms, z)) if PREP else None
     sch = build_scheme(dev, cand, wl.b, np.random.SeedSequence(wl.lattice_seed), box_extent=64,
-                       lazy_streams=True)
-    run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, len(wl.cand))
+                       lazy_streams=True, prepare=prepare)
+    run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, len(wl.cand), prep=sch.prep)
 
 
 for _ in range(5):
@@ -69,7 +73,7 @@ def _wrap(mod, name):
 
 
 for mod, name in ((_m, "lattice_tables"), (_m, "_sample_units"), (_m, "candidate_primes"), (_n, "query"),
-                  (_m, "_attempt_streams")):
+                  (_m, "_attempt_streams"), (_m, "prepare_step")):
     _wrap(mod, name)
 _empty = Device.empty
 
