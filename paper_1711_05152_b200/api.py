@@ -166,7 +166,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     -> oracle(lattice nodes) -> invert_multiple -> _select of the reference
     (construct.py:185-206, detect.py:290-299, transform.py:99-127,
     detect.py:197-212) as one device pipeline."""
-    from .mr1l import prepare_step, run_step
+    from .mr1l import prepare_step, run_step, speculate_scheme
     dev = device or get_device()
     torch = dev.torch
     if isinstance(candidates, torch.Tensor):
@@ -181,22 +181,28 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     fresh = not isinstance(seed_seq, np.random.SeedSequence)
     if fresh:
         seed_seq = np.random.SeedSequence(0 if seed_seq is None else seed_seq)
-    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows)
     h2d = n * t1 * 8
     if hasattr(oracle, "device_terms"):
+        # the oracle's terms are inputs of the call too: copied every call
+        # (asynchronously, ahead of the candidate rows)
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
+    spec = []
+    # the first attempt's primes and draw while the rows are in flight (valid
+    # unless the set's spread exceeds lambda; lazy streams only)
+    guess_fn = (lambda: spec.append(speculate_scheme(n, t1, seed_seq, b))) if fresh else None
+    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=guess_fn)
     sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z))
+                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z),
+                       guess=spec[0] if spec else None)
     res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
                    defer_cap=True, prep=sch.prep)
     res.finalize()  # cap applied (if binding) before the results are read
     coef, keep, words = dev.download_many(res.coef[0], res.keep[0], sch.masks)
     d2h = coef.nbytes + keep.nbytes + words.nbytes
-    # the pinned staging buffers are reused by the next call: own the results
-    coef = coef.view(np.complex128).reshape(n).copy()
-    return StepReport(coef, words.view(np.uint64) != 0, keep.view(bool).copy(),
+    coef = coef.view(np.complex128).reshape(n)  # views of fresh pinned buffers: no host copy
+    return StepReport(coef, words.view(np.uint64) != 0, keep.view(bool),
                       sch.primes[: sch.L], sch.z[: sch.L], sch.attempts, res.nodes, h2d, d2h)
 
 

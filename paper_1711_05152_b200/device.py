@@ -72,32 +72,33 @@ class Device:
     def zeros(self, shape, dtype):
         return self.torch.zeros(shape, dtype=dtype, device=self.device)
 
-    def upload(self, a: np.ndarray, dtype=None):
-        """Host numpy -> device tensor (ordered on the engine stream)."""
+    def upload(self, a: np.ndarray, dtype=None, asynchronous: bool = False):
+        """Host numpy -> device tensor (ordered on the engine stream).
+        ``asynchronous``: stage through (cached) pinned memory and return
+        without waiting for the copy."""
         torch = self.torch
         t = torch.from_numpy(np.ascontiguousarray(a))
         if dtype is not None:
             t = t.to(dtype)
+        if asynchronous:
+            t = t.pin_memory()
         with torch.cuda.stream(self.stream):
-            return t.to(self.device, non_blocking=False)
+            return t.to(self.device, non_blocking=asynchronous)
 
     def download(self, t) -> np.ndarray:
         with self.torch.cuda.stream(self.stream):
             return t.detach().to("cpu").numpy()
 
     def download_many(self, *tensors) -> list[np.ndarray]:
-        """Copy several device tensors to host with asynchronous DMA into
-        pinned buffers (reused across calls, one per slot) and one stream
-        synchronisation; returns uint8 numpy views to reinterpret."""
+        """Copy several device tensors to host with asynchronous DMA into fresh
+        pinned buffers (torch's caching host allocator: no cudaHostAlloc after
+        warm-up) and one stream synchronisation; returns uint8 numpy views that
+        own their buffers (reinterpret with .view, no host copy needed)."""
         torch = self.torch
         outs = []
-        for k, t in enumerate(tensors):
+        for t in tensors:
             nbytes = t.numel() * t.element_size()
-            key = ("many", k)
-            buf = self._pinned.get(key)
-            if buf is None or buf.numel() < nbytes:
-                buf = torch.empty((max(nbytes, 1),), dtype=torch.uint8, pin_memory=True)
-                self._pinned[key] = buf
+            buf = torch.empty((max(nbytes, 1),), dtype=torch.uint8, pin_memory=True)
             with torch.cuda.stream(self.stream):
                 buf[:nbytes].copy_(t.detach().contiguous().reshape(-1).view(torch.uint8), non_blocking=True)
             outs.append(buf[:nbytes].numpy())

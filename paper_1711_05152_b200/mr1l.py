@@ -29,7 +29,8 @@ from .device import Device, dptr, hptr
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig, candidate_primes
 
-__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "run_step", "prepare_step", "StepPrep", "StepResult",
+__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "speculate_scheme", "SchemeGuess", "run_step",
+           "prepare_step", "StepPrep", "StepResult",
            "OracleInterrupt", "OracleError", "evaluate_callback"]
 
 UMAX = 256      # (iteration, lattice) units per launch (plan.cuh SFFT_UMAX)
@@ -82,10 +83,11 @@ class DeviceFreqs:
         return cls(t, rows.shape[0], kmax)
 
     @classmethod
-    def from_rows_tensor(cls, dev: Device, rows) -> tuple["DeviceFreqs", np.ndarray, np.ndarray]:
+    def from_rows_tensor(cls, dev: Device, rows, before_sync=None) -> tuple["DeviceFreqs", np.ndarray, np.ndarray]:
         """Upload (n, d) int64 rows (a CPU tensor; pinned memory makes the copy
         asynchronous DMA) and pack them on the device; also returns the
-        per-component minima and maxima."""
+        per-component minima and maxima.  ``before_sync()`` runs while the
+        copy is in flight."""
         torch = dev.torch
         n, d = (int(x) for x in rows.shape)
         with torch.cuda.stream(dev.stream):
@@ -93,6 +95,8 @@ class DeviceFreqs:
         out = dev.empty((d, n), torch.int32)
         mm = dev.empty((2 * d + 1,), torch.int32)
         dev.call("sfft_pack_rows", dptr(d_rows), n, d, dptr(out), dptr(mm), ctx="pack rows")
+        if before_sync is not None:
+            before_sync()
         mmh = dev.download_small(mm).astype(np.int64)
         if mmh[2 * d]:
             raise ValueError("frequency components must satisfy |k_t| <= 2147483647")
@@ -149,9 +153,34 @@ def _attempt_streams(seed_seq: np.random.SeedSequence, b: int, lazy: bool):
                                      pool_size=seed_seq.pool_size)
 
 
+@dataclass
+class SchemeGuess:
+    """The first attempt of ``build_scheme`` computed before the candidate
+    set's spread is known (``speculate_scheme``): valid whenever every
+    candidate prime exceeds the spread, i.e. the primes are simply the L_max
+    smallest primes above lambda (construct.py:85-102)."""
+    primes: list
+    z: np.ndarray
+
+
+def speculate_scheme(n: int, t1: int, seed_seq: np.random.SeedSequence, b: int,
+                     cfg: MLConfig | None = None) -> SchemeGuess:
+    """Primes and the first attempt's generating vectors for an n-row set,
+    drawn from the same (lazy) child stream build_scheme would use."""
+    from .primes import primes_above
+    cfg = cfg or MLConfig(c=2.0, gamma=0.5)
+    l_max = cfg.max_lattices(n)
+    primes = primes_above(cfg.size_lower_bound(n), l_max)
+    ms = np.asarray(primes, dtype=np.int64)
+    child = next(_attempt_streams(seed_seq, b, True))
+    z = np.random.default_rng(child).integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
+    return SchemeGuess(primes, z)
+
+
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
-                 ctx: str = "", lazy_streams: bool = False, prepare=None) -> DeviceScheme:
+                 ctx: str = "", lazy_streams: bool = False, prepare=None,
+                 guess: SchemeGuess | None = None) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -159,7 +188,9 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     alias masks of all of them in one pass; the early-exit L is the largest
     first-cover index over the candidates.  ``prepare(ms, z)``: called once the
     first attempt's alias kernel is enqueued (host work that overlaps it); its
-    result is returned as ``DeviceScheme.prep``.
+    result is returned as ``DeviceScheme.prep``.  ``guess``: the first attempt
+    precomputed by ``speculate_scheme`` (used when its primes all exceed the
+    spread; requires ``lazy_streams``).
     """
     if b < 1:
         raise ValueError("retry cap b must be >= 1")
@@ -172,8 +203,13 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         raise ValueError(f"L_max = {l_max} lattices exceeds the 64-bit mask width")
     t1 = cand.ncomp
     spread = _spread_bound(cand, box_extent)
-    primes = candidate_primes(None, cfg.size_lower_bound(n), l_max, spread=spread,
-                              rows=lambda: cand.to_host(dev))
+    if guess is not None and (not lazy_streams or len(guess.primes) != l_max or guess.primes[0] <= spread):
+        guess = None
+    if guess is not None:
+        primes = list(guess.primes)
+    else:
+        primes = candidate_primes(None, cfg.size_lower_bound(n), l_max, spread=spread,
+                                  rows=lambda: cand.to_host(dev))
     ms = np.asarray(primes, dtype=np.int64)
     torch = dev.torch
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
@@ -185,10 +221,13 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     attempt = 0
     prep = None
     for attempt, child in enumerate(_attempt_streams(seed_seq, b, lazy_streams), start=1):
-        rng = np.random.default_rng(child)
-        # one vectorised draw with per-row bounds == the reference's per-prime
-        # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
-        z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
+        if attempt == 1 and guess is not None:
+            z = guess.z
+        else:
+            rng = np.random.default_rng(child)
+            # one vectorised draw with per-row bounds == the reference's per-prime
+            # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
+            z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
         zh = np.ascontiguousarray(z.astype(np.int32))
         dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")

@@ -162,9 +162,16 @@ class SparsePolynomialOracle(_DeviceOracle):
         got = self._dev_cache.get(dev.index)
         if got is None:
             torch = dev.torch
-            hf = np.ascontiguousarray(self.freqs.T.astype(np.int32))
-            cf = np.ascontiguousarray(np.stack([self.coeffs.real, self.coeffs.imag], axis=1))
-            got = (dev.upload(hf), dev.upload(cf))
+            host = getattr(self, "_pinned_terms", None)
+            if host is None:
+                # packed once into pinned host memory: every (re-)upload is an
+                # asynchronous DMA on the engine stream
+                hf = np.ascontiguousarray(self.freqs.T.astype(np.int32))
+                cf = np.ascontiguousarray(np.stack([self.coeffs.real, self.coeffs.imag], axis=1))
+                host = (torch.from_numpy(hf).pin_memory(), torch.from_numpy(cf).pin_memory())
+                self._pinned_terms = host
+            with torch.cuda.stream(dev.stream):
+                got = tuple(h.to(dev.device, non_blocking=True) for h in host)
             self._dev_cache[dev.index] = got
         return got
 

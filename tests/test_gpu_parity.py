@@ -145,6 +145,38 @@ def test_mr1l_step_device_path(P, golden):
     assert np.array_equal(rows.to_host(dev), golden["step_sel"].astype(np.int64))
 
 
+def test_mr1l_step_prepared_and_deferred_cap(P, golden):
+    """run_step(prep=prepare_step(...), defer_cap=True) is bit-identical to the
+    default path, including a binding cap (exact radix select, detect.py:205-211)
+    whose survivors match the oracle's _select."""
+    from oracle import sfft_oracle as O
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, compact, prepare_step, run_step
+    dev = get_device()
+    cand = golden["step_cand"].astype(np.int64)
+    oracle = P.SparsePolynomialOracle(golden["step_hf"], golden["step_hc"])
+    dc = DeviceFreqs.from_host(dev, cand)
+    seed = int(golden["step_seed"][0])
+    b = int(golden["step_b"][0])
+    for cap in (len(cand), 37):
+        sch = build_scheme(dev, dc, b, np.random.SeedSequence(seed))
+        ref = run_step(dev, oracle, dc, sch, [np.zeros(0)], 10, 1e-12, cap)
+        sch2 = build_scheme(dev, dc, b, np.random.SeedSequence(seed),
+                            prepare=lambda ms, z: prepare_step(dev, oracle, dc, 1, ms, z))
+        assert sch2.prep is not None and sch2.L == sch.L
+        got = run_step(dev, oracle, dc, sch2, [np.zeros(0)], 10, 1e-12, cap, defer_cap=True, prep=sch2.prep)
+        assert np.array_equal(got.counts, ref.counts)  # .counts finalizes (applies the cap)
+        assert np.array_equal(dev.download(got.coef[0]), dev.download(ref.coef[0]))
+        assert np.array_equal(dev.download(got.keep[0]), dev.download(ref.keep[0]))
+        rows, _ = compact(dev, dc, got.keep[0], 1)
+        coef = dev.download(ref.coef[0])
+        coef = coef[:, 0] + 1j * coef[:, 1]
+        cov = dev.download(sch.masks).view(np.uint64) != 0
+        want, _ = O.select(cand[cov], coef[cov], cap, 1e-12)  # magnitude order when the cap binds
+        want = want[np.lexsort(want.T[::-1])]                 # compaction keeps candidate (lex) order
+        assert len(want) == min(cap, len(want)) and np.array_equal(rows.to_host(dev), want)
+
+
 def _check_report(golden, key, rep, exact_coef=True):
     assert np.array_equal(rep.detected.freqs, golden[f"{key}_freqs"]), key
     ref = golden[f"{key}_coef"]

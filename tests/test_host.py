@@ -169,6 +169,21 @@ class TestWorkloadsAndRng:
             lazy = [np.random.default_rng(c).integers(0, 1 << 40, 5) for c in _attempt_streams(parent, 10, True)]
             assert all(np.array_equal(a, b) for a, b in zip(eager, lazy))
 
+    def test_speculated_first_attempt_equals_oracle_scheme(self):
+        # api.reconstruct_step draws attempt 1 while the rows are in flight
+        # (speculate_scheme); with every prime above the spread it must equal
+        # the oracle's Algorithm 1 primes and first generating vectors
+        from paper_1711_05152_b200.mr1l import speculate_scheme
+        rng = np.random.default_rng(11)
+        cand = O.unique_rows(rng.integers(-8, 9, size=(3000, 6)))
+        g = speculate_scheme(len(cand), 6, np.random.SeedSequence(21), 10)
+        assert g.primes == O.candidate_primes(cand, 2 * (len(cand) - 1), O.max_lattices(len(cand)))
+        assert g.primes[0] > 16
+        child = np.random.SeedSequence(21).spawn(10)[0]
+        r = np.random.default_rng(child)
+        want = np.stack([r.integers(0, m, size=6, dtype=np.int64) for m in g.primes])
+        assert np.array_equal(g.z, want)
+
     def test_spawn_is_stateful(self):
         ss = np.random.SeedSequence(1)
         a = ss.spawn(2)
