@@ -242,12 +242,14 @@ void choose_j1_search(int64_t m, int tw2, int& j1, int& nt1, int& nt2) {
   nt2 = (int)((J2 + tw2 - 1) / tw2);
 }
 
-// polynomial sampling kernel: SFFT_B200_SAMPLE_KERNEL=classic|ws (default ws)
+// polynomial sampling kernel: SFFT_B200_SAMPLE_KERNEL=classic|ws|tc
+// (default tc: warp-specialised, FP64 tensor-core contraction)
 int sample_kind() {
   static int kind = [] {
     const char* e = getenv("SFFT_B200_SAMPLE_KERNEL");
     if (e && strcmp(e, "classic") == 0) return 0;
-    return 1;
+    if (e && strcmp(e, "ws") == 0) return 1;
+    return 2;
   }();
   return kind;
 }
@@ -268,16 +270,16 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
   while (((int64_t)1 << (2 * bl)) < mmax) ++bl;
   pp->bl = bl;
   pp->kind = sample_kind();
-  if (pp->kind == 1 && sample_poly_ws_smem(bl, mmax) > 227 * 1024) pp->kind = 0;
-  const size_t smem = pp->kind == 1 ? sample_poly_ws_smem(bl, mmax) : sample_poly_smem(bl, mmax);
+  if (pp->kind >= 1 && sample_poly_ws_smem(bl, mmax) > 227 * 1024) pp->kind = 0;
+  const size_t smem = pp->kind >= 1 ? sample_poly_ws_smem(bl, mmax) : sample_poly_smem(bl, mmax);
   if (smem > 227 * 1024) return E_2BIG;
   // resident CTAs per SM: classic 2 by registers (256 threads x 128 regs),
   // warp-specialised 1 (384 threads x 168 regs); fewer if shared-memory-bound
-  const int reg_cap = pp->kind == 1 ? 1 : 2;
+  const int reg_cap = pp->kind >= 1 ? 1 : 2;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm > reg_cap) per_sm = reg_cap;
   if (per_sm < 1) per_sm = 1;
-  const int tw2 = pp->kind == 1 ? 128 : 64;
+  const int tw2 = pp->kind >= 1 ? 128 : 64;
   int64_t tiles_l[SFFT_LMAX];
   int64_t tiles_total = 0;
   for (int l = 0; l < L; ++l) {

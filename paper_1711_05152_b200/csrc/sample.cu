@@ -474,7 +474,7 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
   int64_t mmax = 1;
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
   const size_t smem = sample_poly_smem(pp.bl, mmax);
-  if (pp.kind == 1) {
+  if (pp.kind >= 1) {
     int rc = launch_sample_poly_ws(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride, apply_chirp,
                                    part, pstride, st);
     if (rc) return rc;

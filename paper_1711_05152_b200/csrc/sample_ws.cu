@@ -6,6 +6,16 @@
 // stages (Barrett reduction, two-level twiddle tables, short recurrences)
 // into a 3-deep ring of shared-memory stages synchronised with named
 // barriers (full[s] / empty[s]), so generation overlaps the contraction.
+//
+// TC = true: the consumers contract on the FP64 tensor cores (DMMA,
+// mma.sync m8n8k4 f64: 256 FMAs per warp instruction, measured at 37.1
+// TFLOP/s from shared memory on B200 = the DFMA peak, tools/mb_dmma.cu,
+// where a DFMA outer product tops out at 84% of it, tools/mb_dfma.cu).  The
+// complex product is four real MMAs (Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br)
+// and the producers store the operands as split real / imaginary planes in
+// MMA fragment order, so every consumer operand load is one conflict-free
+// 256 B LDS.64 per warp.  (tcgen05 has no FP64 kind: mma.sync is the FP64
+// tensor path on sm_100a.)
 #include "common.cuh"
 #include "plan.cuh"
 #include "sample.cuh"
@@ -44,7 +54,14 @@ __device__ __forceinline__ double2 ws_tw(const double2* __restrict__ tlo, const 
   return cmul(thi[n >> bl], tlo[n & ((1u << bl) - 1u)]);
 }
 
-template <bool SPLIT>
+// D += A B for one 8x8x4 FP64 tile; A (8x4 row) / B (4x8 col) one element per
+// lane, D two elements per lane (PTX mma.m8n8k4 fragment layout)
+__device__ __forceinline__ void dmma_acc(double2& d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d.x), "+d"(d.y) : "d"(a), "d"(b));
+}
+
+template <bool SPLIT, bool TC>
 __global__ void __launch_bounds__(ws::NT, 1)
 sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
                       const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
@@ -131,17 +148,43 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
         v[1] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (j2_0 + gt), M32, mu), bl);
         v[2] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (j2_0 + gt + 64u), M32, mu), bl);
       }
-      double2* ar = As + gh * TJ1 + gt;
-      double2* br = Bs + gh * TJ2 + gt;
+      if (!TC) {
+        double2* ar = As + gh * TJ1 + gt;
+        double2* br = Bs + gh * TJ2 + gt;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        ar[8 * i] = v[0];
-        br[8 * i] = v[1];
-        br[64 + 8 * i] = v[2];
-        if (i < 7) {
-          v[0] = cmul(v[0], ea);
-          v[1] = cmul(v[1], eb);
-          v[2] = cmul(v[2], eb);
+        for (int i = 0; i < 8; ++i) {
+          ar[8 * i] = v[0];
+          br[8 * i] = v[1];
+          br[64 + 8 * i] = v[2];
+          if (i < 7) {
+            v[0] = cmul(v[0], ea);
+            v[1] = cmul(v[1], eb);
+            v[2] = cmul(v[2], eb);
+          }
+        }
+      } else {
+        // fragment order: A(j1, h) -> plane[((h>>2) * 8 + (j1>>3)) * 32 + (j1&7) * 4 + (h&3)],
+        // B(h, j2) -> plane[((h>>2) * 16 + (j2>>3)) * 32 + (j2&7) * 4 + (h&3)]
+        double* a_re = (double*)As;
+        double* a_im = a_re + KC * TJ1;
+        double* b_re = a_im + KC * TJ1;
+        double* b_im = b_re + KC * TJ2;
+        const int la = gt * 4 + (gh & 3);
+        const int ka = (gh >> 2) * 8 * 32 + la;
+        const int kb = (gh >> 2) * 16 * 32 + la;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          a_re[ka + i * 32] = v[0].x;
+          a_im[ka + i * 32] = v[0].y;
+          b_re[kb + i * 32] = v[1].x;
+          b_im[kb + i * 32] = v[1].y;
+          b_re[kb + (i + 8) * 32] = v[2].x;
+          b_im[kb + (i + 8) * 32] = v[2].y;
+          if (i < 7) {
+            v[0] = cmul(v[0], ea);
+            v[1] = cmul(v[1], eb);
+            v[2] = cmul(v[2], eb);
+          }
         }
       }
       bar_arrive(1 + st, NT);  // stage full
@@ -151,6 +194,74 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
 
   // ---------------- consumers ----------------
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONS));
+  if (TC) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int bi0 = (w & 1) * 4;   // 4 row blocks (j1) of 8
+    const int bj0 = (w >> 1) * 4;  // 4 column blocks (j2) of 8
+    double2 cr[4][4], ci[4][4];    // (.x, .y) = the lane's two columns of the 8x8 block
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) cr[x][y] = ci[x][y] = make_double2(0.0, 0.0);
+    for (int c = 0; c < nchunk; ++c) {
+      const int st = c % NS;
+      bar_sync(1 + st, NT);  // stage full
+      const double* a_re = (const double*)(sm + st * STAGE);
+      const double* a_im = a_re + KC * TJ1;
+      const double* b_re = a_im + KC * TJ1;
+      const double* b_im = b_re + KC * TJ2;
+#pragma unroll
+      for (int kk = 0; kk < KC / 4; ++kk) {
+        double ar[4], ai[4], nai[4], br[4], bm[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          ar[x] = a_re[(kk * 8 + bi0 + x) * 32 + lane];
+          ai[x] = a_im[(kk * 8 + bi0 + x) * 32 + lane];
+          nai[x] = -ai[x];
+        }
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          br[y] = b_re[(kk * 16 + bj0 + y) * 32 + lane];
+          bm[y] = b_im[(kk * 16 + bj0 + y) * 32 + lane];
+        }
+        // four sweeps over the 16 blocks: dependent MMAs on one accumulator are 16 apart
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_acc(cr[x][y], ar[x], br[y]);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_acc(ci[x][y], ar[x], bm[y]);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_acc(cr[x][y], nai[x], bm[y]);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_acc(ci[x][y], ai[x], br[y]);
+      }
+      if (c + NS < nchunk) bar_arrive(1 + NS + st, NT);  // stage empty (only if it will be refilled)
+    }
+    const double2* ch = chirp + lt.off[l];
+    double2* ub = SPLIT ? part + ((int64_t)q * pp.nunits + u) * pstride : buf + (int64_t)u * ustride;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int64_t j1 = j1_0 + (bi0 + x) * 8 + (lane >> 2);
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int64_t j2 = j2_0 + (bj0 + y) * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t n = j1 + J1 * (j2 + e);
+          const double2 v = make_double2(e ? cr[x][y].y : cr[x][y].x, e ? ci[x][y].y : ci[x][y].x);
+          if (n < M) ub[n] = (!SPLIT && apply_chirp) ? cmul(v, __ldg(&ch[n])) : v;
+        }
+      }
+    }
+    return;
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tx = lane & 15;               // j1 = tx + 16 i, i < 4
   const int ty = (lane >> 4) + 2 * w;     // j2 = ty + 16 j, j < 8
@@ -219,16 +330,24 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
   int64_t mmax = 1;
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
   const size_t smem = sample_poly_ws_smem(pp.bl, mmax);
-  const void* fn = pp.ks > 1 ? (const void*)sample_poly_ws_kernel<true> : (const void*)sample_poly_ws_kernel<false>;
+  const bool tc = pp.kind == 2;
+  const void* fn = pp.ks > 1 ? (tc ? (const void*)sample_poly_ws_kernel<true, true>
+                                   : (const void*)sample_poly_ws_kernel<true, false>)
+                             : (tc ? (const void*)sample_poly_ws_kernel<false, true>
+                                   : (const void*)sample_poly_ws_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   prof_mark(PROF_SAMPLE, true, st);
-  if (pp.ks > 1)
-    sample_poly_ws_kernel<true><<<ctas, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
-                                                            ustride, apply_chirp ? 1 : 0, part, pstride);
-  else
-    sample_poly_ws_kernel<false><<<ctas, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
-                                                             ustride, apply_chirp ? 1 : 0, nullptr, 0);
+#define SFFT_WS_LAUNCH(SPLIT, TCV)                                                                      \
+  sample_poly_ws_kernel<SPLIT, TCV><<<ctas, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, \
+                                                                ustride, apply_chirp ? 1 : 0,            \
+                                                                SPLIT ? part : nullptr, SPLIT ? pstride : 0)
+  if (pp.ks > 1) {
+    if (tc) SFFT_WS_LAUNCH(true, true); else SFFT_WS_LAUNCH(true, false);
+  } else {
+    if (tc) SFFT_WS_LAUNCH(false, true); else SFFT_WS_LAUNCH(false, false);
+  }
+#undef SFFT_WS_LAUNCH
   prof_mark(PROF_SAMPLE, false, st);
   SFFT_CHECK_LAUNCH();
   return 0;
