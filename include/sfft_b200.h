@@ -219,6 +219,10 @@ int sfft_pack_rows(const int64_t* d_rows, int64_t n, int d, int32_t* d_out, int3
 int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream);
 /* FP64 roofline probe: blocks x 256 threads x iters x 16 DFMA */
 int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream);
+/* FP64 tensor-core (DMMA m8n8k4) peak loop: blocks x 256 threads, iters x 16
+ * MMAs per warp (512 flop each).  K1's roofline denominator is the larger of
+ * this and the DFMA loop above. */
+int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream);
 
 #ifdef __cplusplus
 }

@@ -63,6 +63,7 @@ _SIGS = {
     "sfft_pack_rows": (_int, [_vp, _i64, _int, _vp, _vp, _vp]),
     "sfft_cscale": (_int, [_vp, _i64, _dbl, _int, _vp]),
     "sfft_fp64_peak": (_int, [_vp, _int, _int, _vp]),
+    "sfft_fp64_mma_peak": (_int, [_vp, _int, _int, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

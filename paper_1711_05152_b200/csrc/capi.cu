@@ -21,6 +21,7 @@ int launch_prefix_flags(const int32_t* freqs, int64_t n, int t1, uint8_t* flags,
 int launch_scatter_residues(const int32_t* freqs, int64_t n, const LatTable& lt, const double2* coef,
                             double2* acc, int num_sms, cudaStream_t st);
 int launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t st);
+int launch_fp64_mma_peak(double* out, int iters, int blocks, cudaStream_t st);
 int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* hf,
                             const double2* coef, int s, double2* out, cudaStream_t st);
 int launch_eval_bspline_points(const double* pts, int64_t n, const BsplineSpec& bs, double2* out,
@@ -710,6 +711,10 @@ int sfft_cscale(double* d_x, int64_t n, double scale, int conj, void* stream) {
 
 int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream) {
   return launch_fp64_peak(d_out, iters, blocks, S(stream));
+}
+
+int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream) {
+  return launch_fp64_mma_peak(d_out, iters, blocks, S(stream));
 }
 
 }  // extern "C"
