@@ -85,9 +85,11 @@ def main():
             t_us = t * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ms": 1e3, "us": 1.0,
                         "ns": 1e-3}.get(tu, 1.0)
             fp64 = d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+            dmma = d.get("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active")
             dram = d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
             per.setdefault(name, []).append({"dram_bytes": rb + wb, "duration_us": t_us,
                                              "fp64_pipe_pct": float(fp64) if fp64 else None,
+                                             "dmma_pipe_pct": float(dmma) if dmma else None,
                                              "dram_pct": float(dram) if dram else None})
         summary["full_capture"] = per
         for name, lst in per.items():
