@@ -9,7 +9,7 @@
 // the phase is exact for every M < 2^31 (SURVEY §7 hard part 3).
 //
 // Layout of one transform buffer (P complex128): natural index n.  The FFT
-// of length P = P1 * P2 (P2 = 2^min(12,p)) runs as
+// of length P = P1 * P2 (P2 = 2^min(11,p), 4096 for p > 22) runs as
 //   column pass  : P2 columns of length P1 (stride P2) + twiddle e^{-2pi i n2 k1/P}
 //   row pass     : P1 rows of length P2, fused: forward FFT, * Bhat, inverse
 //                  FFT, * e^{+2pi i n2 k1 / P}
@@ -88,18 +88,18 @@ __global__ void bluestein_b_kernel(LatTable lt, const double2* __restrict__ chir
 }
 
 // ---------------------------------------------------------------------------
-// column pass (P1 = 2^LOG1 > 1, P2 = 4096).  CTA = C = 4096/P1 consecutive
+// column pass (P1 = 2^LOG1 > 1, P2 = TE).  CTA = C = TE/P1 consecutive
 // columns of one unit.  FWD: mask n >= M to zero if mask_input, forward FFT,
 // twiddle, store transposed.  INV: inverse FFT, post-chirp, store n < M.
-template <int LOG1, bool INV>
-__global__ void __launch_bounds__(FFT_T, 2)
+template <int LOG1, bool INV, int TE>
+__global__ void __launch_bounds__(FFT_T, TE == 2048 ? 4 : 2)
 fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int mask_input,
                const double2* __restrict__ ftab, const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
   constexpr int P1 = 1 << LOG1;
-  constexpr int P2 = FFT_E;
-  constexpr int C = FFT_E / P1;
-  constexpr int rstride = fft_rstride(P1);
+  constexpr int P2 = TE;  // the row length equals the tile size
+  constexpr int C = TE / P1;
+  constexpr int rstride = Tile<TE>::rstride(P1);
   const FftGeom g = fft_geom(p);
   const int u = blockIdx.y;
   const int c0 = blockIdx.x * C;
@@ -109,16 +109,16 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 
   // load (coalesced along columns), transpose into rows of length P1
 #pragma unroll
-  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+  for (int f = threadIdx.x; f < TE; f += FFT_T) {
     const int c = f % C, n1 = f / C;
     const int64_t n = (int64_t)n1 * P2 + c0 + c;
     double2 v;
     if (!INV && mask_input && n >= m) v = make_double2(0.0, 0.0);
     else v = ub[n];
-    s[c * rstride + fpad(n1)] = v;
+    s[c * rstride + Tile<TE>::pad(n1)] = v;
   }
   __syncthreads();
-  block_fft<LOG1, INV>(s, ftab + g.off_p1);
+  block_fft<LOG1, INV, TE>(s, ftab + g.off_p1);
   if (!INV && C <= FFT_T) {
     // this thread's elements share the column n2 and step k1 by FFT_T / C:
     // twiddles e^{-2 pi i n2 k1 / P} by a short recurrence from two table
@@ -129,18 +129,18 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     double2 w = twP(g, ftab, n2 * (int64_t)(threadIdx.x / C));
     const double2 step = twP(g, ftab, n2 * (int64_t)(FFT_T / C));
 #pragma unroll
-    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    for (int f = threadIdx.x; f < TE; f += FFT_T) {
       const int k1 = f / C;
-      const double2 v = cmul(s[c * rstride + fpad(k1)], w);
+      const double2 v = cmul(s[c * rstride + Tile<TE>::pad(k1)], w);
       ub[(int64_t)k1 * P2 + n2] = v;
       w = cmul(w, step);
     }
   } else if (!INV) {
 #pragma unroll
-    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    for (int f = threadIdx.x; f < TE; f += FFT_T) {
       const int c = f % C, k1 = f / C;
       const int64_t n2 = c0 + c;
-      double2 v = s[c * rstride + fpad(k1)];
+      double2 v = s[c * rstride + Tile<TE>::pad(k1)];
       v = cmul(v, twP(g, ftab, n2 * (int64_t)k1));
       ub[(int64_t)k1 * P2 + n2] = v;
     }
@@ -148,7 +148,7 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     // post-chirp: all chirp loads first, then multiply + store (one exposed
     // latency instead of one per group of four)
     const double2* ch = chirp + ut.off[lat];
-    constexpr int Q = FFT_E / FFT_T;
+    constexpr int Q = TE / FFT_T;
     double2 cv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -161,25 +161,25 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
       const int f = threadIdx.x + q * FFT_T;
       const int c = f % C, n1 = f / C;
       const int64_t n = (int64_t)n1 * P2 + c0 + c;
-      if (n < m) ub[n] = cmul(s[c * rstride + fpad(n1)], cv[q]);
+      if (n < m) ub[n] = cmul(s[c * rstride + Tile<TE>::pad(n1)], cv[q]);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// row pass (P2 = 2^LOG2).  CTA = 4096/P2 rows (rows index (unit, k1) flattened).
+// row pass (P2 = 2^LOG2).  CTA = TE/P2 rows (rows index (unit, k1) flattened).
 // MODE 0 (conv): forward FFT, * bhat, inverse FFT, then twiddle (P1 > 1) or
 //                post-chirp (P1 == 1, whole transform in one row).
 // MODE 1 (fwd only, builds bhat): forward FFT, scale by 1/P.
-template <int LOG2, int MODE>
-__global__ void __launch_bounds__(FFT_T, 2)
+template <int LOG2, int MODE, int TE>
+__global__ void __launch_bounds__(FFT_T, TE == 2048 ? 4 : 2)
 fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int total_rows,
                const double2* __restrict__ ftab, const double2* __restrict__ bhat,
                const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
   constexpr int P2 = 1 << LOG2;
-  constexpr int rows = FFT_E / P2;
-  constexpr int rstride = fft_rstride(P2);
+  constexpr int rows = TE / P2;
+  constexpr int rstride = Tile<TE>::rstride(P2);
   const FftGeom g = fft_geom(p);
   const int P1 = g.P1;
   const int g0 = blockIdx.x * rows;
@@ -187,7 +187,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 
   // all loads first, then the shared-memory stores: keeps the 16 loads of a
   // thread in flight together (interleaved, ptxas serialised them)
-  constexpr int Q = FFT_E / FFT_T;
+  constexpr int Q = TE / FFT_T;
   double2 v[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -205,19 +205,19 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int f = threadIdx.x + q * FFT_T;
-    s[(f / P2) * rstride + fpad(f % P2)] = v[q];
+    s[(f / P2) * rstride + Tile<TE>::pad(f % P2)] = v[q];
   }
   __syncthreads();
-  block_fft<LOG2, false>(s, ftab + g.off_p2);
+  block_fft<LOG2, false, TE>(s, ftab + g.off_p2);
   if (MODE == 1) {
     const double scale = 1.0 / (double)g.P;  // exact: P is a power of two
 #pragma unroll
-    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+    for (int f = threadIdx.x; f < TE; f += FFT_T) {
       const int r = f / P2, i = f % P2;
       const int grow = g0 + r;
       if (grow < total_rows) {
         const int u = grow / P1, k1 = grow - u * P1;
-        double2 v = s[r * rstride + fpad(i)];
+        double2 v = s[r * rstride + Tile<TE>::pad(i)];
         buf[(int64_t)u * ustride + (int64_t)k1 * P2 + i] = make_double2(v.x * scale, v.y * scale);
       }
     }
@@ -238,11 +238,11 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int f = threadIdx.x + q * FFT_T;
-    const int si = (f / P2) * rstride + fpad(f % P2);
+    const int si = (f / P2) * rstride + Tile<TE>::pad(f % P2);
     s[si] = cmul(s[si], v[q]);
   }
   __syncthreads();
-  block_fft<LOG2, true>(s, ftab + g.off_p2);
+  block_fft<LOG2, true, TE>(s, ftab + g.off_p2);
   if (rows == 1 && !single) {
     // one row k1 per CTA: e^{+2 pi i i k1 / P} for i = tid + FFT_T q by a short
     // recurrence from two table lookups (see the column pass)
@@ -253,19 +253,19 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
     const double2 step = twP(g, ftab, (int64_t)FFT_T * k1);
 #pragma unroll
     for (int i = threadIdx.x; i < P2; i += FFT_T) {
-      ub[i] = cmulc(s[fpad(i)], w);
+      ub[i] = cmulc(s[Tile<TE>::pad(i)], w);
       w = cmul(w, step);
     }
     return;
   }
 #pragma unroll
-  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) {
+  for (int f = threadIdx.x; f < TE; f += FFT_T) {
     const int r = f / P2, i = f % P2;
     const int grow = g0 + r;
     if (grow < total_rows) {
       const int u = grow / P1, k1 = grow - u * P1;
       const int lat = ut.lat[u];
-      double2 v = s[r * rstride + fpad(i)];
+      double2 v = s[r * rstride + Tile<TE>::pad(i)];
       double2* ub = buf + (int64_t)u * ustride;
       if (!single) {
         v = cmulc(v, twP(g, ftab, (int64_t)i * k1));  // e^{+2 pi i n2 k1 / P}
@@ -277,22 +277,31 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   }
 }
 
-// compile-time size dispatch
+// compile-time size dispatch: TE = 2048 for log sizes <= 11, 4096 for 12
+// (the column length P1 = 2^11..2^12 of p = 23, 24 also uses 4096 tiles)
 template <bool INV>
-static int launch_col(int lg, dim3 grid, size_t sm, cudaStream_t st, double2* buf, int64_t us,
+static int launch_col(int te, int lg, dim3 grid, size_t sm, cudaStream_t st, double2* buf, int64_t us,
                       const UnitTable& ut, int p, int mask, const double2* ftab, const double2* chirp) {
-#define SFFT_COL(L)                                                                            \
-  case L: {                                                                                    \
-    cudaError_t e = cudaFuncSetAttribute((const void*)fft_col_kernel<L, INV>,                  \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    if (e != cudaSuccess) return (int)e;                                                       \
-    fft_col_kernel<L, INV><<<grid, FFT_T, sm, st>>>(buf, us, ut, p, mask, ftab, chirp);        \
-    break;                                                                                     \
+#define SFFT_COL(TEV, L)                                                                         \
+  case L: {                                                                                      \
+    cudaError_t e = cudaFuncSetAttribute((const void*)fft_col_kernel<L, INV, TEV>,               \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+    if (e != cudaSuccess) return (int)e;                                                         \
+    fft_col_kernel<L, INV, TEV><<<grid, FFT_T, sm, st>>>(buf, us, ut, p, mask, ftab, chirp);     \
+    break;                                                                                       \
   }
-  switch (lg) {
-    SFFT_COL(1) SFFT_COL(2) SFFT_COL(3) SFFT_COL(4) SFFT_COL(5) SFFT_COL(6)
-    SFFT_COL(7) SFFT_COL(8) SFFT_COL(9) SFFT_COL(10) SFFT_COL(11) SFFT_COL(12)
-    default: return -22;
+  if (te == 2048) {
+    switch (lg) {
+      SFFT_COL(2048, 1) SFFT_COL(2048, 2) SFFT_COL(2048, 3) SFFT_COL(2048, 4) SFFT_COL(2048, 5)
+      SFFT_COL(2048, 6) SFFT_COL(2048, 7) SFFT_COL(2048, 8) SFFT_COL(2048, 9) SFFT_COL(2048, 10)
+      SFFT_COL(2048, 11)
+      default: return -22;
+    }
+  } else {
+    switch (lg) {
+      SFFT_COL(4096, 11) SFFT_COL(4096, 12)
+      default: return -22;
+    }
   }
 #undef SFFT_COL
   SFFT_CHECK_LAUNCH();
@@ -300,31 +309,39 @@ static int launch_col(int lg, dim3 grid, size_t sm, cudaStream_t st, double2* bu
 }
 
 template <int MODE>
-static int launch_row(int lg, unsigned blocks, size_t sm, cudaStream_t st, double2* buf, int64_t us,
+static int launch_row(int te, int lg, unsigned blocks, size_t sm, cudaStream_t st, double2* buf, int64_t us,
                       const UnitTable& ut, int p, int total_rows, const double2* ftab,
                       const double2* bhat, const double2* chirp) {
-#define SFFT_ROW(L)                                                                            \
-  case L: {                                                                                    \
-    cudaError_t e = cudaFuncSetAttribute((const void*)fft_row_kernel<L, MODE>,                 \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    if (e != cudaSuccess) return (int)e;                                                       \
-    fft_row_kernel<L, MODE><<<blocks, FFT_T, sm, st>>>(buf, us, ut, p, total_rows, ftab, bhat,  \
-                                                       chirp);                                 \
-    break;                                                                                     \
+#define SFFT_ROW(TEV, L)                                                                         \
+  case L: {                                                                                      \
+    cudaError_t e = cudaFuncSetAttribute((const void*)fft_row_kernel<L, MODE, TEV>,              \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+    if (e != cudaSuccess) return (int)e;                                                         \
+    fft_row_kernel<L, MODE, TEV><<<blocks, FFT_T, sm, st>>>(buf, us, ut, p, total_rows, ftab, bhat, \
+                                                            chirp);                              \
+    break;                                                                                       \
   }
-  switch (lg) {
-    SFFT_ROW(4) SFFT_ROW(5) SFFT_ROW(6) SFFT_ROW(7) SFFT_ROW(8)
-    SFFT_ROW(9) SFFT_ROW(10) SFFT_ROW(11) SFFT_ROW(12)
-    default: return -22;
+  if (te == 2048) {
+    switch (lg) {
+      SFFT_ROW(2048, 4) SFFT_ROW(2048, 5) SFFT_ROW(2048, 6) SFFT_ROW(2048, 7) SFFT_ROW(2048, 8)
+      SFFT_ROW(2048, 9) SFFT_ROW(2048, 10) SFFT_ROW(2048, 11)
+      default: return -22;
+    }
+  } else {
+    switch (lg) {
+      SFFT_ROW(4096, 12)
+      default: return -22;
+    }
   }
 #undef SFFT_ROW
   SFFT_CHECK_LAUNCH();
   return 0;
 }
 
-static size_t fft_smem_bytes(int rows_len) {
-  const int rows = FFT_E / rows_len;
-  return (size_t)rows * fft_rstride(rows_len) * sizeof(double2);
+static size_t fft_smem_bytes(int te, int rows_len) {
+  const int rows = te / rows_len;
+  const int rs = te == 2048 ? Tile<2048>::rstride(rows_len) : Tile<4096>::rstride(rows_len);
+  return (size_t)rows * rs * sizeof(double2);
 }
 
 int launch_fft_tables(int p, double2* out, cudaStream_t st) {
@@ -351,9 +368,9 @@ static int run_forward_cols(double2* buf, int64_t ustride, const UnitTable& ut, 
                             const double2* ftab, const double2* chirp, cudaStream_t st) {
   const FftGeom g = fft_geom(p);
   if (g.P1 == 1) return 0;
-  const size_t sm = fft_smem_bytes(g.P1);
-  dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
-  return launch_col<false>(g.p1, grid, sm, st, buf, ustride, ut, p, mask, ftab, chirp);
+  const size_t sm = fft_smem_bytes(g.te, g.P1);
+  dim3 grid(g.P2 / (g.te / g.P1), ut.nunits);
+  return launch_col<false>(g.te, g.p1, grid, sm, st, buf, ustride, ut, p, mask, ftab, chirp);
 }
 
 int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
@@ -370,10 +387,10 @@ int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
   for (int l = 0; l < lt.nlat; ++l) { ut.lat[l] = l; ut.m[l] = lt.m[l]; ut.off[l] = lt.off[l]; }
   int rc = run_forward_cols(bhat, P, ut, p, 0, ftab, chirp, st);
   if (rc) return rc;
-  const size_t sm = fft_smem_bytes(g.P2);
+  const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
-  const int rows = FFT_E / g.P2;
-  return launch_row<1>(g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, p, total_rows,
+  const int rows = g.te / g.P2;
+  return launch_row<1>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, p, total_rows,
                        ftab, nullptr, chirp);
 }
 
@@ -384,16 +401,16 @@ int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ft
   prof_mark(PROF_FFT, true, st);
   int rc = run_forward_cols(buf, P, ut, p, 1, ftab, chirp, st);
   if (rc) return rc;
-  const size_t sm = fft_smem_bytes(g.P2);
+  const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
-  const int rows = FFT_E / g.P2;
-  rc = launch_row<0>(g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, p, total_rows, ftab,
+  const int rows = g.te / g.P2;
+  rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, p, total_rows, ftab,
                      bhat, chirp);
   if (rc) return rc;
   if (g.P1 > 1) {
-    const size_t smc = fft_smem_bytes(g.P1);
-    dim3 grid(g.P2 / (FFT_E / g.P1), ut.nunits);
-    rc = launch_col<true>(g.p1, grid, smc, st, buf, P, ut, p, 0, ftab, chirp);
+    const size_t smc = fft_smem_bytes(g.te, g.P1);
+    dim3 grid(g.P2 / (g.te / g.P1), ut.nunits);
+    rc = launch_col<true>(g.te, g.p1, grid, smc, st, buf, P, ut, p, 0, ftab, chirp);
   }
   prof_mark(PROF_FFT, false, st);
   return rc;

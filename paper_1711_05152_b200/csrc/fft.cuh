@@ -1,21 +1,33 @@
 // In-shared-memory Stockham FFT building blocks shared by the Bluestein
 // passes (fft.cu) and the line-detection kernel.
 //
-// A CTA of FFT_T = 256 threads owns a tile of FFT_E = 4096 complex128
-// elements (64 KB + padding), organised as `rows` independent transforms of
-// length N = 4096 / rows.  Every radix pass keeps 16 values per thread in
-// registers (one radix-16 butterfly, or 16/R butterflies of radix R).
+// A CTA of FFT_T = 256 threads owns a tile of TE complex128 elements,
+// organised as `rows` independent transforms of length N = TE / rows.  Two
+// tile shapes (template parameter TE):
+//   TE = 2048: 8 values per thread, radix-8 passes, <= 64 registers, four
+//              CTAs (32 warps) per SM — the default (P = 2^p, p <= 22);
+//   TE = 4096: 16 values per thread, radix-16 passes, two CTAs per SM, for
+//              the largest transforms (p = 23, 24).
+// The passes are latency bound (shared-memory round trips, barriers): more
+// resident CTAs overlap one CTA's DRAM phases with another's FFT passes.
 #pragma once
 #include "common.cuh"
 
 namespace sfft {
 
 constexpr int FFT_T = 256;
-constexpr int FFT_E = 4096;
 
-// padded shared-memory index of element i inside a row (one gap per 16)
-__device__ __forceinline__ int fpad(int i) { return i + (i >> 4); }
-__host__ __device__ constexpr int fft_rstride(int n) { return n + (n >> 4) + 1; }
+template <int TE>
+struct Tile {
+  static constexpr int E = TE;
+  static constexpr int V = TE / FFT_T;           // values per thread and pass
+  static constexpr int LV = V == 16 ? 4 : 3;     // log2 of the largest radix
+  static constexpr int PADS = V == 16 ? 4 : 3;   // one padding slot per 2^PADS
+  // padded shared-memory index of element i inside a row: the radix-V scatter
+  // of the first pass (lane stride V) becomes bank-conflict free
+  __device__ static __forceinline__ int pad(int i) { return i + (i >> PADS); }
+  __host__ __device__ static constexpr int rstride(int n) { return n + (n >> PADS) + 1; }
+};
 
 // constant twiddles of the 16th roots of unity: e^{-2 pi i m / 16}, m < 8
 __device__ __forceinline__ double2 tw16(int m, bool inv) {
@@ -74,10 +86,10 @@ __device__ __forceinline__ void dft_reg(double2* v) {
 
 // One Stockham radix-R pass over `rows` rows of length N (all in smem).
 // twN[m] = e^{-2 pi i m / N}, m < N (global, read-only).
-template <int R, bool INV>
+template <int R, bool INV, int TE>
 __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride, int N, int Ns,
                                               const double2* __restrict__ twN) {
-  constexpr int BPT = 16 / R;
+  constexpr int BPT = Tile<TE>::V / R;
   const int per_row = N / R;
   const int nb = rows * per_row;
   const int tstep = N / (Ns * R);
@@ -93,7 +105,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride,
       const int k = j & (Ns - 1);
       const int base = row * rstride;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = s[base + fpad(j + r * per_row)];
+      for (int r = 0; r < R; ++r) v[q][r] = s[base + Tile<TE>::pad(j + r * per_row)];
       if (Ns > 1) {
         // w^r for r < R from two table entries (w^1, w^4): few live registers
         const double2 w1 = __ldg(&twN[k * tstep]);
@@ -124,28 +136,28 @@ __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride,
       const int idx0 = obase[q] - row * rstride;
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        s[row * rstride + fpad(idx0 + r * Ns)] = v[q][bitrev_small(r, Log2<R>::v)];
+        s[row * rstride + Tile<TE>::pad(idx0 + r * Ns)] = v[q][bitrev_small(r, Log2<R>::v)];
     }
   }
   __syncthreads();
 }
 
-// Full Stockham FFT of FFT_E >> LOGN rows of length 2^LOGN (natural order
-// in/out), fully unrolled at compile time: radix-16 passes first, one
+// Full Stockham FFT of TE >> LOGN rows of length 2^LOGN (natural order
+// in/out), fully unrolled at compile time: largest-radix passes first, one
 // smaller pass last.
-template <int LOGN, int DONE, bool INV>
+template <int LOGN, int DONE, bool INV, int TE>
 __device__ __forceinline__ void fft_passes(double2* s, const double2* __restrict__ twN) {
   if constexpr (DONE < LOGN) {
     constexpr int REM = LOGN - DONE;
-    constexpr int RB = REM >= 4 ? 4 : REM;
-    stockham_pass<(1 << RB), INV>(s, FFT_E >> LOGN, fft_rstride(1 << LOGN), 1 << LOGN, 1 << DONE, twN);
-    fft_passes<LOGN, DONE + RB, INV>(s, twN);
+    constexpr int RB = REM >= Tile<TE>::LV ? Tile<TE>::LV : REM;
+    stockham_pass<(1 << RB), INV, TE>(s, TE >> LOGN, Tile<TE>::rstride(1 << LOGN), 1 << LOGN, 1 << DONE, twN);
+    fft_passes<LOGN, DONE + RB, INV, TE>(s, twN);
   }
 }
 
-template <int LOGN, bool INV>
+template <int LOGN, bool INV, int TE>
 __device__ __forceinline__ void block_fft(double2* s, const double2* __restrict__ twN) {
-  fft_passes<LOGN, 0, INV>(s, twN);
+  fft_passes<LOGN, 0, INV, TE>(s, twN);
 }
 
 }  // namespace sfft

@@ -42,9 +42,11 @@ struct RowMap {
   int row[SFFT_UMAX];
 };
 
-// Power-of-two FFT geometry: P = P1 * P2, P2 = 2^min(12, p).
+// Power-of-two FFT geometry: P = P1 * P2, P2 = 2^min(11, p) (tiles of 2048)
+// for p <= 22, P2 = 4096 (tiles of 4096) for p = 23, 24.
 struct FftGeom {
   int p, p1, p2, P1, P2, qlo, nlo;
+  int te;  // shared-memory tile (elements): 2048 for p <= 22, 4096 above
   int64_t P;
   int64_t off_p1, off_p2, off_lo, off_hi, table_len;
 };
@@ -52,7 +54,9 @@ struct FftGeom {
 __host__ __device__ inline FftGeom fft_geom(int p) {
   FftGeom g;
   g.p = p;
-  g.p2 = p < 12 ? p : 12;
+  g.te = p <= 22 ? 2048 : 4096;
+  const int ptile = p <= 22 ? 11 : 12;
+  g.p2 = p < ptile ? p : ptile;
   g.p1 = p - g.p2;
   g.P1 = 1 << g.p1;
   g.P2 = 1 << g.p2;

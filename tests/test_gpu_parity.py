@@ -73,7 +73,9 @@ def test_dft_1d_known_answers(P, golden, K):
 
 def test_dft_large_primes_vs_numpy(P):
     rng = np.random.default_rng(1)
-    for K in (130003, 199999, 1300021):
+    # 1300021 -> P = 2^22 (largest 2048-point tiles); 2097169 and 4194319 ->
+    # P = 2^23, 2^24 (4096-point tiles)
+    for K in (130003, 199999, 1300021, 2097169, 4194319):
         v = rng.normal(size=K) + 1j * rng.normal(size=K)
         got = P.dft_1d(v)
         ref = np.fft.fft(v)

@@ -9,20 +9,20 @@ using namespace sfft;
 template <int MODE>
 __global__ void __launch_bounds__(FFT_T, 2) mb_row_kernel(const double2* __restrict__ tw, double2* out, int reps) {
   extern __shared__ double2 s[];
-  for (int f = threadIdx.x; f < FFT_E; f += FFT_T) s[fpad(f)] = make_double2(1e-3 * f, 1.0);
+  for (int f = threadIdx.x; f < 4096; f += FFT_T) s[Tile<4096>::pad(f)] = make_double2(1e-3 * f, 1.0);
   __syncthreads();
   // no loop (a loop makes ptxas keep every pass's addresses live and spill)
-  block_fft<12, false>(s, tw);
+  block_fft<12, false, 4096>(s, tw);
   if (MODE == 1) {
-    for (int f = threadIdx.x; f < FFT_E; f += FFT_T) s[fpad(f)] = cmul(s[fpad(f)], make_double2(0.5, 0.25));
+    for (int f = threadIdx.x; f < 4096; f += FFT_T) s[Tile<4096>::pad(f)] = cmul(s[Tile<4096>::pad(f)], make_double2(0.5, 0.25));
     __syncthreads();
   }
-  block_fft<12, true>(s, tw);
+  block_fft<12, true, 4096>(s, tw);
   if (threadIdx.x == 0 && s[0].x == 12345.0) out[blockIdx.x] = s[1];
 }
 
 extern "C" int mb_row(int mode, int blocks, const double* tw, double* out, int reps, void* st) {
-  const size_t sm = (size_t)fft_rstride(4096) * sizeof(double2);
+  const size_t sm = (size_t)Tile<4096>::rstride(4096) * sizeof(double2);
   if (mode == 0) {
     cudaFuncSetAttribute((const void*)mb_row_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     mb_row_kernel<0><<<blocks, FFT_T, sm, (cudaStream_t)st>>>((const double2*)tw, (double2*)out, reps);
