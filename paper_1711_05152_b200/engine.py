@@ -24,7 +24,7 @@ import numpy as np
 
 from .core import FrequencyIndexSet, SearchBox, SparseSpectrum
 from .device import Device, dptr, get_device, hptr
-from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact,
+from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact, prepare_step,
                    evaluate_callback, product, run_step)
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig
@@ -326,8 +326,14 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             from .single import single_scheme
             sch = single_scheme(dev, cand)  # CBC (reference detect.py:269-271), no RNG consumed
         else:
+            prepare = None
+            if not sharded:
+                # while the alias kernel runs: buffers (and the tables, when this
+                # step's sizes were seen before) for the run_step that follows
+                prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
+                                                     cached_tables_only=True)
             sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
-                               ctx=f"lattice search, step {t}", lazy_streams=True)
+                               ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare)
         rep.scheme_sizes[t] = sch.total_size
         rep.lattice_attempts[t] = sch.attempts
         rep.inversion_calls[t] = r_tilde * sch.total_size
@@ -342,7 +348,7 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
         if sharded:
             res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
         else:
-            res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t)
+            res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t, prep=sch.prep)
         if last:
             rows_d, coef_d = compact(dev, cand, res.keep[0], 1, res.coef[0])
             final_rows = rows_d.to_host(dev)

@@ -551,16 +551,24 @@ class StepPrep:
     n: int
 
 
-def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all) -> StepPrep | None:
+def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
+                 cached_tables_only: bool = False) -> StepPrep | None:
     """Host work of ``run_step`` that can overlap the alias kernel (single
-    chunk of iterations, r * L_max <= the unit capacity); None otherwise."""
+    chunk of iterations, r * L_max <= the unit capacity); None otherwise.
+    ``cached_tables_only``: do not build the per-size tables of all L_max
+    primes when they are not cached already (run_step then builds the L it
+    uses), so a step with new sizes does no extra table work."""
     torch = dev.torch
     ms_all = np.ascontiguousarray(np.asarray(ms_all, dtype=np.int64))
     L_max = len(ms_all)
     if r * L_max > UMAX or r > RBMAX:
         return None
-    tabs = lattice_tables(dev, ms_all, np.ascontiguousarray(np.asarray(zs_all).astype(np.int32)),
-                          ctx="lattice tables (prepared)")
+    zs32 = np.ascontiguousarray(np.asarray(zs_all).astype(np.int32))
+    if cached_tables_only:
+        key = (fft_exponent(int(ms_all.max())),) + tuple(int(m) for m in ms_all)
+        if _TABLES.setdefault(dev.index, _TableCache()).get(key) is None:
+            return None
+    tabs = lattice_tables(dev, ms_all, zs32, ctx="lattice tables (prepared)")
     n = cand.n
     keep = dev.empty((r, n), torch.uint8)
     coef = dev.empty((r, n, 2), torch.float64)

@@ -48,8 +48,10 @@ def test_size_queries_without_gpu(lib):
     assert _native.query("sfft_abi_version") == 1
     assert _native.query("sfft_fft_table_len", 3) == -1
     n18 = _native.query("sfft_fft_table_len", 18)
-    # [P1 | P2 | 2^9 | 2^9] with P = 2^18 = 2^6 * 2^12
-    assert n18 == 64 + 4096 + 512 + 512
+    # [P1 | P2 | 2^9 | 2^9] with P = 2^18 = 2^7 * 2^11 (2048-point tiles up to 2^22)
+    assert n18 == 128 + 2048 + 512 + 512
+    # P = 2^23 = 2^11 * 2^12 (4096-point tiles), two-level table 2^12 + 2^11
+    assert _native.query("sfft_fft_table_len", 23) == 2048 + 4096 + 4096 + 2048
     ms = np.array([7, 64, 65], dtype=np.int64)
     assert _native.query("sfft_alias_scratch_words", ms.ctypes.data, 3) == 2 * (1 + 2 + 3)
     assert _native.query("sfft_scan_scratch_len", 0) == 1

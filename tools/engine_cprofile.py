@@ -1,0 +1,23 @@
+"""cProfile one warm config-2 sparse_fft (host hotspots; run on a GPU box)."""
+import cProfile
+import pstats
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_1711_05152_b200 as P  # noqa: E402
+from paper_1711_05152_b200 import workloads  # noqa: E402
+from paper_1711_05152_b200.device import get_device  # noqa: E402
+
+dev = get_device()
+wl = workloads.config2()
+P.sparse_fft(wl.oracle, wl.cfg)
+dev.sync()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(3):
+    P.sparse_fft(wl.oracle, wl.cfg)
+dev.sync()
+pr.disable()
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(30)
