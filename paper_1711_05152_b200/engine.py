@@ -230,14 +230,36 @@ def projected_line_coefficients(oracle, t: int, box: SearchBox, anchor: np.ndarr
     return ks, c[:, 0] + 1j * c[:, 1]
 
 
-def _detect(dev: Device, oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator, step: int):
+def _detect_launch(dev: Device, oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator, step: int):
     box = cfg.box
     d = box.dim
     zero = cfg.mode == "deterministic_zero_anchor"
     anchors = np.stack([np.zeros(d) if zero else rng.random(d) for _ in range(cfg.r)])
     ks, _, keep = _lines(dev, oracle, t, box, anchors, cfg.local_sparsity, cfg.component_threshold, step)
+    return ks, keep
+
+
+def _detect(dev: Device, oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator, step: int):
+    ks, keep = _detect_launch(dev, oracle, t, cfg, rng, step)
     hit = dev.download(keep).astype(bool).any(axis=0)
     return ks[hit]
+
+
+def _detect_all(dev: Device, oracle, cfg: DetectionConfig, streams) -> list[np.ndarray]:
+    """Line detection of every component at once: each
+    component's lines use their own stream (detect_streams[t]) and do not
+    depend on the other steps, so for a noiseless device oracle all d
+    detections are launched back to back and read back with one
+    synchronisation.  (Noisy and host-callback oracles keep the reference's
+    per-step call order.)"""
+    launched = [_detect_launch(dev, oracle, t, cfg, np.random.default_rng(streams[t]), t)
+                for t in range(cfg.box.dim)]
+    outs = dev.download_many(*[keep for _, keep in launched])
+    comps = []
+    for (ks, keep), raw in zip(launched, outs):
+        hit = raw.view(np.uint8).reshape(tuple(keep.shape)).astype(bool).any(axis=0)
+        comps.append(ks[hit])
+    return comps
 
 
 def detect_component(oracle, t: int, cfg: DetectionConfig, rng: np.random.Generator | None = None):
@@ -295,9 +317,16 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
     final_coef = np.empty(0, dtype=np.complex128)
     prefixes: DeviceFreqs | None = None
 
+    hoisted = None
+    if _is_device_oracle(oracle) and not isinstance(oracle, NoisyOracle):
+        hoisted = _detect_all(dev, oracle, cfg, detect_streams)
+
     for t in range(d):
         t_step = time.perf_counter()
-        comp = _detect(dev, oracle, t, cfg, np.random.default_rng(detect_streams[t]), t)
+        if hoisted is not None:
+            comp = hoisted[t]
+        else:
+            comp = _detect(dev, oracle, t, cfg, np.random.default_rng(detect_streams[t]), t)
         rep.component_counts[t] = len(comp)
         rep.detection_calls[t] = cfg.r * int(box.sizes[t])
         if t == 0:
