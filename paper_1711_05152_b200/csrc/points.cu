@@ -8,20 +8,6 @@
 
 namespace sfft {
 
-__device__ double cardinal_bspline_pt(int m, double u) {
-  if (!(u >= 0.0 && u <= (double)m)) return 0.0;
-  double N[8];
-  int iv = (int)floor(u);
-  if (iv >= m) iv = m - 1;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) N[j] = (j == iv) ? 1.0 : 0.0;
-  for (int k = 2; k <= m; ++k) {
-    const double inv = 1.0 / (double)(k - 1);
-    for (int j = 0; j <= m - k; ++j) N[j] = ((u - j) * N[j] + ((double)(j + k) - u) * N[j + 1]) * inv;
-  }
-  return N[0];
-}
-
 constexpr int PCH = 256;
 
 // p(x) = sum_h c_h e^{2 pi i h.x}; phase accumulated in float64 per point
@@ -75,7 +61,7 @@ __global__ void eval_bspline_points_kernel(const double* __restrict__ pts, int64
         double x = pts[i * bs.d + bs.comps[q]];
         x = x - floor(x);  // np.mod(x, 1.0) for finite x
         if (x >= 1.0) x = 0.0;
-        term = term * (bs.scale[g] * cardinal_bspline_pt(m, (double)m * x));
+        term = term * (bs.scale[g] * cardinal_bspline(m, (double)m * x));
       }
       total += term;
     }

@@ -257,21 +257,6 @@ __global__ void poly_split_reduce_kernel(UnitTable ut, int ks, const double2* __
 // ---------------------------------------------------------------------------
 // B-spline oracle (testbed.py:198-244): f(x) = sum_g prod_{c in A_g} C_m m B_m(m x_c)
 
-// cardinal B-spline of order m (degree m-1) on knots 0..m, Cox-de Boor
-__device__ __forceinline__ double cardinal_bspline(int m, double u) {
-  if (!(u >= 0.0 && u <= (double)m)) return 0.0;
-  double N[8];
-  int iv = (int)floor(u);
-  if (iv >= m) iv = m - 1;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) N[j] = (j == iv) ? 1.0 : 0.0;
-  for (int k = 2; k <= m; ++k) {
-    const double inv = 1.0 / (double)(k - 1);
-    for (int j = 0; j <= m - k; ++j) N[j] = ((u - j) * N[j] + ((double)(j + k) - u) * N[j + 1]) * inv;
-  }
-  return N[0];
-}
-
 template <bool FAST>
 __global__ void sample_bspline_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at,
                                       const double2* __restrict__ chirp, double2* __restrict__ buf,

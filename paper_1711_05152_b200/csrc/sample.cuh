@@ -65,4 +65,38 @@ int launch_unit_norm2(const UnitTable& ut, const double2* buf, int64_t ustride, 
 int launch_lattice_nodes(const LatTable& lt, int l, int d, const AnchorTable& at, int it,
                          double* pts, bool fast, cudaStream_t st);
 
+// cardinal B-spline of order m (degree m-1) on knots 0..m, Cox-de Boor.
+// Compile-time order: the triangle is fully unrolled in registers (a runtime
+// order puts N[] in local memory and divides at every level); same
+// arithmetic, same rounding as the runtime form.
+template <int MO>
+__device__ __forceinline__ double cardinal_bspline_t(double u) {
+  if (!(u >= 0.0 && u <= (double)MO)) return 0.0;
+  double N[MO + 1];
+  int iv = (int)floor(u);
+  if (iv >= MO) iv = MO - 1;
+#pragma unroll
+  for (int j = 0; j <= MO; ++j) N[j] = (j == iv) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 2; k <= MO; ++k) {
+    const double inv = 1.0 / (double)(k - 1);
+#pragma unroll
+    for (int j = 0; j <= MO - k; ++j) N[j] = ((u - j) * N[j] + ((double)(j + k) - u) * N[j + 1]) * inv;
+  }
+  return N[0];
+}
+
+__device__ __forceinline__ double cardinal_bspline(int m, double u) {
+  switch (m) {
+    case 1: return cardinal_bspline_t<1>(u);
+    case 2: return cardinal_bspline_t<2>(u);
+    case 3: return cardinal_bspline_t<3>(u);
+    case 4: return cardinal_bspline_t<4>(u);
+    case 5: return cardinal_bspline_t<5>(u);
+    case 6: return cardinal_bspline_t<6>(u);
+    default: return cardinal_bspline_t<7>(u);
+  }
+}
+
+
 }  // namespace sfft
