@@ -280,7 +280,7 @@ __global__ void sample_bspline_kernel(UnitTable ut, LatTable lt, BsplineSpec bs,
         double x;
         if (c < t1) {
           const int64_t r = mulmod<FAST>(n, (int64_t)lt.z[l * t1 + c], M, invM);
-          x = (double)r / (double)M;
+          x = (double)r * invM;  // within 1 ulp of r / M (the reference's node), no FP64 division
         } else {
           x = at.a[it * tail + (c - t1)];
         }
@@ -288,8 +288,12 @@ __global__ void sample_bspline_kernel(UnitTable ut, LatTable lt, BsplineSpec bs,
       }
       total += term;
     }
-    const double2 v = make_double2(total, 0.0);
-    ub[n] = apply_chirp ? cmul(v, __ldg(&ch[n])) : v;
+    if (apply_chirp) {
+      const double2 c = __ldg(&ch[n]);
+      ub[n] = make_double2(total * c.x, total * c.y);  // (total + 0i) * c
+    } else {
+      ub[n] = make_double2(total, 0.0);
+    }
   }
 }
 
