@@ -608,6 +608,15 @@ int sfft_select_cap(const double* d_coef, uint8_t* d_keep, int64_t n, int cap, u
                            S(stream));
 }
 
+int64_t sfft_select_rows_scratch_bytes(int nrows) { return select_rows_scratch_bytes(nrows); }
+
+int sfft_select_cap_rows(const double* d_coef, uint8_t* d_keep, int64_t n, const int32_t* h_rows, int nrows,
+                         int cap, uint8_t* d_scratch, void* stream) {
+  if (n < 0 || cap < 0 || nrows < 0 || nrows > 64) return E_INVAL;
+  return launch_select_cap_rows((const double2*)d_coef, d_keep, n, h_rows, nrows, cap, d_scratch,
+                                num_sms_current(), S(stream));
+}
+
 int64_t sfft_scan_scratch_len(int64_t n) { return scan_scratch_len(n); }
 
 int sfft_flag_indices(const uint8_t* d_flags, int64_t n, int nrows, int32_t* d_idx,

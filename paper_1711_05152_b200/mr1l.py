@@ -640,21 +640,28 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
                      dptr(sch.masks), dptr(buf), P, rb, i0, float(delta), dptr(coef), dptr(keep),
                      dptr(counts), ctx=f"gather/select, step {step}")
     def apply_cap(counts_h):
-        counts_h = counts_h.astype(np.int64)
-        over = [i for i in range(r) if counts_h[i] > cap]
-        if over:
-            sbytes = int(_native.query("sfft_select_scratch_bytes", n))
-            scratch = dev.empty((sbytes,), torch.uint8)
-            for i in over:
-                dev.call("sfft_select_cap", dptr(coef[i]), dptr(keep[i]), n, int(cap), dptr(scratch),
-                         ctx=f"cap selection, step {step}")
-                counts_h[i] = cap
-        return counts_h
+        return apply_cap_rows(dev, coef, keep, n, counts_h, cap, step)
 
     if defer_cap:
         wait = dev.download_async(counts)
         return StepResult(keep, coef, None, nodes, _finish=lambda: apply_cap(wait()))
     return StepResult(keep, coef, apply_cap(dev.download_small(counts)), nodes)
+
+
+def apply_cap_rows(dev: Device, coef, keep, n: int, counts_h: np.ndarray, cap: int, step: int = 0) -> np.ndarray:
+    """The cap of detect.py:205-211 on every iteration whose survivor count
+    exceeds it: the exact radix selection of all such rows in one batched
+    launch sequence (sfft_select_cap_rows).  Returns the updated counts."""
+    counts_h = np.asarray(counts_h).astype(np.int64)
+    over = np.ascontiguousarray([i for i in range(len(counts_h)) if counts_h[i] > cap], dtype=np.int32)
+    for c0 in range(0, len(over), 64):
+        rows = np.ascontiguousarray(over[c0:c0 + 64])
+        sbytes = int(_native.query("sfft_select_rows_scratch_bytes", len(rows)))
+        scratch = dev.empty((max(sbytes, 1),), dev.torch.uint8)
+        dev.call("sfft_select_cap_rows", dptr(coef), dptr(keep), n, hptr(rows), len(rows), int(cap),
+                 dptr(scratch), ctx=f"cap selection, step {step}")
+    counts_h[over] = cap
+    return counts_h
 
 
 def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):

@@ -18,7 +18,8 @@ import math
 import numpy as np
 
 from .device import Device, dptr, hptr
-from .mr1l import (RBMAX, UMAX, DeviceFreqs, DeviceScheme, StepResult, _sample_units, lattice_tables)
+from .mr1l import (RBMAX, UMAX, DeviceFreqs, DeviceScheme, StepResult, _sample_units, apply_cap_rows,
+                   lattice_tables)
 from .oracles import NoisyOracle
 from . import _native
 
@@ -137,13 +138,5 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
         dev.call("sfft_combine_units", n, L, dptr(sch.masks), dptr(allrows), hptr(rmap), rb, rb, 0,
                  float(delta), dptr(coef[i0]), dptr(keep[i0]), dptr(counts[i0:]),
                  ctx=f"combine, step {step}")
-    counts_h = dev.download_small(counts).astype(np.int64)
-    over = [i for i in range(r) if counts_h[i] > cap]
-    if over:
-        sbytes = int(_native.query("sfft_select_scratch_bytes", n))
-        scratch = dev.empty((sbytes,), torch.uint8)
-        for i in over:
-            dev.call("sfft_select_cap", dptr(coef[i]), dptr(keep[i]), n, int(cap), dptr(scratch),
-                     ctx=f"cap selection, step {step}")
-            counts_h[i] = cap
+    counts_h = apply_cap_rows(dev, coef, keep, n, dev.download_small(counts), cap, step)
     return StepResult(keep, coef, counts_h, nodes)
