@@ -561,15 +561,20 @@ struct SelRows {
   int row[64];
 };
 
+constexpr int SEL_TIE_LIST = 2048;  // tie entries resolved by rank in shared memory
+
 struct SelRowState {
   unsigned long long prefix, pmask;
   int need, done;  // done: CTAs finished with the current pass
+  int count_eq;    // entries whose key equals the threshold (after the last pass)
+  int nlist;       // tie entries appended by selr_apply
   int hist[256];
+  int list[SEL_TIE_LIST];
 };
 
 __global__ void selr_init_kernel(SelRowState* st, int cap) {
   SelRowState& s = st[blockIdx.x];
-  if (threadIdx.x == 0) { s.prefix = 0; s.pmask = 0; s.need = cap; s.done = 0; }
+  if (threadIdx.x == 0) { s.prefix = 0; s.pmask = 0; s.need = cap; s.done = 0; s.count_eq = 0; s.nlist = 0; }
   s.hist[threadIdx.x] = 0;
 }
 
@@ -610,31 +615,57 @@ __global__ void selr_pass_kernel(const double2* __restrict__ coef, const uint8_t
     s.prefix |= ((unsigned long long)dsel) << shift;
     s.pmask |= 255ull << shift;
     s.need = need - above;
+    s.count_eq = h[dsel];
     s.done = 0;
   }
 }
 
-// keep <- key > T; entries with key == T are marked 2 (resolved by selr_ties)
+// keep <- key > T; entries with key == T: all kept when they are exactly the
+// `need` still missing, otherwise marked 2 and listed for selr_ties
 __global__ void selr_apply_kernel(const double2* __restrict__ coef, uint8_t* __restrict__ keep, int64_t n,
-                                  SelRows rows, const SelRowState* __restrict__ st) {
+                                  SelRows rows, SelRowState* st) {
   const int y = blockIdx.y;
-  const unsigned long long T = st[y].prefix;
+  SelRowState& s = st[y];
+  const unsigned long long T = s.prefix;
+  const bool all_ties = s.count_eq == s.need;
   const double2* c = coef + (int64_t)rows.row[y] * n;
   uint8_t* k = keep + (int64_t)rows.row[y] * n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (!k[i]) continue;
     const unsigned long long key = mag_key(c[i]);
-    k[i] = key > T ? 1 : (key == T ? 2 : 0);
+    if (key == T && !all_ties) {
+      const int pos = atomicAdd(&s.nlist, 1);
+      if (pos < SEL_TIE_LIST) s.list[pos] = (int)i;
+      k[i] = 2;
+    } else {
+      k[i] = key >= T ? 1 : 0;
+    }
   }
 }
 
 // one CTA per row: the first `need` tie entries in index order are kept
+// (rank within the appended list; a sequential block scan if it overflowed)
 __global__ void __launch_bounds__(1024) selr_ties_kernel(uint8_t* __restrict__ keep, int64_t n, SelRows rows,
                                                          const SelRowState* __restrict__ st) {
   __shared__ int wsum[32];
   __shared__ int base;
+  __shared__ int lst[SEL_TIE_LIST];
+  const SelRowState& s = st[blockIdx.x];
+  if (s.count_eq == s.need) return;  // every tie kept in selr_apply
   uint8_t* k = keep + (int64_t)rows.row[blockIdx.x] * n;
-  const int need = st[blockIdx.x].need;
+  const int need = s.need;
+  const int nl = s.nlist;
+  if (nl <= SEL_TIE_LIST) {
+    for (int j = threadIdx.x; j < nl; j += blockDim.x) lst[j] = s.list[j];
+    __syncthreads();
+    for (int j = threadIdx.x; j < nl; j += blockDim.x) {
+      const int v = lst[j];
+      int rank = 0;
+      for (int q = 0; q < nl; ++q) rank += lst[q] < v;
+      k[v] = rank < need ? 1 : 0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) base = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
