@@ -164,10 +164,13 @@ int64_t sfft_select_scratch_bytes(int64_t n);
 int sfft_select_cap(const double* d_coef, uint8_t* d_keep, int64_t n, int cap,
                     uint8_t* d_scratch, void* stream);
 /* the same cap selection for `nrows` iterations at once: rows h_rows[i] of
- * d_coef (r, n, 2) / d_keep (r, n); scratch = sfft_select_rows_scratch_bytes */
+ * d_coef (r, n, 2) / d_keep (r, n); scratch = sfft_select_rows_scratch_bytes.
+ * d_counts (nullable, int32 per row): when given, a row is capped only if its
+ * survivor count exceeds `cap` (decided on the device, count set to cap), so
+ * the caller needs no host read-back of the counts. */
 int64_t sfft_select_rows_scratch_bytes(int nrows);
 int sfft_select_cap_rows(const double* d_coef, uint8_t* d_keep, int64_t n, const int32_t* h_rows,
-                         int nrows, int cap, uint8_t* d_scratch, void* stream);
+                         int nrows, int cap, int32_t* d_counts, uint8_t* d_scratch, void* stream);
 
 /* ---- compaction / sets (detect.py:257-260, 367-371, 412; lattice.py:97-109) */
 int64_t sfft_scan_scratch_len(int64_t n);

@@ -48,7 +48,7 @@ _SIGS = {
     "sfft_select_scratch_bytes": (_i64, [_i64]),
     "sfft_select_cap": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
     "sfft_select_rows_scratch_bytes": (_i64, [_int]),
-    "sfft_select_cap_rows": (_int, [_vp, _vp, _i64, _vp, _int, _int, _vp, _vp]),
+    "sfft_select_cap_rows": (_int, [_vp, _vp, _i64, _vp, _int, _int, _vp, _vp, _vp]),
     "sfft_scan_scratch_len": (_i64, [_i64]),
     "sfft_flag_indices": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp]),
     "sfft_gather_rows": (_int, [_vp, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),

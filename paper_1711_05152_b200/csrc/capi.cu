@@ -611,9 +611,9 @@ int sfft_select_cap(const double* d_coef, uint8_t* d_keep, int64_t n, int cap, u
 int64_t sfft_select_rows_scratch_bytes(int nrows) { return select_rows_scratch_bytes(nrows); }
 
 int sfft_select_cap_rows(const double* d_coef, uint8_t* d_keep, int64_t n, const int32_t* h_rows, int nrows,
-                         int cap, uint8_t* d_scratch, void* stream) {
+                         int cap, int32_t* d_counts, uint8_t* d_scratch, void* stream) {
   if (n < 0 || cap < 0 || nrows < 0 || nrows > 64) return E_INVAL;
-  return launch_select_cap_rows((const double2*)d_coef, d_keep, n, h_rows, nrows, cap, d_scratch,
+  return launch_select_cap_rows((const double2*)d_coef, d_keep, n, h_rows, nrows, cap, d_counts, d_scratch,
                                 num_sms_current(), S(stream));
 }
 

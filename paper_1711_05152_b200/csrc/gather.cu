@@ -568,13 +568,24 @@ struct SelRowState {
   int need, done;  // done: CTAs finished with the current pass
   int count_eq;    // entries whose key equals the threshold (after the last pass)
   int nlist;       // tie entries appended by selr_apply
+  int active;      // the row's survivor count exceeds the cap (device-side decision)
   int hist[256];
   int list[SEL_TIE_LIST];
 };
 
-__global__ void selr_init_kernel(SelRowState* st, int cap) {
+// d_counts (optional): survivor counts per row of keep; rows not above the cap
+// are left untouched by every later kernel, capped rows get count = cap
+__global__ void selr_init_kernel(SelRowState* st, int cap, SelRows rows, int32_t* counts) {
   SelRowState& s = st[blockIdx.x];
-  if (threadIdx.x == 0) { s.prefix = 0; s.pmask = 0; s.need = cap; s.done = 0; s.count_eq = 0; s.nlist = 0; }
+  if (threadIdx.x == 0) {
+    s.prefix = 0; s.pmask = 0; s.need = cap; s.done = 0; s.count_eq = 0; s.nlist = 0;
+    s.active = 1;
+    if (counts) {
+      const int c = counts[rows.row[blockIdx.x]];
+      s.active = c > cap;
+      if (s.active) counts[rows.row[blockIdx.x]] = cap;
+    }
+  }
   s.hist[threadIdx.x] = 0;
 }
 
@@ -584,6 +595,7 @@ __global__ void selr_pass_kernel(const double2* __restrict__ coef, const uint8_t
   __shared__ bool last;
   const int y = blockIdx.y;
   SelRowState& s = st[y];
+  if (!s.active) return;
   const double2* c = coef + (int64_t)rows.row[y] * n;
   const uint8_t* k = keep + (int64_t)rows.row[y] * n;
   h[threadIdx.x] = 0;
@@ -626,6 +638,7 @@ __global__ void selr_apply_kernel(const double2* __restrict__ coef, uint8_t* __r
                                   SelRows rows, SelRowState* st) {
   const int y = blockIdx.y;
   SelRowState& s = st[y];
+  if (!s.active) return;
   const unsigned long long T = s.prefix;
   const bool all_ties = s.count_eq == s.need;
   const double2* c = coef + (int64_t)rows.row[y] * n;
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(1024) selr_ties_kernel(uint8_t* __restrict__ k
   __shared__ int base;
   __shared__ int lst[SEL_TIE_LIST];
   const SelRowState& s = st[blockIdx.x];
-  if (s.count_eq == s.need) return;  // every tie kept in selr_apply
+  if (!s.active || s.count_eq == s.need) return;  // nothing capped, or every tie kept in selr_apply
   uint8_t* k = keep + (int64_t)rows.row[blockIdx.x] * n;
   const int need = s.need;
   const int nl = s.nlist;
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(1024) selr_ties_kernel(uint8_t* __restrict__ k
 int64_t select_rows_scratch_bytes(int nrows) { return (int64_t)nrows * sizeof(SelRowState); }
 
 int launch_select_cap_rows(const double2* coef, uint8_t* keep, int64_t n, const int32_t* h_rows, int nrows,
-                           int cap, uint8_t* scratch, int num_sms, cudaStream_t st) {
+                           int cap, int32_t* counts, uint8_t* scratch, int num_sms, cudaStream_t st) {
   if (n == 0 || nrows == 0) return 0;
   if (nrows > 64) return -7;
   SelRows rows;
@@ -700,7 +713,7 @@ int launch_select_cap_rows(const double2* coef, uint8_t* keep, int64_t n, const 
   int64_t want = (n + 255) / 256;
   int64_t capb = ((int64_t)num_sms * 4 + nrows - 1) / nrows;
   const unsigned blocks = (unsigned)(want < capb ? want : capb);
-  selr_init_kernel<<<nrows, 256, 0, st>>>(s, cap);
+  selr_init_kernel<<<nrows, 256, 0, st>>>(s, cap, rows, counts);
   for (int dgt = 7; dgt >= 0; --dgt)
     selr_pass_kernel<<<dim3(blocks, nrows), 256, 0, st>>>(coef, keep, n, rows, s, dgt * 8);
   selr_apply_kernel<<<dim3(blocks, nrows), 256, 0, st>>>(coef, keep, n, rows, s);

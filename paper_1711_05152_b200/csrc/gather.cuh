@@ -25,7 +25,7 @@ int launch_gather_rows(const int32_t* in, int64_t n_in, int ncomp, const int32_t
 int64_t select_scratch_bytes(int64_t n);
 int64_t select_rows_scratch_bytes(int nrows);
 int launch_select_cap_rows(const double2* coef, uint8_t* keep, int64_t n, const int32_t* h_rows, int nrows,
-                           int cap, uint8_t* scratch, int num_sms, cudaStream_t st);
+                           int cap, int32_t* counts, uint8_t* scratch, int num_sms, cudaStream_t st);
 int launch_select_cap(const double2* coef, uint8_t* keep, int64_t n, int cap, uint8_t* scratch,
                       int num_sms, cudaStream_t st);
 int launch_product(const int32_t* pref, int64_t np, int t, const int32_t* comp, int64_t nc,

@@ -377,7 +377,8 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
         if sharded:
             res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
         else:
-            res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t, prep=sch.prep)
+            res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t, prep=sch.prep,
+                           device_cap=True)
         if last:
             rows_d, coef_d = compact(dev, cand, res.keep[0], 1, res.coef[0])
             final_rows = rows_d.to_host(dev)

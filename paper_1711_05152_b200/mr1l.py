@@ -589,14 +589,16 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
 def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
              d: int, delta: float, cap: int, step: int = 0, tabs: LatticeTables | None = None,
              timer: StageTimer | None = None, defer_cap: bool = False,
-             prep: StepPrep | None = None) -> StepResult:
+             prep: StepPrep | None = None, device_cap: bool = False) -> StepResult:
     """Sample, transform and invert all r~ iterations of one step; threshold + cap.
 
     ``defer_cap``: return as soon as the work is enqueued; the survivor counts
     come back asynchronously and the cap is applied by ``StepResult.finalize()``
     (or the first ``.counts`` access), so the host can prepare the next
     independent step while this one runs.  ``prep``: buffers and tables made
-    by ``prepare_step`` while the alias kernel ran."""
+    by ``prepare_step`` while the alias kernel ran.  ``device_cap``: the cap
+    is decided and applied on the device for every iteration (no host
+    read-back at all; ``.counts`` downloads on first use)."""
     torch = dev.torch
     tm = timer or _NoTimer()
     n = cand.n
@@ -642,6 +644,16 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     def apply_cap(counts_h):
         return apply_cap_rows(dev, coef, keep, n, counts_h, cap, step)
 
+    if device_cap:
+        for c0 in range(0, r, 64):
+            rows = np.arange(c0, min(r, c0 + 64), dtype=np.int32)
+            sbytes = int(_native.query("sfft_select_rows_scratch_bytes", len(rows)))
+            scratch_sel = dev.empty((max(sbytes, 1),), torch.uint8)
+            dev.call("sfft_select_cap_rows", dptr(coef), dptr(keep), n, hptr(rows), len(rows), int(cap),
+                     dptr(counts), dptr(scratch_sel), ctx=f"cap selection, step {step}")
+        return StepResult(keep, coef, None, nodes,
+                          _finish=lambda: dev.download_small(counts).astype(np.int64))
+
     if defer_cap:
         wait = dev.download_async(counts)
         return StepResult(keep, coef, None, nodes, _finish=lambda: apply_cap(wait()))
@@ -658,7 +670,7 @@ def apply_cap_rows(dev: Device, coef, keep, n: int, counts_h: np.ndarray, cap: i
         rows = np.ascontiguousarray(over[c0:c0 + 64])
         sbytes = int(_native.query("sfft_select_rows_scratch_bytes", len(rows)))
         scratch = dev.empty((max(sbytes, 1),), dev.torch.uint8)
-        dev.call("sfft_select_cap_rows", dptr(coef), dptr(keep), n, hptr(rows), len(rows), int(cap),
+        dev.call("sfft_select_cap_rows", dptr(coef), dptr(keep), n, hptr(rows), len(rows), int(cap), 0,
                  dptr(scratch), ctx=f"cap selection, step {step}")
     counts_h[over] = cap
     return counts_h
