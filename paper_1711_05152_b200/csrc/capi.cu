@@ -271,7 +271,7 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
   while (((int64_t)1 << (2 * bl)) < mmax) ++bl;
   pp->bl = bl;
   pp->kind = sample_kind();
-  if (pp->kind >= 1 && sample_poly_ws_smem(bl, mmax) > 227 * 1024) pp->kind = 0;
+  if (pp->kind >= 1 && sample_poly_ws_smem(bl, mmax) > 227 * 1024 - 256) pp->kind = 0;  // + static mbarriers
   const size_t smem = pp->kind >= 1 ? sample_poly_ws_smem(bl, mmax) : sample_poly_smem(bl, mmax);
   if (smem > 227 * 1024) return E_2BIG;
   // resident CTAs per SM: classic 2 by registers (256 threads x 128 regs),

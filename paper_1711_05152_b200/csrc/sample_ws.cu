@@ -42,6 +42,23 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// mbarrier handshake (TC path): consumer warps wait on `full` independently
+// instead of meeting at a CTA-wide named barrier every stage
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+      ::"r"(smem_addr(b)), "r"(parity) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ws_barrett(uint64_t x, uint32_t m, uint64_t mu) {
   const uint64_t q = __umul64hi(x, mu);
   uint64_t r = x - q * (uint64_t)m;
@@ -99,6 +116,13 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
   const int nhi = (int)((M + nlo - 1) >> bl);
   for (int i = threadIdx.x; i < nlo; i += NT) tlo[i] = __ldg(&twl[i < M ? i : 0]);
   for (int i = threadIdx.x; i < nhi; i += NT) thi[i] = __ldg(&twl[(int64_t)i << bl]);
+  __shared__ uint64_t mbar[2 * NS];  // TC: full[s] (NPROD arrivals), empty[s] (one per consumer warp)
+  if (TC && threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&mbar[i], NPROD);
+      mbar_init(&mbar[NS + i], NCONS / 32);
+    }
+  }
   __syncthreads();
 
   if (threadIdx.x >= NCONS) {
@@ -131,7 +155,10 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
       const uint32_t r = nr, qq = nq;
       const double2 cf = nc;
       fetch(c + 1);
-      if (c >= NS) bar_sync(1 + NS + st, NT);  // consumers released the stage
+      if (c >= NS) {  // consumers released the stage
+        if (TC) mbar_wait(&mbar[NS + st], ((c / NS) - 1) & 1);
+        else bar_sync(1 + NS + st, NT);
+      }
       double2* As = sm + st * STAGE;
       double2* Bs = As + KC * TJ1;
       // A[gh][gt + 8 i], i < 8: one lookup, recurrence by w^{8 r};
@@ -186,6 +213,8 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
             v[2] = cmul(v[2], eb);
           }
         }
+        mbar_arrive(&mbar[st]);  // stage full (release of this thread's stores)
+        continue;
       }
       bar_arrive(1 + st, NT);  // stage full
     }
@@ -205,7 +234,7 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
       for (int y = 0; y < 4; ++y) cr[x][y] = ci[x][y] = make_double2(0.0, 0.0);
     for (int c = 0; c < nchunk; ++c) {
       const int st = c % NS;
-      bar_sync(1 + st, NT);  // stage full
+      mbar_wait(&mbar[st], (c / NS) & 1);  // stage full
       const double* a_re = (const double*)(sm + st * STAGE);
       const double* a_im = a_re + KC * TJ1;
       const double* b_re = a_im + KC * TJ1;
@@ -242,7 +271,8 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
 #pragma unroll
           for (int y = 0; y < 4; ++y) dmma_acc(ci[x][y], ai[x], br[y]);
       }
-      if (c + NS < nchunk) bar_arrive(1 + NS + st, NT);  // stage empty (only if it will be refilled)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mbar[NS + st]);  // stage empty (this warp is done reading it)
     }
     const double2* ch = chirp + lt.off[l];
     double2* ub = SPLIT ? part + ((int64_t)q * pp.nunits + u) * pstride : buf + (int64_t)u * ustride;
