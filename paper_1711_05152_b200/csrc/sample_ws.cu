@@ -16,6 +16,8 @@
 // MMA fragment order, so every consumer operand load is one conflict-free
 // 256 B LDS.64 per warp.  (tcgen05 has no FP64 kind: mma.sync is the FP64
 // tensor path on sm_100a.)
+#include <cstring>
+#include <cstdlib>
 #include "common.cuh"
 #include "plan.cuh"
 #include "sample.cuh"
@@ -345,6 +347,231 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent TC variant: one CTA per SM walks a contiguous range of work items
+// (item = one (tile, term slice), the CTA of the kernel above).  The stage
+// ring and its mbarriers run across item boundaries, so the producers fill
+// the next item's first stages (reloading the twiddle tables, which only
+// they read, when the lattice changes) while the consumers run the previous
+// item's epilogue; no per-CTA launch, table load or pipeline fill per item.
+// Per item the arithmetic is exactly that of sample_poly_ws_kernel<SPLIT, true>.
+struct WsItem {
+  int u, l, it, q, nchunk, h_begin, h_end;
+  uint32_t j1_0, j2_0;
+};
+
+__device__ __forceinline__ WsItem ws_item(const PolyPlan& pp, int w) {
+  using namespace ws;
+  int lo = 0, hi = pp.nunits - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pp.tile_start[mid] <= w) lo = mid; else hi = mid - 1;
+  }
+  WsItem x;
+  x.u = lo;
+  x.l = pp.unit_lat[lo];
+  x.it = pp.unit_it[lo];
+  const int local = w - pp.tile_start[lo];
+  x.q = local % pp.ks;
+  const int tau = local / pp.ks;
+  const int nt1 = pp.nt1[x.l];
+  x.j1_0 = (uint32_t)(tau % nt1) * TJ1;
+  x.j2_0 = (uint32_t)(tau / nt1) * TJ2;
+  x.h_begin = x.q * pp.kper;
+  x.h_end = min(pp.s, x.h_begin + pp.kper);
+  x.nchunk = x.h_end > x.h_begin ? (x.h_end - x.h_begin + KC - 1) / KC : 0;
+  return x;
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(ws::NT, 1)
+sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
+                       const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
+                       const double2* __restrict__ tw, const double2* __restrict__ chirp,
+                       double2* __restrict__ buf, int64_t ustride, int apply_chirp,
+                       double2* __restrict__ part, int64_t pstride) {
+  using namespace ws;
+  extern __shared__ double2 sm[];
+  __shared__ uint64_t mbar[2 * NS];  // full[s] (NPROD arrivals), empty[s] (one per consumer warp)
+  double2* tlo = sm + NS * STAGE;
+  double2* thi = tlo + (1 << pp.bl);
+  const int items = pp.tile_start[pp.nunits];
+  const int w0 = (int)(((int64_t)blockIdx.x * items) / gridDim.x);
+  const int w1 = (int)(((int64_t)(blockIdx.x + 1) * items) / gridDim.x);
+  const int bl = pp.bl;
+  const int s = pp.s;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&mbar[i], NPROD);
+      mbar_init(&mbar[NS + i], NCONS / 32);
+    }
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= NCONS) {
+    // ---------------- producers ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PROD));
+    const int pt = threadIdx.x - NCONS;
+    const int gh = pt >> 3;  // term of the stage (0..15)
+    const int gt = pt & 7;   // row / column phase
+    const int nlo = 1 << bl;
+    const int la = gt * 4 + (gh & 3);
+    const int ka = (gh >> 2) * 8 * 32 + la;
+    const int kb = (gh >> 2) * 16 * 32 + la;
+    int cur_lat = -1;
+    int gc = 0;  // stage-ring position over all items of this CTA
+    for (int w = w0; w < w1; ++w) {
+      const WsItem x = ws_item(pp, w);
+      const int64_t M = lt.m[x.l];
+      if (x.l != cur_lat) {
+        bar_sync(1, NPROD);  // every producer is past its last read of the old tables
+        const double2* twl = tw + lt.off[x.l];
+        const int nhi = (int)((M + nlo - 1) >> bl);
+        for (int i = pt; i < nlo; i += NPROD) tlo[i] = __ldg(&twl[i < M ? i : 0]);
+        for (int i = pt; i < nhi; i += NPROD) thi[i] = __ldg(&twl[(int64_t)i << bl]);
+        bar_sync(1, NPROD);
+        cur_lat = x.l;
+      }
+      const uint32_t M32 = (uint32_t)M;
+      const uint64_t mu = pp.mu[x.l];
+      const double2* cp = cprime + (int64_t)x.it * s;
+      const int32_t* rr = rres + (int64_t)x.l * s;
+      const int32_t* rj = rjs + (int64_t)x.l * s;
+      uint32_t nr = 0, nq = 0;
+      double2 nc = make_double2(0.0, 0.0);
+      {
+        const int h = x.h_begin + gh;
+        if (x.nchunk > 0 && h < x.h_end) {
+          nr = (uint32_t)__ldg(&rr[h]);
+          nq = (uint32_t)__ldg(&rj[h]);
+          nc = __ldg(&cp[h]);
+        }
+      }
+      for (int c = 0; c < x.nchunk; ++c, ++gc) {
+        const int st = gc % NS;
+        const int h = x.h_begin + c * KC + gh;
+        const bool live = h < x.h_end;
+        const uint32_t r = nr, qq = nq;
+        const double2 cf = nc;
+        {  // per-term data one stage ahead
+          const int hn = h + KC;
+          if (c + 1 < x.nchunk && hn < x.h_end) {
+            nr = (uint32_t)__ldg(&rr[hn]);
+            nq = (uint32_t)__ldg(&rj[hn]);
+            nc = __ldg(&cp[hn]);
+          }
+        }
+        if (gc >= NS) mbar_wait(&mbar[NS + st], ((gc / NS) - 1) & 1);  // consumers released the stage
+        double* a_re = (double*)(sm + st * STAGE);
+        double* a_im = a_re + KC * TJ1;
+        double* b_re = a_im + KC * TJ1;
+        double* b_im = b_re + KC * TJ2;
+        double2 ea = make_double2(1.0, 0.0), eb = make_double2(1.0, 0.0);
+        double2 v[3];
+        v[0] = make_double2(0.0, 0.0);
+        v[1] = v[2] = make_double2(1.0, 0.0);
+        if (live) {
+          ea = ws_tw(tlo, thi, ws_barrett((uint64_t)r * 8u, M32, mu), bl);
+          eb = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * 8u, M32, mu), bl);
+          v[0] = cmul(cf, ws_tw(tlo, thi, ws_barrett((uint64_t)r * (x.j1_0 + gt), M32, mu), bl));
+          v[1] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (x.j2_0 + gt), M32, mu), bl);
+          v[2] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (x.j2_0 + gt + 64u), M32, mu), bl);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          a_re[ka + i * 32] = v[0].x;
+          a_im[ka + i * 32] = v[0].y;
+          b_re[kb + i * 32] = v[1].x;
+          b_im[kb + i * 32] = v[1].y;
+          b_re[kb + (i + 8) * 32] = v[2].x;
+          b_im[kb + (i + 8) * 32] = v[2].y;
+          if (i < 7) {
+            v[0] = cmul(v[0], ea);
+            v[1] = cmul(v[1], eb);
+            v[2] = cmul(v[2], eb);
+          }
+        }
+        mbar_arrive(&mbar[st]);  // stage full
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONS));
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  const int bi0 = (wv & 1) * 4;   // 4 row blocks (j1) of 8
+  const int bj0 = (wv >> 1) * 4;  // 4 column blocks (j2) of 8
+  int gc = 0;
+  for (int w = w0; w < w1; ++w) {
+    const WsItem x = ws_item(pp, w);
+    double2 cr[4][4], ci[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cr[i][j] = ci[i][j] = make_double2(0.0, 0.0);
+    for (int c = 0; c < x.nchunk; ++c, ++gc) {
+      const int st = gc % NS;
+      mbar_wait(&mbar[st], (gc / NS) & 1);  // stage full
+      const double* a_re = (const double*)(sm + st * STAGE);
+      const double* a_im = a_re + KC * TJ1;
+      const double* b_re = a_im + KC * TJ1;
+      const double* b_im = b_re + KC * TJ2;
+#pragma unroll
+      for (int kk = 0; kk < KC / 4; ++kk) {
+        double ar[4], ai[4], nai[4], br[4], bm[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ar[i] = a_re[(kk * 8 + bi0 + i) * 32 + lane];
+          ai[i] = a_im[(kk * 8 + bi0 + i) * 32 + lane];
+          nai[i] = -ai[i];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          br[j] = b_re[(kk * 16 + bj0 + j) * 32 + lane];
+          bm[j] = b_im[(kk * 16 + bj0 + j) * 32 + lane];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_acc(cr[i][j], ar[i], br[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_acc(ci[i][j], ar[i], bm[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_acc(cr[i][j], nai[i], bm[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_acc(ci[i][j], ai[i], br[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mbar[NS + st]);  // stage empty
+    }
+    const int64_t M = lt.m[x.l];
+    const int64_t J1 = pp.J1[x.l];
+    const double2* ch = chirp + lt.off[x.l];
+    double2* ub = SPLIT ? part + ((int64_t)x.q * pp.nunits + x.u) * pstride : buf + (int64_t)x.u * ustride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t j1 = x.j1_0 + (bi0 + i) * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t j2 = x.j2_0 + (bj0 + j) * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t n = j1 + J1 * (j2 + e);
+          const double2 v = make_double2(e ? cr[i][j].y : cr[i][j].x, e ? ci[i][j].y : ci[i][j].x);
+          if (n < M) ub[n] = (!SPLIT && apply_chirp) ? cmul(v, __ldg(&ch[n])) : v;
+        }
+      }
+    }
+  }
+}
+
 size_t sample_poly_ws_smem(int bl, int64_t mmax) {
   const int64_t nlo = (int64_t)1 << bl;
   const int64_t nhi = (mmax + nlo - 1) / nlo;
@@ -361,6 +588,28 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
   const size_t smem = sample_poly_ws_smem(pp.bl, mmax);
   const bool tc = pp.kind == 2;
+  static const bool persistent = [] {
+    const char* e = getenv("SFFT_B200_TC_PERSISTENT");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  if (tc && persistent) {
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = ctas < nsm ? ctas : nsm;
+    const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
+    cudaError_t e2 = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return (int)e2;
+    prof_mark(PROF_SAMPLE, true, st);
+    if (pp.ks > 1)
+      sample_poly_tcp_kernel<true><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
+                                                               apply_chirp ? 1 : 0, part, pstride);
+    else
+      sample_poly_tcp_kernel<false><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
+                                                                apply_chirp ? 1 : 0, nullptr, 0);
+    prof_mark(PROF_SAMPLE, false, st);
+    SFFT_CHECK_LAUNCH();
+    return 0;
+  }
   const void* fn = pp.ks > 1 ? (tc ? (const void*)sample_poly_ws_kernel<true, true>
                                    : (const void*)sample_poly_ws_kernel<true, false>)
                              : (tc ? (const void*)sample_poly_ws_kernel<false, true>
