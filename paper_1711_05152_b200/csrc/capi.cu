@@ -288,6 +288,7 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
     choose_j1(h_m[l], tw2, j1, nt1, nt2);
     pp->J1[l] = j1;
     pp->nt1[l] = nt1;
+    pp->nt2[l] = nt2;
     tiles_l[l] = (int64_t)nt1 * nt2;
     pp->mu[l] = ~0ull / (uint64_t)h_m[l];
   }
@@ -324,7 +325,20 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
   }
   pp->tile_start[ut.nunits] = (int)acc;
   if (acc > 0x7fffffffLL) return E_2BIG;
-  *need = best_ks > 1 ? (int64_t)best_ks * pp->nunits * mmax : 0;
+  const int64_t partials = best_ks > 1 ? (int64_t)best_ks * pp->nunits * mmax : 0;
+  *need = partials;
+  if (pp->kind == 2) {
+    pp->nchunk_max = (best_kper + 15) / 16;
+    int64_t blocks = 0;
+    for (int l = 0; l < L; ++l) {
+      pp->panel_off[l] = (int)blocks;
+      blocks += (int64_t)best_ks * pp->nt2[l] * pp->nchunk_max;
+    }
+    if (blocks > 0x7fffffffLL / 2048) return E_2BIG;
+    pp->npanels = (int)blocks;
+    pp->panel_base = ((partials + 2047) / 2048) * 2048;  // 32 KB aligned (complex elements)
+    *need = pp->panel_base + blocks * 2048;
+  }
   return 0;
 }
 
@@ -466,6 +480,7 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
   int64_t need = 0;
   rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), partial_len, &need);
   if (rc) { delete pp; return rc; }
+  if (need > partial_len) { delete pp; return E_2BIG; }  // scratch smaller than sfft_sample_poly_scratch
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
   cudaStream_t st = S(stream);

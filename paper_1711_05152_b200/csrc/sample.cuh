@@ -24,6 +24,15 @@ struct PolyPlan {
   int J1[SFFT_LMAX];
   int nt1[SFFT_LMAX];
   uint64_t mu[SFFT_LMAX];         // Barrett constants floor((2^64-1) / M_l)
+  // kind 2: B operand panels (16 terms x 128 columns, 32 KB in MMA fragment
+  // order) precomputed once per (lattice, slice, column tile, chunk) in the
+  // sampling scratch at complex offset panel_base; block index
+  // panel_off[l] + (q * nt2[l] + tj2) * nchunk_max + c
+  int nt2[SFFT_LMAX];
+  int panel_off[SFFT_LMAX];
+  int nchunk_max;
+  int npanels;
+  long long panel_base;
 };
 
 // B-spline test function: groups of (order, component slots)

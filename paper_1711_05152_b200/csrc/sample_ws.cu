@@ -61,6 +61,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
       ::"r"(smem_addr(b)), "r"(parity) : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+// bulk global -> shared copy completing on an mbarrier (no tensor map)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ws_barrett(uint64_t x, uint32_t m, uint64_t mu) {
   const uint64_t q = __umul64hi(x, mu);
   uint64_t r = x - q * (uint64_t)m;
@@ -383,13 +392,60 @@ __device__ __forceinline__ WsItem ws_item(const PolyPlan& pp, int w) {
   return x;
 }
 
+// B operand panels: block b = (lattice l, slice q, column tile tj2, chunk c)
+// holds B[h][j2] = w^{(rJ_h j2) mod M} for the chunk's 16 terms and the
+// tile's 128 columns, real / imaginary planes in MMA fragment order (the
+// stage layout), dead terms (past the slice) = 1.  B depends only on the
+// lattice, so every tile along j1 and every iteration share it; the sampling
+// producers then fetch it with one bulk copy per stage instead of
+// generating it per CTA.
+__global__ void __launch_bounds__(128) poly_bpanel_kernel(PolyPlan pp, LatTable lt, const int32_t* __restrict__ rjs,
+                                                          const double2* __restrict__ tw, double* __restrict__ panels) {
+  using namespace ws;
+  const int b = blockIdx.x;
+  int l = 0;
+  while (l + 1 < lt.nlat && pp.panel_off[l + 1] <= b) ++l;
+  const int idx = b - pp.panel_off[l];
+  const int c = idx % pp.nchunk_max;
+  const int rest = idx / pp.nchunk_max;
+  const int tj2 = rest % pp.nt2[l];
+  const int q = rest / pp.nt2[l];
+  const int64_t M = lt.m[l];
+  const uint32_t M32 = (uint32_t)M;
+  const uint64_t mu = pp.mu[l];
+  const double2* twl = tw + lt.off[l];
+  // warp kk owns terms 4 kk .. 4 kk + 3; lane = (j2 & 7) * 4 + (h & 3), the
+  // fragment order, so each store of the 16 column blocks is one contiguous
+  // 256 B warp access
+  const int kk = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hl = kk * 4 + (lane & 3);
+  const int col = lane >> 2;  // j2 = 8 bj + col
+  const int h = q * pp.kper + c * KC + hl;
+  const bool live = h < min(pp.s, (q + 1) * pp.kper);
+  double* bre = panels + (int64_t)b * (2 * KC * TJ2);
+  double* bim = bre + KC * TJ2;
+  double2 v = make_double2(1.0, 0.0), e = make_double2(1.0, 0.0);
+  if (live) {
+    const uint32_t rq = (uint32_t)__ldg(&rjs[(int64_t)l * pp.s + h]);
+    v = __ldg(&twl[ws_barrett((uint64_t)rq * (uint32_t)(tj2 * TJ2 + col), M32, mu)]);
+    e = __ldg(&twl[ws_barrett((uint64_t)rq * 8u, M32, mu)]);
+  }
+#pragma unroll
+  for (int bj = 0; bj < TJ2 / 8; ++bj) {
+    const int at = (kk * 16 + bj) * 32 + lane;
+    bre[at] = v.x;
+    bim[at] = v.y;
+    if (bj + 1 < TJ2 / 8) v = cmul(v, e);
+  }
+}
+
 template <bool SPLIT>
 __global__ void __launch_bounds__(ws::NT, 1)
 sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
                        const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
                        const double2* __restrict__ tw, const double2* __restrict__ chirp,
                        double2* __restrict__ buf, int64_t ustride, int apply_chirp,
-                       double2* __restrict__ part, int64_t pstride) {
+                       double2* __restrict__ part, int64_t pstride, const double* __restrict__ panels) {
   using namespace ws;
   extern __shared__ double2 sm[];
   __shared__ uint64_t mbar[2 * NS];  // full[s] (NPROD arrivals), empty[s] (one per consumer warp)
@@ -465,33 +521,30 @@ sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpr
         double* a_re = (double*)(sm + st * STAGE);
         double* a_im = a_re + KC * TJ1;
         double* b_re = a_im + KC * TJ1;
-        double* b_im = b_re + KC * TJ2;
-        double2 ea = make_double2(1.0, 0.0), eb = make_double2(1.0, 0.0);
-        double2 v[3];
-        v[0] = make_double2(0.0, 0.0);
-        v[1] = v[2] = make_double2(1.0, 0.0);
+        if (pt == 0) {
+          // B: the precomputed panel, one bulk copy completing on full[st]
+          const int tj2 = (int)(x.j2_0 / TJ2);
+          const double* src = panels + ((int64_t)pp.panel_off[x.l] + ((int64_t)x.q * pp.nt2[x.l] + tj2) *
+                                        pp.nchunk_max + c) * (2 * KC * TJ2);
+          mbar_expect_tx(&mbar[st], 2 * KC * TJ2 * 8);
+          bulk_g2s(b_re, src, 2 * KC * TJ2 * 8, &mbar[st]);
+        }
+        // A[gh][gt + 8 i], i < 8: one lookup, recurrence by w^{8 r}
+        double2 ea = make_double2(1.0, 0.0);
+        double2 va = make_double2(0.0, 0.0);
         if (live) {
           ea = ws_tw(tlo, thi, ws_barrett((uint64_t)r * 8u, M32, mu), bl);
-          eb = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * 8u, M32, mu), bl);
-          v[0] = cmul(cf, ws_tw(tlo, thi, ws_barrett((uint64_t)r * (x.j1_0 + gt), M32, mu), bl));
-          v[1] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (x.j2_0 + gt), M32, mu), bl);
-          v[2] = ws_tw(tlo, thi, ws_barrett((uint64_t)qq * (x.j2_0 + gt + 64u), M32, mu), bl);
+          va = cmul(cf, ws_tw(tlo, thi, ws_barrett((uint64_t)r * (x.j1_0 + gt), M32, mu), bl));
         }
+        (void)qq;
+        (void)kb;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          a_re[ka + i * 32] = v[0].x;
-          a_im[ka + i * 32] = v[0].y;
-          b_re[kb + i * 32] = v[1].x;
-          b_im[kb + i * 32] = v[1].y;
-          b_re[kb + (i + 8) * 32] = v[2].x;
-          b_im[kb + (i + 8) * 32] = v[2].y;
-          if (i < 7) {
-            v[0] = cmul(v[0], ea);
-            v[1] = cmul(v[1], eb);
-            v[2] = cmul(v[2], eb);
-          }
+          a_re[ka + i * 32] = va.x;
+          a_im[ka + i * 32] = va.y;
+          if (i < 7) va = cmul(va, ea);
         }
-        mbar_arrive(&mbar[st]);  // stage full
+        mbar_arrive(&mbar[st]);  // stage full (A stored; B lands via complete_tx)
       }
     }
     return;
@@ -592,22 +645,24 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     const char* e = getenv("SFFT_B200_TC_PERSISTENT");
     return !(e && strcmp(e, "0") == 0);
   }();
-  if (tc && persistent) {
+  if (tc && persistent && pp.npanels > 0) {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = ctas < nsm ? ctas : nsm;
     const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
     cudaError_t e2 = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return (int)e2;
+    double* panels = (double*)(part + pp.panel_base);
     prof_mark(PROF_SAMPLE, true, st);
+    poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
     if (pp.ks > 1)
       sample_poly_tcp_kernel<true><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
-                                                               apply_chirp ? 1 : 0, part, pstride);
+                                                               apply_chirp ? 1 : 0, part, pstride, panels);
     else
       sample_poly_tcp_kernel<false><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
-                                                                apply_chirp ? 1 : 0, nullptr, 0);
+                                                                apply_chirp ? 1 : 0, nullptr, 0, panels);
     prof_mark(PROF_SAMPLE, false, st);
-    SFFT_CHECK_LAUNCH();
+    SFFT_CHECK_LAUNCHES(2);
     return 0;
   }
   const void* fn = pp.ks > 1 ? (tc ? (const void*)sample_poly_ws_kernel<true, true>
