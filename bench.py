@@ -269,7 +269,7 @@ def run_ours(args):
         (``prev.finalize()``: by then the counts have long arrived), so the host
         prepares step k+1 while step k still runs, as a stream of independent
         steps would."""
-        prepare = lambda ms, z: prepare_step(dev, wl.oracle, cand, 1, ms, z)  # noqa: E731
+        prepare = lambda ms, z: prepare_step(dev, wl.oracle, cand, 1, ms, z, tails=[np.zeros(0)], d=10)  # noqa: E731
         if timer is None:
             sch = build_scheme(dev, cand, wl.b, np.random.SeedSequence(wl.lattice_seed), box_extent=64,
                                lazy_streams=True, prepare=prepare)

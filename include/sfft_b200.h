@@ -106,6 +106,21 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
                      double* d_buf, int64_t P, int apply_chirp,
                      double* d_partial, int64_t partial_len,
                      const int32_t* h_units, int nunits, void* stream);
+/* sfft_sample_poly split in its two phases: _prepare (anchor-rotated
+ * coefficients c' for rb iterations, residues r_h and r_h J1 for L lattices;
+ * depends on the sizes and vectors only, so it can run for all L_max
+ * lattices while the alias kernel decides L) and _run (everything else, for
+ * the first L lattices of the prepared set, same arguments as
+ * sfft_sample_poly). */
+int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                             const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, void* stream);
+int sfft_sample_poly_run(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                         const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                         double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                         const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                         double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
+                         void* stream);
 /* B-spline oracle (testbed.py:198-244): ngroups tensor-product terms; group g
  * has spline order h_order[g] (<= 8), scale h_scale[g] = C_m * m, and the
  * component slots h_comps[h_start[g] .. h_start[g+1]). */

@@ -194,7 +194,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     guess_fn = (lambda: spec.append(speculate_scheme(n, t1, seed_seq, b))) if fresh else None
     cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=guess_fn)
     sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z),
+                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d),
                        guess=spec[0] if spec else None)
     res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
                    defer_cap=True, prep=sch.prep)

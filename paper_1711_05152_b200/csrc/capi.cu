@@ -457,12 +457,12 @@ int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_fta
                           (const double2*)d_chirp, S(stream));
 }
 
-int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
-                     const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
-                     double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
-                     const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
-                     double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
-                     void* stream) {
+static int sample_poly_impl(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                            const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                            double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                            const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                            double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
+                            void* stream, bool do_prepare, bool do_run) {
   if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX || rb < 1) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
@@ -484,14 +484,63 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
   cudaStream_t st = S(stream);
-  rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at,
-                           (double2*)d_cprime, d_rres, d_rj, st);
-  if (!rc)
+  if (do_prepare)
+    rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at,
+                             (double2*)d_cprime, d_rres, d_rj, st);
+  if (!rc && do_run)
     rc = launch_sample_poly(*pp, lt, ut, (const double2*)d_cprime, d_rres, d_rj,
                             (const double2*)d_tw, (const double2*)d_chirp, (double2*)d_buf, P,
                             apply_chirp != 0, (double2*)d_partial, mmax, num_sms_current(), st);
   delete pp;
   return rc;
+}
+
+int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                     const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                     double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                     const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                     double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
+                     void* stream) {
+  return sample_poly_impl(d_hfreqs, d_hcoef, s, d, t1, h_m, h_z, L, h_anchor, rb, d_cprime, d_rres, d_rj, d_tw,
+                          d_chirp, d_buf, P, apply_chirp, d_partial, partial_len, h_units, nunits, stream, true,
+                          true);
+}
+
+int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                             const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, void* stream) {
+  if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX || rb < 1) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb, nullptr, 0);
+  if (rc) return rc;
+  const int tail = d - t1;
+  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  AnchorTable at;
+  at.rb = rb;
+  at.tail = tail;
+  for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
+  PolyPlan* pp = new PolyPlan;
+  int64_t need = 0;
+  rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), -1, &need);  // J1 per lattice
+  if (!rc)
+    rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at, (double2*)d_cprime, d_rres,
+                             d_rj, S(stream));
+  delete pp;
+  return rc;
+}
+
+int sfft_sample_poly_run(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
+                         const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
+                         double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                         const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
+                         double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
+                         void* stream) {
+  return sample_poly_impl(d_hfreqs, d_hcoef, s, d, t1, h_m, h_z, L, h_anchor, rb, d_cprime, d_rres, d_rj, d_tw,
+                          d_chirp, d_buf, P, apply_chirp, d_partial, partial_len, h_units, nunits, stream, false,
+                          true);
 }
 
 int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s, const int32_t* h_units,

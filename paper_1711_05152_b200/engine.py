@@ -355,12 +355,16 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             from .single import single_scheme
             sch = single_scheme(dev, cand)  # CBC (reference detect.py:269-271), no RNG consumed
         else:
+            # anchors first (their own stream, independent of the lattice search)
+            anchor_rng = np.random.default_rng(anchor_streams[t])
+            tail = d - (t + 1)
+            tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
             prepare = None
             if not sharded:
-                # while the alias kernel runs: buffers (and the tables, when this
-                # step's sizes were seen before) for the run_step that follows
+                # while the alias kernel runs: buffers, the sampling operands
+                # (and the tables, when this step's sizes were seen before)
                 prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
-                                                     cached_tables_only=True)
+                                                     cached_tables_only=True, tails=tails, d=d)
             sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
                                ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare)
         rep.scheme_sizes[t] = sch.total_size
@@ -371,9 +375,10 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
                 f"step {t}: sampling scheme covers only {cand.n - sch.uncovered}/{cand.n} "
                 f"candidates after {sch.attempts} attempts"
             )
-        anchor_rng = np.random.default_rng(anchor_streams[t])
-        tail = d - (t + 1)
-        tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
+        if cfg.lattice_kind == "single":
+            anchor_rng = np.random.default_rng(anchor_streams[t])
+            tail = d - (t + 1)
+            tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
         if sharded:
             res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
         else:

@@ -386,7 +386,8 @@ def _unit_arg(units):
 
 
 def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
-                  tails: list[np.ndarray], buf, step: int, it0: int, units=None, scratch=None):
+                  tails: list[np.ndarray], buf, step: int, it0: int, units=None, scratch=None,
+                  prepared: bool = False):
     """Fill buffer slot j with the pre-chirped samples of unit units[j]
     (global id i * L + l within this chunk of iterations; all rb * L units in
     order when ``units`` is None).  Noise streams are consumed for every unit
@@ -414,11 +415,13 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
             if scratch is not None and scratch[3].shape[0] >= max(need, 1):
                 cprime, rres, rj, part = scratch
             else:
+                prepared = False
                 cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
                 rres = dev.empty((L, max(s, 1)), torch.int32)
                 rj = dev.empty((L, max(s, 1)), torch.int32)
                 part = dev.empty((max(need, 1), 2), torch.float64)
-            dev.call("sfft_sample_poly", dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
+            dev.call("sfft_sample_poly_run" if prepared else "sfft_sample_poly",
+                     dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
                      hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
                      dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0), up, nu,
                      ctx=f"sampling, step {step}")
@@ -541,7 +544,7 @@ class StepPrep:
     the per-size tables of all L_max primes (cached; the used lattices' are a
     prefix), the output buffers, the transform buffer and the sampling scratch
     sized for L_max lattices."""
-    tabs: LatticeTables
+    tabs: LatticeTables | None  # None: not cached (run_step builds the L it uses)
     keep: object
     coef: object
     counts: object
@@ -549,10 +552,12 @@ class StepPrep:
     poly: tuple | None
     r: int
     n: int
+    poly_ready: bool = False  # c' and residues of all L_max lattices computed (attempt 1's vectors)
+    l_max: int = 0
 
 
 def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
-                 cached_tables_only: bool = False) -> StepPrep | None:
+                 cached_tables_only: bool = False, tails=None, d: int | None = None) -> StepPrep | None:
     """Host work of ``run_step`` that can overlap the alias kernel (single
     chunk of iterations, r * L_max <= the unit capacity); None otherwise.
     ``cached_tables_only``: do not build the per-size tables of all L_max
@@ -564,17 +569,21 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
     if r * L_max > UMAX or r > RBMAX:
         return None
     zs32 = np.ascontiguousarray(np.asarray(zs_all).astype(np.int32))
-    if cached_tables_only:
-        key = (fft_exponent(int(ms_all.max())),) + tuple(int(m) for m in ms_all)
-        if _TABLES.setdefault(dev.index, _TableCache()).get(key) is None:
-            return None
-    tabs = lattice_tables(dev, ms_all, zs32, ctx="lattice tables (prepared)")
+    p_all = fft_exponent(int(ms_all.max()))
+    tabs = None
+    if not cached_tables_only or \
+            _TABLES.setdefault(dev.index, _TableCache()).get((p_all,) + tuple(int(m) for m in ms_all)) is not None:
+        tabs = lattice_tables(dev, ms_all, zs32, ctx="lattice tables (prepared)")
     n = cand.n
     keep = dev.empty((r, n), torch.uint8)
     coef = dev.empty((r, n, 2), torch.float64)
     counts = dev.zeros((r,), torch.int32)
-    buf = dev.empty((r * L_max, tabs.P, 2), torch.float64)
+    # the transform buffer for all L_max lattices only while that is small
+    # (the early-exit L is about half of L_max); otherwise run_step allocates
+    buf = dev.empty((r * L_max, 1 << p_all, 2), torch.float64) \
+        if r * L_max * (16 << p_all) <= (1 << 30) else None
     poly = None
+    ready = False
     base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
     if isinstance(base, SparsePolynomialOracle):
         s = max(base.s, 1)
@@ -583,7 +592,19 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
         need = int(_native.query("sfft_sample_poly_scratch", hptr(ms_all), L_max, r, base.s, 0, 0))
         poly = (dev.empty((r, s, 2), torch.float64), dev.empty((L_max, s), torch.int32),
                 dev.empty((L_max, s), torch.int32), dev.empty((max(need, 1), 2), torch.float64))
-    return StepPrep(tabs, keep, coef, counts, buf, poly, r, n)
+        if tails is not None and d is not None and len(tails) == r and base.s > 0:
+            # anchor-rotated coefficients and the residues of every candidate
+            # lattice now; run_step then only launches the contraction
+            t1 = cand.ncomp
+            tail = d - t1
+            anchor = np.ascontiguousarray(np.asarray(tails, dtype=np.float64).reshape(r, tail)) \
+                if tail else np.zeros(1, dtype=np.float64)
+            hf, cf = base.device_terms(dev)
+            dev.call("sfft_sample_poly_prepare", dptr(hf), dptr(cf), base.s, d, t1, hptr(ms_all), hptr(zs32),
+                     L_max, hptr(anchor), r, dptr(poly[0]), dptr(poly[1]), dptr(poly[2]),
+                     ctx="sampling operands (prepared)")
+            ready = True
+    return StepPrep(tabs, keep, coef, counts, buf, poly, r, n, ready, L_max)
 
 
 def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
@@ -605,13 +626,11 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     t1 = cand.ncomp
     L = sch.L
     r = len(tails)
-    if prep is not None and (prep.r != r or prep.n != n or len(prep.tabs.ms) < L):
+    if prep is not None and (prep.r != r or prep.n != n or prep.l_max < L):
         prep = None
-    if tabs is None and prep is not None:
+    if tabs is None and prep is not None and prep.tabs is not None:
         tabs = prep.tabs.prefix(L)
-        if tabs is None:
-            prep = None
-        else:
+        if tabs is not None:
             tabs.zs = sch.z_used  # the accepted attempt's vectors
     if tabs is None:
         with tm.span("tables"):
@@ -621,7 +640,10 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     rb_alloc = min(rb_max, r)
     if prep is not None:
         keep, coef, counts, scratch = prep.keep, prep.coef, prep.counts, prep.poly
-        buf = prep.buf[: rb_alloc * L]
+        if prep.buf is not None and prep.buf.shape[1] == P:
+            buf = prep.buf[: rb_alloc * L]
+        else:
+            buf = dev.empty((rb_alloc * L, P, 2), torch.float64)
     else:
         keep = dev.empty((r, n), torch.uint8)
         coef = dev.empty((r, n, 2), torch.float64)
@@ -633,7 +655,9 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
         rb = min(rb_max, r - i0)
         with tm.span("sample"):
             nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0,
-                                   scratch=scratch)
+                                   scratch=scratch,
+                                   prepared=prep is not None and prep.poly_ready and sch.attempts == 1
+                                   and i0 == 0 and rb == r)
         with tm.span("fft"):
             dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
                      dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")
