@@ -99,7 +99,14 @@ def load() -> C.CDLL:
 
 
 class NativeError(RuntimeError):
-    """A CUDA or argument error reported by libsfft_b200."""
+    """A CUDA or argument error reported by libsfft_b200 (``code``: its status)."""
+
+    def __init__(self, msg: str, code: int = 0):
+        super().__init__(msg)
+        self.code = code
+
+
+E_2BIG = -7  # an argument exceeds a table limit / a scratch is too small
 
 
 def call(name: str, *args, ctx: str = ""):
@@ -109,7 +116,7 @@ def call(name: str, *args, ctx: str = ""):
     if rc != 0:
         msg = lib.sfft_error_string(rc).decode()
         where = f" ({ctx})" if ctx else ""
-        raise NativeError(f"{name} failed{where}: {msg} [code {rc}]")
+        raise NativeError(f"{name} failed{where}: {msg} [code {rc}]", rc)
     return rc
 
 

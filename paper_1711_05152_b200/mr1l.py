@@ -411,20 +411,32 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
         if isinstance(base, SparsePolynomialOracle):
             hf, cf = base.device_terms(dev)
             s = base.s
-            need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
-            if scratch is not None and scratch[3].shape[0] >= max(need, 1):
-                cprime, rres, rj, part = scratch
-            else:
-                prepared = False
-                cprime = dev.empty((rb, max(s, 1), 2), torch.float64)
-                rres = dev.empty((L, max(s, 1)), torch.int32)
-                rj = dev.empty((L, max(s, 1)), torch.int32)
-                part = dev.empty((max(need, 1), 2), torch.float64)
-            dev.call("sfft_sample_poly_run" if prepared else "sfft_sample_poly",
-                     dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
-                     hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
-                     dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), max(need, 0), up, nu,
-                     ctx=f"sampling, step {step}")
+
+            def launch(name, cprime, rres, rj, part):
+                dev.call(name, dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
+                         hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
+                         dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), int(part.shape[0]), up, nu,
+                         ctx=f"sampling, step {step}")
+
+            done = False
+            if scratch is not None:
+                # the library checks the scratch against this plan's need (E_2BIG if short)
+                try:
+                    launch("sfft_sample_poly_run" if prepared else "sfft_sample_poly", *scratch)
+                    done = True
+                except _native.NativeError as exc:
+                    if exc.code != _native.E_2BIG:
+                        raise
+                    if prepared:  # operands are ready; only the partial-sum scratch is short
+                        need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
+                        launch("sfft_sample_poly_run", *scratch[:3],
+                               dev.empty((max(need, 1), 2), torch.float64))
+                        done = True
+            if not done:
+                need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
+                launch("sfft_sample_poly", dev.empty((rb, max(s, 1), 2), torch.float64),
+                       dev.empty((L, max(s, 1)), torch.int32), dev.empty((L, max(s, 1)), torch.int32),
+                       dev.empty((max(need, 1), 2), torch.float64))
         else:
             order, start, comps, scale = base.host_spec()
             dev.call("sfft_sample_bspline", len(base.groups), hptr(order), hptr(start), hptr(comps),
