@@ -427,7 +427,8 @@ def run_ours(args):
         "stages_ms": stages,
         "kernels_ms": kernels,
         "kernel_share_of_step": kernels["sample_poly"] / ms_step,
-        "roofline": {"bound": "fp64", "kernel": "sample_poly_ws_kernel (K1, GEMM-factored, FP64 tensor-core DMMA)",
+        "roofline": {"bound": "fp64", "kernel": "K1: poly_bpanel_kernel + sample_poly_tcp_kernel (GEMM-factored sampling, "
+                                                "FP64 tensor-core DMMA; both timed together)",
                      "timing": "CUDA events recorded by the library around the kernel launch on its stream "
                                f"during the timed steps (sfft_profile_*), mean of {nprof} launches",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
