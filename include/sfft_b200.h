@@ -114,13 +114,18 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
  * sfft_sample_poly). */
 int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
                              const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
-                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, void* stream);
+                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                             double* d_scratch, int64_t scratch_len, int* h_panels_built, void* stream);
+/* d_tw / d_scratch (nullable): also build the B panels of the tensor-core
+ * kernel (they depend on the lattices only) at the start of the scratch when
+ * it is large enough; *h_panels_built (nullable) reports whether they were
+ * queued, and sfft_sample_poly_run(panels_ready = 1) then skips them. */
 int sfft_sample_poly_run(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
                          const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
                          double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
                          const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
                          double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
-                         void* stream);
+                         int panels_ready, void* stream);
 /* B-spline oracle (testbed.py:198-244): ngroups tensor-product terms; group g
  * has spline order h_order[g] (<= 8), scale h_scale[g] = C_m * m, and the
  * component slots h_comps[h_start[g] .. h_start[g+1]). */

@@ -35,8 +35,9 @@ _SIGS = {
     "sfft_sample_poly": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int,
                                 _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _vp]),
     "sfft_sample_poly_run": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int,
-                                _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _vp]),
-    "sfft_sample_poly_prepare": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int, _vp, _vp, _vp, _vp]),
+                                _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _int, _vp]),
+    "sfft_sample_poly_prepare": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int, _vp, _vp, _vp,
+                                        _vp, _vp, _i64, _vp, _vp]),
     "sfft_sample_bspline": (_int, [_int, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp, _int, _vp, _int,
                                    _vp, _vp, _i64, _int, _vp, _int, _vp]),
     "sfft_finish_samples": (_int, [_vp, _int, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _int, _vp]),

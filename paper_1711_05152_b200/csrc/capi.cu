@@ -328,16 +328,16 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
   const int64_t partials = best_ks > 1 ? (int64_t)best_ks * pp->nunits * mmax : 0;
   *need = partials;
   if (pp->kind == 2) {
-    pp->nchunk_max = (best_kper + 15) / 16;
+    pp->nchunk_total = (s + 15) / 16;
     int64_t blocks = 0;
     for (int l = 0; l < L; ++l) {
       pp->panel_off[l] = (int)blocks;
-      blocks += (int64_t)best_ks * pp->nt2[l] * pp->nchunk_max;
+      blocks += (int64_t)pp->nt2[l] * pp->nchunk_total;
     }
     if (blocks > 0x7fffffffLL / 2048) return E_2BIG;
     pp->npanels = (int)blocks;
-    pp->panel_base = ((partials + 2047) / 2048) * 2048;  // 32 KB aligned (complex elements)
-    *need = pp->panel_base + blocks * 2048;
+    pp->partial_base = blocks * 2048;  // panels first (32 KB each), partial sums after
+    *need = pp->partial_base + partials;
   }
   return 0;
 }
@@ -462,7 +462,7 @@ static int sample_poly_impl(const int32_t* d_hfreqs, const double* d_hcoef, int 
                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
                             const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
                             double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
-                            void* stream, bool do_prepare, bool do_run) {
+                            void* stream, bool do_prepare, bool do_run, bool panels_ready = false) {
   if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX || rb < 1) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
@@ -490,7 +490,7 @@ static int sample_poly_impl(const int32_t* d_hfreqs, const double* d_hcoef, int 
   if (!rc && do_run)
     rc = launch_sample_poly(*pp, lt, ut, (const double2*)d_cprime, d_rres, d_rj,
                             (const double2*)d_tw, (const double2*)d_chirp, (double2*)d_buf, P,
-                            apply_chirp != 0, (double2*)d_partial, mmax, num_sms_current(), st);
+                            apply_chirp != 0, (double2*)d_partial, mmax, num_sms_current(), st, panels_ready);
   delete pp;
   return rc;
 }
@@ -508,7 +508,9 @@ int sfft_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int 
 
 int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t1,
                              const int64_t* h_m, const int32_t* h_z, int L, const double* h_anchor, int rb,
-                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, void* stream) {
+                             double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
+                             double* d_scratch, int64_t scratch_len, int* h_panels_built, void* stream) {
+  if (h_panels_built) *h_panels_built = 0;
   if (s < 0 || d < 1 || t1 < 1 || t1 > d || d > SFFT_DMAX || rb < 1) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, L, t1);
@@ -524,10 +526,16 @@ int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int
   for (int i = 0; i < rb * tail; ++i) at.a[i] = h_anchor[i];
   PolyPlan* pp = new PolyPlan;
   int64_t need = 0;
-  rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), -1, &need);  // J1 per lattice
+  rc = build_poly_plan(pp, h_m, L, ut, rb, s, num_sms_current(), -1, &need);  // J1, panel layout
   if (!rc)
     rc = launch_poly_prepare(d_hfreqs, (const double2*)d_hcoef, s, d, lt, *pp, at, (double2*)d_cprime, d_rres,
                              d_rj, S(stream));
+  // B panels of all L lattices (the K-split-independent region at the start of
+  // the scratch) when a scratch and the lattice twiddles are given
+  if (!rc && d_scratch && d_tw && pp->kind == 2 && (int64_t)pp->npanels * 2048 <= scratch_len) {
+    rc = launch_bpanels(*pp, lt, d_rj, (const double2*)d_tw, d_scratch, S(stream));
+    if (!rc && h_panels_built) *h_panels_built = 1;
+  }
   delete pp;
   return rc;
 }
@@ -537,10 +545,10 @@ int sfft_sample_poly_run(const int32_t* d_hfreqs, const double* d_hcoef, int s, 
                          double* d_cprime, int32_t* d_rres, int32_t* d_rj, const double* d_tw,
                          const double* d_chirp, double* d_buf, int64_t P, int apply_chirp,
                          double* d_partial, int64_t partial_len, const int32_t* h_units, int nunits,
-                         void* stream) {
+                         int panels_ready, void* stream) {
   return sample_poly_impl(d_hfreqs, d_hcoef, s, d, t1, h_m, h_z, L, h_anchor, rb, d_cprime, d_rres, d_rj, d_tw,
                           d_chirp, d_buf, P, apply_chirp, d_partial, partial_len, h_units, nunits, stream, false,
-                          true);
+                          true, panels_ready != 0);
 }
 
 int64_t sfft_sample_poly_scratch(const int64_t* h_m, int L, int rb, int s, const int32_t* h_units,

@@ -456,16 +456,17 @@ size_t sample_poly_smem(int bl, int64_t mmax) {
 int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& ut,
                        const double2* cprime, const int32_t* rres, const int32_t* rj,
                        const double2* tw, const double2* chirp, double2* buf, int64_t ustride,
-                       bool apply_chirp, double2* part, int64_t pstride, int num_sms,
-                       cudaStream_t st) {
+                       bool apply_chirp, double2* scratch, int64_t pstride, int num_sms,
+                       cudaStream_t st, bool panels_ready) {
   const int ctas = pp.tile_start[pp.nunits];
   if (ctas <= 0) return 0;
   int64_t mmax = 1;
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
   const size_t smem = sample_poly_smem(pp.bl, mmax);
+  double2* part = scratch + pp.partial_base;  // [B panels | partial sums]
   if (pp.kind >= 1) {
     int rc = launch_sample_poly_ws(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride, apply_chirp,
-                                   part, pstride, st);
+                                   part, pstride, (double*)scratch, panels_ready, st);
     if (rc) return rc;
     if (pp.ks > 1) {
       int bx = (int)((mmax + 255) / 256);

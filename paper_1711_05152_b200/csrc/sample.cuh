@@ -25,14 +25,15 @@ struct PolyPlan {
   int nt1[SFFT_LMAX];
   uint64_t mu[SFFT_LMAX];         // Barrett constants floor((2^64-1) / M_l)
   // kind 2: B operand panels (16 terms x 128 columns, 32 KB in MMA fragment
-  // order) precomputed once per (lattice, slice, column tile, chunk) in the
-  // sampling scratch at complex offset panel_base; block index
-  // panel_off[l] + (q * nt2[l] + tj2) * nchunk_max + c
+  // order) precomputed once per (lattice, column tile, 16-term chunk) at the
+  // start of the sampling scratch: block panel_off[l] + tj2 * nchunk_total +
+  // h / 16.  Independent of the K split and of the early-exit L (a prefix of
+  // the L_max panels is the L panels).  Partial sums follow at partial_base.
   int nt2[SFFT_LMAX];
   int panel_off[SFFT_LMAX];
-  int nchunk_max;
+  int nchunk_total;
   int npanels;
-  long long panel_base;
+  long long partial_base;
 };
 
 // B-spline test function: groups of (order, component slots)
@@ -51,14 +52,17 @@ int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, co
 int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& ut,
                        const double2* cprime, const int32_t* rres, const int32_t* rj,
                        const double2* tw, const double2* chirp, double2* buf, int64_t ustride,
-                       bool apply_chirp, double2* part, int64_t pstride, int num_sms,
-                       cudaStream_t st);
+                       bool apply_chirp, double2* scratch, int64_t pstride, int num_sms,
+                       cudaStream_t st, bool panels_ready = false);
 size_t sample_poly_smem(int bl, int64_t mmax);
 size_t sample_poly_ws_smem(int bl, int64_t mmax);
+int launch_bpanels(const PolyPlan& pp, const LatTable& lt, const int32_t* rj, const double2* tw, double* panels,
+                   cudaStream_t st);
 int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
                           const int32_t* rres, const int32_t* rj, const double2* tw,
                           const double2* chirp, double2* buf, int64_t ustride, bool apply_chirp,
-                          double2* part, int64_t pstride, cudaStream_t st);
+                          double2* part, int64_t pstride, double* panels, bool panels_ready,
+                          cudaStream_t st);
 int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
                           const AnchorTable& at, const double2* chirp, double2* buf,
                           int64_t ustride, bool fast, bool apply_chirp, int num_sms,

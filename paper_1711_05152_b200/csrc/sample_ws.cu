@@ -406,10 +406,8 @@ __global__ void __launch_bounds__(128) poly_bpanel_kernel(PolyPlan pp, LatTable 
   int l = 0;
   while (l + 1 < lt.nlat && pp.panel_off[l + 1] <= b) ++l;
   const int idx = b - pp.panel_off[l];
-  const int c = idx % pp.nchunk_max;
-  const int rest = idx / pp.nchunk_max;
-  const int tj2 = rest % pp.nt2[l];
-  const int q = rest / pp.nt2[l];
+  const int ca = idx % pp.nchunk_total;  // absolute 16-term chunk
+  const int tj2 = idx / pp.nchunk_total;
   const int64_t M = lt.m[l];
   const uint32_t M32 = (uint32_t)M;
   const uint64_t mu = pp.mu[l];
@@ -420,8 +418,8 @@ __global__ void __launch_bounds__(128) poly_bpanel_kernel(PolyPlan pp, LatTable 
   const int kk = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hl = kk * 4 + (lane & 3);
   const int col = lane >> 2;  // j2 = 8 bj + col
-  const int h = q * pp.kper + c * KC + hl;
-  const bool live = h < min(pp.s, (q + 1) * pp.kper);
+  const int h = ca * KC + hl;
+  const bool live = h < pp.s;
   double* bre = panels + (int64_t)b * (2 * KC * TJ2);
   double* bim = bre + KC * TJ2;
   double2 v = make_double2(1.0, 0.0), e = make_double2(1.0, 0.0);
@@ -430,11 +428,16 @@ __global__ void __launch_bounds__(128) poly_bpanel_kernel(PolyPlan pp, LatTable 
     v = __ldg(&twl[ws_barrett((uint64_t)rq * (uint32_t)(tj2 * TJ2 + col), M32, mu)]);
     e = __ldg(&twl[ws_barrett((uint64_t)rq * 8u, M32, mu)]);
   }
+  // columns j2 >= J2 = ceil(M / J1) only feed outputs n = j1 + J1 j2 >= M,
+  // which are discarded: their panel entries are left unwritten
+  const int64_t J2 = (M + pp.J1[l] - 1) / pp.J1[l];
 #pragma unroll
   for (int bj = 0; bj < TJ2 / 8; ++bj) {
     const int at = (kk * 16 + bj) * 32 + lane;
-    bre[at] = v.x;
-    bim[at] = v.y;
+    if ((int64_t)tj2 * TJ2 + bj * 8 + col < J2) {
+      bre[at] = v.x;
+      bim[at] = v.y;
+    }
     if (bj + 1 < TJ2 / 8) v = cmul(v, e);
   }
 }
@@ -524,8 +527,8 @@ sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpr
         if (pt == 0) {
           // B: the precomputed panel, one bulk copy completing on full[st]
           const int tj2 = (int)(x.j2_0 / TJ2);
-          const double* src = panels + ((int64_t)pp.panel_off[x.l] + ((int64_t)x.q * pp.nt2[x.l] + tj2) *
-                                        pp.nchunk_max + c) * (2 * KC * TJ2);
+          const double* src = panels + ((int64_t)pp.panel_off[x.l] + (int64_t)tj2 * pp.nchunk_total +
+                                        x.h_begin / KC + c) * (2 * KC * TJ2);
           mbar_expect_tx(&mbar[st], 2 * KC * TJ2 * 8);
           bulk_g2s(b_re, src, 2 * KC * TJ2 * 8, &mbar[st]);
         }
@@ -631,10 +634,19 @@ size_t sample_poly_ws_smem(int bl, int64_t mmax) {
   return (size_t)(ws::NS * ws::STAGE + nlo + nhi) * sizeof(double2);
 }
 
+int launch_bpanels(const PolyPlan& pp, const LatTable& lt, const int32_t* rj, const double2* tw, double* panels,
+                   cudaStream_t st) {
+  if (pp.kind != 2 || pp.npanels <= 0) return 0;
+  poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
 int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2* cprime,
                           const int32_t* rres, const int32_t* rj, const double2* tw,
                           const double2* chirp, double2* buf, int64_t ustride, bool apply_chirp,
-                          double2* part, int64_t pstride, cudaStream_t st) {
+                          double2* part, int64_t pstride, double* panels, bool panels_ready,
+                          cudaStream_t st) {
   const int ctas = pp.tile_start[pp.nunits];
   if (ctas <= 0) return 0;
   int64_t mmax = 1;
@@ -652,9 +664,8 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
     cudaError_t e2 = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return (int)e2;
-    double* panels = (double*)(part + pp.panel_base);
     prof_mark(PROF_SAMPLE, true, st);
-    poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
+    if (!panels_ready) poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
     if (pp.ks > 1)
       sample_poly_tcp_kernel<true><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
                                                                apply_chirp ? 1 : 0, part, pstride, panels);
@@ -662,7 +673,7 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
       sample_poly_tcp_kernel<false><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
                                                                 apply_chirp ? 1 : 0, nullptr, 0, panels);
     prof_mark(PROF_SAMPLE, false, st);
-    SFFT_CHECK_LAUNCHES(2);
+    SFFT_CHECK_LAUNCHES(panels_ready ? 1 : 2);
     return 0;
   }
   const void* fn = pp.ks > 1 ? (tc ? (const void*)sample_poly_ws_kernel<true, true>

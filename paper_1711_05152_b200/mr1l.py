@@ -232,8 +232,13 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
         if prepare is not None and attempt == 1:
+            # read the stats back through an event, so the preparation kernels
+            # queued behind the alias kernel run while the host continues
+            wait = dev.download_async(stats)
             prep = prepare(ms, zh)
-        stats_h = dev.download_small(stats)
+            stats_h = wait()
+        else:
+            stats_h = dev.download_small(stats)
         if int(stats_h[1]) == 0:
             return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep)
     return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep)
@@ -387,7 +392,7 @@ def _unit_arg(units):
 
 def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
                   tails: list[np.ndarray], buf, step: int, it0: int, units=None, scratch=None,
-                  prepared: bool = False):
+                  prepared: bool = False, panels_ready: bool = False):
     """Fill buffer slot j with the pre-chirped samples of unit units[j]
     (global id i * L + l within this chunk of iterations; all rb * L units in
     order when ``units`` is None).  Noise streams are consumed for every unit
@@ -412,22 +417,26 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
             hf, cf = base.device_terms(dev)
             s = base.s
 
-            def launch(name, cprime, rres, rj, part):
+            def launch(name, cprime, rres, rj, part, panels=False):
+                extra = (1 if panels else 0,) if name == "sfft_sample_poly_run" else ()
                 dev.call(name, dptr(hf), dptr(cf), s, d, t1, hptr(tabs.ms), hptr(tabs.zs), L,
                          hptr(anchor), rb, dptr(cprime), dptr(rres), dptr(rj), dptr(tabs.tw),
                          dptr(tabs.chirp), dptr(buf), P, chirp_now, dptr(part), int(part.shape[0]), up, nu,
-                         ctx=f"sampling, step {step}")
+                         *extra, ctx=f"sampling, step {step}")
 
             done = False
             if scratch is not None:
                 # the library checks the scratch against this plan's need (E_2BIG if short)
                 try:
-                    launch("sfft_sample_poly_run" if prepared else "sfft_sample_poly", *scratch)
+                    if prepared:
+                        launch("sfft_sample_poly_run", *scratch, panels=panels_ready)
+                    else:
+                        launch("sfft_sample_poly", *scratch)
                     done = True
                 except _native.NativeError as exc:
                     if exc.code != _native.E_2BIG:
                         raise
-                    if prepared:  # operands are ready; only the partial-sum scratch is short
+                    if prepared:  # operands are ready; only the scratch is short (panels rebuilt)
                         need = int(_native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, rb, s, up, nu))
                         launch("sfft_sample_poly_run", *scratch[:3],
                                dev.empty((max(need, 1), 2), torch.float64))
@@ -566,6 +575,7 @@ class StepPrep:
     n: int
     poly_ready: bool = False  # c' and residues of all L_max lattices computed (attempt 1's vectors)
     l_max: int = 0
+    panels_ready: bool = False  # tensor-core B panels of all L_max lattices built in poly[3]
 
 
 def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
@@ -596,6 +606,7 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
         if r * L_max * (16 << p_all) <= (1 << 30) else None
     poly = None
     ready = False
+    built = np.zeros(1, dtype=np.int32)
     base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
     if isinstance(base, SparsePolynomialOracle):
         s = max(base.s, 1)
@@ -614,9 +625,10 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
             hf, cf = base.device_terms(dev)
             dev.call("sfft_sample_poly_prepare", dptr(hf), dptr(cf), base.s, d, t1, hptr(ms_all), hptr(zs32),
                      L_max, hptr(anchor), r, dptr(poly[0]), dptr(poly[1]), dptr(poly[2]),
-                     ctx="sampling operands (prepared)")
+                     dptr(tabs.tw) if tabs is not None else 0, dptr(poly[3]), int(poly[3].shape[0]),
+                     hptr(built), ctx="sampling operands (prepared)")
             ready = True
-    return StepPrep(tabs, keep, coef, counts, buf, poly, r, n, ready, L_max)
+    return StepPrep(tabs, keep, coef, counts, buf, poly, r, n, ready, L_max, bool(built[0]))
 
 
 def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list[np.ndarray],
@@ -669,7 +681,8 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
             nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0,
                                    scratch=scratch,
                                    prepared=prep is not None and prep.poly_ready and sch.attempts == 1
-                                   and i0 == 0 and rb == r)
+                                   and i0 == 0 and rb == r,
+                                   panels_ready=prep is not None and prep.panels_ready)
         with tm.span("fft"):
             dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
                      dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")
