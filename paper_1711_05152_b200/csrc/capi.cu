@@ -338,6 +338,10 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
     pp->npanels = (int)blocks;
     pp->partial_base = blocks * 2048;  // panels first (32 KB each), partial sums after
     *need = pp->partial_base + partials;
+    if (best_ks > 1) {  // then the publish flags of the in-kernel reduction
+      pp->flag_base = *need;
+      *need += SFFT_WS_MAX_FLAGS * 4 / 16;
+    }
   }
   return 0;
 }

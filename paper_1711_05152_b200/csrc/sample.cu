@@ -465,10 +465,12 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
   const size_t smem = sample_poly_smem(pp.bl, mmax);
   double2* part = scratch + pp.partial_base;  // [B panels | partial sums]
   if (pp.kind >= 1) {
+    unsigned* flags = pp.flag_base > 0 ? (unsigned*)(scratch + pp.flag_base) : nullptr;
+    bool reduced = false;
     int rc = launch_sample_poly_ws(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride, apply_chirp,
-                                   part, pstride, (double*)scratch, panels_ready, st);
+                                   part, pstride, (double*)scratch, panels_ready, flags, &reduced, st);
     if (rc) return rc;
-    if (pp.ks > 1) {
+    if (pp.ks > 1 && !reduced) {
       int bx = (int)((mmax + 255) / 256);
       const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
       if (bx > cap) bx = cap;

@@ -34,7 +34,10 @@ struct PolyPlan {
   int nchunk_total;
   int npanels;
   long long partial_base;
+  long long flag_base;  // kind 2 with a K split: per-CTA publish flags (SFFT_WS_MAX_FLAGS u32)
 };
+
+#define SFFT_WS_MAX_FLAGS 1024
 
 // B-spline test function: groups of (order, component slots)
 struct BsplineSpec {
@@ -62,7 +65,7 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
                           const int32_t* rres, const int32_t* rj, const double2* tw,
                           const double2* chirp, double2* buf, int64_t ustride, bool apply_chirp,
                           double2* part, int64_t pstride, double* panels, bool panels_ready,
-                          cudaStream_t st);
+                          unsigned* flags, bool* reduced, cudaStream_t st);
 int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const BsplineSpec& bs,
                           const AnchorTable& at, const double2* chirp, double2* buf,
                           int64_t ustride, bool fast, bool apply_chirp, int num_sms,

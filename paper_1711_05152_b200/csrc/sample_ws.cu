@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include "common.cuh"
 #include "plan.cuh"
+#include <atomic>
+
 #include "sample.cuh"
 
 namespace sfft {
@@ -363,7 +365,8 @@ sample_poly_ws_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpri
 // the next item's first stages (reloading the twiddle tables, which only
 // they read, when the lattice changes) while the consumers run the previous
 // item's epilogue; no per-CTA launch, table load or pipeline fill per item.
-// Per item the arithmetic is exactly that of sample_poly_ws_kernel<SPLIT, true>.
+// Per item the terms and phases are those of sample_poly_ws_kernel<SPLIT, true>;
+// the complex products use the 3-multiplication form (see the consumers).
 struct WsItem {
   int u, l, it, q, nchunk, h_begin, h_end;
   uint32_t j1_0, j2_0;
@@ -390,6 +393,37 @@ __device__ __forceinline__ WsItem ws_item(const PolyPlan& pp, int w) {
   x.h_end = min(pp.s, x.h_begin + pp.kper);
   x.nchunk = x.h_end > x.h_begin ? (x.h_end - x.h_begin + KC - 1) / KC : 0;
   return x;
+}
+
+// TMEM (tensor memory, 512 columns x 128 lanes x 32 bit per SM): warp w of a
+// warpgroup reaches lanes 32 (w % 4) .. + 31; .32x32b.x64 moves 64 columns
+// of the thread's own lane.  Used as a register extension for the K-split
+// running sum (this FP64 kernel issues no tcgen05.mma, TMEM is free).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// CTA whose contiguous item range [floor(c I / G), floor((c+1) I / G)) holds item w
+__device__ __forceinline__ int ws_cta_of(int w, int items, int grid) {
+  return (int)((((int64_t)w + 1) * grid - 1) / items);
+}
+__device__ __forceinline__ int ws_range_begin(int c, int items, int grid) {
+  return (int)(((int64_t)c * items) / grid);
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // B operand panels: block b = (lattice l, slice q, column tile tj2, chunk c)
@@ -442,13 +476,47 @@ __global__ void __launch_bounds__(128) poly_bpanel_kernel(PolyPlan pp, LatTable 
   }
 }
 
+// L2 prefetch of what the K-split epilogue of item x will read (the owner's
+// running sum, the partials of later CTAs, the chirp), issued a few chunks
+// before the epilogue so that its loads hit L2
+__device__ __forceinline__ void tcp_prefetch_epilogue(const PolyPlan& pp, const LatTable& lt, const WsItem& x, int w,
+                                                   int w0, int w1, int items, int bi0, int bj0, int lane,
+                                                   const double2* buf, int64_t ustride, const double2* part,
+                                                   int64_t pstride, const double2* chirp, int apply_chirp) {
+  const int tb = w - x.q;
+  if (tb < w0) return;  // not the owner: plain stores only
+  const int qe = min(pp.ks - 1, w1 - 1 - tb);
+  const bool last = x.q == qe;
+  const bool fin = last || x.q == pp.ks - 1;
+  if (!(last && qe < pp.ks - 1) && !(fin && apply_chirp)) return;
+  const int64_t M = lt.m[x.l];
+  const int64_t J1 = pp.J1[x.l];
+  const double2* ch = chirp + lt.off[x.l];
+  for (int i = 0; i < 4; ++i) {
+    const int64_t j1 = x.j1_0 + (bi0 + i) * 8 + (lane >> 2);
+    for (int j = 0; j < 4; ++j)
+      for (int e = 0; e < 2; ++e) {
+        const int64_t n = j1 + J1 * (x.j2_0 + (bj0 + j) * 8 + 2 * (lane & 3) + e);
+        if (n >= M) continue;
+        if (fin && apply_chirp) asm volatile("prefetch.global.L2 [%0];" ::"l"(ch + n));
+        if (last)
+          for (int q2 = qe + 1; q2 < pp.ks; ++q2)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(part + ((int64_t)q2 * pp.nunits + x.u) * pstride + n));
+      }
+  }
+  (void)items;
+  (void)buf;
+  (void)ustride;
+}
+
 template <bool SPLIT>
 __global__ void __launch_bounds__(ws::NT, 1)
 sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cprime,
                        const int32_t* __restrict__ rres, const int32_t* __restrict__ rjs,
                        const double2* __restrict__ tw, const double2* __restrict__ chirp,
                        double2* __restrict__ buf, int64_t ustride, int apply_chirp,
-                       double2* __restrict__ part, int64_t pstride, const double* __restrict__ panels) {
+                       double2* __restrict__ part, int64_t pstride, const double* __restrict__ panels,
+                       unsigned* __restrict__ flags, unsigned epoch) {
   using namespace ws;
   extern __shared__ double2 sm[];
   __shared__ uint64_t mbar[2 * NS];  // full[s] (NPROD arrivals), empty[s] (one per consumer warp)
@@ -554,20 +622,42 @@ sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpr
   }
 
   // ---------------- consumers ----------------
+  // Complex product in the 3-multiplication form: per term chunk
+  //   t1 += Re A Re B,  t2 += Im A Im B,  t3 += (Re A + Im A)(Re B + Im B)
+  // and at the end Re = t1 - t2, Im = (t3 - t1) - t2: three real MMAs per
+  // complex multiply-accumulate instead of four (the FP64 tensor pipe is the
+  // bound).  The plane sums are formed in registers from the staged planes.
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONS));
   const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
   const int bi0 = (wv & 1) * 4;   // 4 row blocks (j1) of 8
   const int bj0 = (wv >> 1) * 4;  // 4 column blocks (j2) of 8
+  // K split reduced in this kernel (SPLIT with publish flags): the running
+  // sum of the owned tile lives in TMEM, 128 columns per consumer thread
+  const bool fused = SPLIT && flags != nullptr;
+  __shared__ uint32_t tmem_slot;
+  if (fused) {
+    if (wv == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_addr(&tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    bar_sync(2, NCONS);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   int gc = 0;
   for (int w = w0; w < w1; ++w) {
     const WsItem x = ws_item(pp, w);
-    double2 cr[4][4], ci[4][4];
+    double2 t1[4][4], t2[4][4], t3[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) cr[i][j] = ci[i][j] = make_double2(0.0, 0.0);
+      for (int j = 0; j < 4; ++j) t1[i][j] = t2[i][j] = t3[i][j] = make_double2(0.0, 0.0);
+    const int pf_at = x.nchunk > 4 ? x.nchunk - 4 : 0;
     for (int c = 0; c < x.nchunk; ++c, ++gc) {
       const int st = gc % NS;
+      if (fused && c == pf_at) tcp_prefetch_epilogue(pp, lt, x, w, w0, w1, items, bi0, bj0, lane, buf, ustride,
+                                                     part, pstride, chirp, apply_chirp);
       mbar_wait(&mbar[st], (gc / NS) & 1);  // stage full
       const double* a_re = (const double*)(sm + st * STAGE);
       const double* a_im = a_re + KC * TJ1;
@@ -575,56 +665,153 @@ sample_poly_tcp_kernel(PolyPlan pp, LatTable lt, const double2* __restrict__ cpr
       const double* b_im = b_re + KC * TJ2;
 #pragma unroll
       for (int kk = 0; kk < KC / 4; ++kk) {
-        double ar[4], ai[4], nai[4], br[4], bm[4];
+        double ar[4], ai[4], as[4], br[4], bm[4], bs[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           ar[i] = a_re[(kk * 8 + bi0 + i) * 32 + lane];
           ai[i] = a_im[(kk * 8 + bi0 + i) * 32 + lane];
-          nai[i] = -ai[i];
+          as[i] = ar[i] + ai[i];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           br[j] = b_re[(kk * 16 + bj0 + j) * 32 + lane];
           bm[j] = b_im[(kk * 16 + bj0 + j) * 32 + lane];
+          bs[j] = br[j] + bm[j];
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_acc(cr[i][j], ar[i], br[j]);
+          for (int j = 0; j < 4; ++j) dmma_acc(t1[i][j], ar[i], br[j]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_acc(ci[i][j], ar[i], bm[j]);
+          for (int j = 0; j < 4; ++j) dmma_acc(t2[i][j], ai[i], bm[j]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_acc(cr[i][j], nai[i], bm[j]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_acc(ci[i][j], ai[i], br[j]);
+          for (int j = 0; j < 4; ++j) dmma_acc(t3[i][j], as[i], bs[j]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&mbar[NS + st]);  // stage empty
     }
-    const int64_t M = lt.m[x.l];
-    const int64_t J1 = pp.J1[x.l];
-    const double2* ch = chirp + lt.off[x.l];
-    double2* ub = SPLIT ? part + ((int64_t)x.q * pp.nunits + x.u) * pstride : buf + (int64_t)x.u * ustride;
+    // K split reduced in place (fused): the slices of a tile are consecutive
+    // items, so the CTA holding slice 0 ("owner") carries the running sum
+    // p_0 + p_1 + ... in TMEM from slice to slice, adds the partials of the
+    // slices that fell into the next CTAs' ranges (published with a release
+    // flag) and writes the chirped total.  The summation order
+    // ((p_0 + p_1) + p_2) + ... is that of poly_split_reduce_kernel, so the
+    // result is bit-identical to the partials + reduce path (flags == null).
+    const int tb = w - x.q;                          // item of the tile's slice 0
+    const bool owns = !SPLIT || (fused && tb >= w0);
+    const int qe = min(pp.ks - 1, w1 - 1 - tb);      // last slice of the tile in this CTA
+    const bool last = !SPLIT || x.q == qe;
+    const bool pulls = SPLIT && owns && last && qe < pp.ks - 1;
+    if (pulls) {
+      const int clast = ws_cta_of(tb + pp.ks - 1, items, gridDim.x);
+      for (int c2 = blockIdx.x + 1; c2 <= clast; ++c2) {
+        if (ws_range_begin(c2, items, gridDim.x) == ws_range_begin(c2 + 1, items, gridDim.x)) continue;
+        while (ld_acquire_u32(&flags[c2]) != epoch) __nanosleep(64);
+      }
+    }
+    // this thread's TMEM columns (re-read here: no register held across the loop)
+    const uint32_t taddr = fused ? *(volatile uint32_t*)&tmem_slot + ((uint32_t)(32 * (wv & 3)) << 16) +
+                                       (uint32_t)((wv >> 2) * 128)
+                                 : 0u;
+    // this slice's values (t1..t3 die here): index k = (i * 4 + j) * 2 + e
+    double vr[32], vi[32];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t j1 = x.j1_0 + (bi0 + i) * 8 + (lane >> 2);
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t j2 = x.j2_0 + (bj0 + j) * 8 + 2 * (lane & 3);
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int64_t n = j1 + J1 * (j2 + e);
-          const double2 v = make_double2(e ? cr[i][j].y : cr[i][j].x, e ? ci[i][j].y : ci[i][j].x);
-          if (n < M) ub[n] = (!SPLIT && apply_chirp) ? cmul(v, __ldg(&ch[n])) : v;
+          const double p1 = e ? t1[i][j].y : t1[i][j].x;
+          const double p2 = e ? t2[i][j].y : t2[i][j].x;
+          const double p3 = e ? t3[i][j].y : t3[i][j].x;
+          vr[(i * 4 + j) * 2 + e] = p1 - p2;
+          vi[(i * 4 + j) * 2 + e] = (p3 - p1) - p2;
+        }
+    if (SPLIT && owns && x.q > 0) {
+      // S_q = S_{q-1} + p_q, S_{q-1} from TMEM in 4 pieces of 16 values
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        uint32_t r[16];
+        tmem_ld16(taddr + h * 16, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double pv = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+          if (h < 4) vr[h * 8 + k] = pv + vr[h * 8 + k];
+          else vi[(h - 4) * 8 + k] = pv + vi[(h - 4) * 8 + k];
         }
       }
     }
+    const int64_t M = lt.m[x.l];
+    const int64_t J1 = pp.J1[x.l];
+    const double2* ch = chirp + lt.off[x.l];
+    double2* bu = buf + (int64_t)x.u * ustride;
+    if (pulls) {
+      for (int q2 = qe + 1; q2 < pp.ks; ++q2) {
+        const double2* src = part + ((int64_t)q2 * pp.nunits + x.u) * pstride;
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 8) {  // 8 loads in flight (registers)
+          double2 pv[8];
+#pragma unroll
+          for (int k = k0; k < k0 + 8; ++k) {
+            const int i = k >> 3, j = (k >> 1) & 3, e = k & 1;
+            const int64_t n =
+                x.j1_0 + (bi0 + i) * 8 + (lane >> 2) + J1 * (x.j2_0 + (bj0 + j) * 8 + 2 * (lane & 3) + e);
+            pv[k - k0] = n < M ? __ldcg(&src[n]) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int k = k0; k < k0 + 8; ++k) {
+            vr[k] = vr[k] + pv[k - k0].x;
+            vi[k] = vi[k] + pv[k - k0].y;
+          }
+        }
+      }
+    }
+    const bool final_out = owns && (last || x.q == pp.ks - 1);
+    if (SPLIT && owns && !final_out) {
+      // running sum to TMEM: columns [0, 64) real parts, [64, 128) imaginary
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        uint32_t r[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double v = h < 4 ? vr[h * 8 + k] : vi[(h - 4) * 8 + k];
+          r[2 * k] = (uint32_t)__double2loint(v);
+          r[2 * k + 1] = (uint32_t)__double2hiint(v);
+        }
+        tmem_st16(taddr + h * 16, r);
+      }
+      tmem_wait_st();
+    } else {
+      double2* dst = owns ? bu : part + ((int64_t)x.q * pp.nunits + x.u) * pstride;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int i = k >> 3, j = (k >> 1) & 3, e = k & 1;
+        const int64_t n = x.j1_0 + (bi0 + i) * 8 + (lane >> 2) + J1 * (x.j2_0 + (bj0 + j) * 8 + 2 * (lane & 3) + e);
+        if (n < M) {
+          const double2 v = make_double2(vr[k], vi[k]);
+          dst[n] = (final_out && apply_chirp) ? cmul(v, __ldg(&ch[n])) : v;
+        }
+      }
+    }
+    if (fused && !owns && last) {
+      // this CTA's slices of the tile it entered mid-way are stored: publish
+      bar_sync(2, NCONS);
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(&flags[blockIdx.x], epoch);
+      }
+    }
+  }
+  if (fused) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    bar_sync(2, NCONS);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (wv == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_slot) : "memory");
   }
 }
 
@@ -646,7 +833,8 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
                           const int32_t* rres, const int32_t* rj, const double2* tw,
                           const double2* chirp, double2* buf, int64_t ustride, bool apply_chirp,
                           double2* part, int64_t pstride, double* panels, bool panels_ready,
-                          cudaStream_t st) {
+                          unsigned* flags, bool* reduced, cudaStream_t st) {
+  *reduced = false;
   const int ctas = pp.tile_start[pp.nunits];
   if (ctas <= 0) return 0;
   int64_t mmax = 1;
@@ -657,10 +845,19 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     const char* e = getenv("SFFT_B200_TC_PERSISTENT");
     return !(e && strcmp(e, "0") == 0);
   }();
+  static const bool fused = [] {
+    const char* e = getenv("SFFT_B200_TC_FUSED_REDUCE");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  if (!fused) flags = nullptr;
   if (tc && persistent && pp.npanels > 0) {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = ctas < nsm ? ctas : nsm;
+    int grid = ctas < nsm ? ctas : nsm;
+    if (grid > SFFT_WS_MAX_FLAGS) grid = SFFT_WS_MAX_FLAGS;
+    // launch-unique flag value: the flags need no reset between launches
+    static std::atomic<unsigned> epochs{0x5f3a0001u};  // odd, step 2: never 0, never repeats soon
+    const unsigned epoch = epochs.fetch_add(2u);
     const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
     cudaError_t e2 = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return (int)e2;
@@ -668,11 +865,14 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     if (!panels_ready) poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
     if (pp.ks > 1)
       sample_poly_tcp_kernel<true><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
-                                                               apply_chirp ? 1 : 0, part, pstride, panels);
+                                                               apply_chirp ? 1 : 0, part, pstride, panels,
+                                                               flags, epoch);
     else
       sample_poly_tcp_kernel<false><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
-                                                                apply_chirp ? 1 : 0, nullptr, 0, panels);
+                                                                apply_chirp ? 1 : 0, nullptr, 0, panels,
+                                                                nullptr, 0u);
     prof_mark(PROF_SAMPLE, false, st);
+    *reduced = pp.ks == 1 || flags != nullptr;
     SFFT_CHECK_LAUNCHES(panels_ready ? 1 : 2);
     return 0;
   }

@@ -91,7 +91,7 @@ def main():
                                              "fp64_pipe_pct": float(fp64) if fp64 else None,
                                              "dmma_pipe_pct": float(dmma) if dmma else None,
                                              "dram_pct": float(dram) if dram else None})
-        summary["full_capture"] = per
+        summary.setdefault("full_capture", {}).update(per)  # merge: one rep per kernel group
         for name, lst in per.items():
             if name.startswith("sample_poly") and "reduce" not in name:
                 summary["sample_poly_dram_bytes"] = lst[0]["dram_bytes"]
