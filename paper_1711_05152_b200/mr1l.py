@@ -677,12 +677,12 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     nodes = 0
     for i0 in range(0, r, rb_max):
         rb = min(rb_max, r - i0)
+        # the prepared operands and B panels belong to the first attempt's vectors
+        prepared = prep is not None and prep.poly_ready and sch.attempts == 1 and i0 == 0 and rb == r
         with tm.span("sample"):
             nodes += _sample_units(dev, oracle, tabs, t1, d, tails[i0:i0 + rb], buf, step, i0,
-                                   scratch=scratch,
-                                   prepared=prep is not None and prep.poly_ready and sch.attempts == 1
-                                   and i0 == 0 and rb == r,
-                                   panels_ready=prep is not None and prep.panels_ready)
+                                   scratch=scratch, prepared=prepared,
+                                   panels_ready=prepared and prep.panels_ready)
         with tm.span("fft"):
             dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
                      dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")

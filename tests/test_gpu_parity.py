@@ -179,6 +179,32 @@ def test_mr1l_step_prepared_and_deferred_cap(P, golden):
         assert len(want) == min(cap, len(want)) and np.array_equal(rows.to_host(dev), want)
 
 
+@pytest.mark.gpu
+def test_prepared_operands_only_for_first_attempt(P, golden):
+    """Operands and tensor-core B panels prepared beside the alias kernel
+    belong to the first attempt's generating vectors: a scheme from a later
+    attempt (construct.py:185-206 retries) must not consume them."""
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, prepare_step, run_step
+    dev = get_device()
+    cand = golden["step_cand"].astype(np.int64)
+    oracle = P.SparsePolynomialOracle(golden["step_hf"], golden["step_hc"])
+    dc = DeviceFreqs.from_host(dev, cand)
+    seed = int(golden["step_seed"][0])
+    b = int(golden["step_b"][0])
+    tails = [np.zeros(0)]
+    first = build_scheme(dev, dc, b, np.random.SeedSequence(seed),
+                         prepare=lambda ms, z: prepare_step(dev, oracle, dc, 1, ms, z, tails=tails, d=10))
+    assert first.prep is not None and first.prep.poly_ready
+    other = build_scheme(dev, dc, b, np.random.SeedSequence(seed + 1))
+    assert not np.array_equal(other.z, first.z)
+    other.attempts = 2  # as if the first attempt had failed
+    ref = run_step(dev, oracle, dc, other, tails, 10, 1e-12, len(cand))
+    got = run_step(dev, oracle, dc, other, tails, 10, 1e-12, len(cand), prep=first.prep)
+    assert np.array_equal(dev.download(got.coef[0]), dev.download(ref.coef[0]))
+    assert np.array_equal(dev.download(got.keep[0]), dev.download(ref.keep[0]))
+
+
 def _check_report(golden, key, rep, exact_coef=True):
     assert np.array_equal(rep.detected.freqs, golden[f"{key}_freqs"]), key
     ref = golden[f"{key}_coef"]
