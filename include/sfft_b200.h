@@ -62,6 +62,15 @@ int sfft_alias_masks(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax,
                      const int64_t* h_m, const int32_t* h_z, int L,
                      uint32_t* d_scratch, int64_t scratch_words,
                      uint64_t* d_masks, int32_t* d_stats, void* stream);
+/* The same for lattices [l0, l1) only (h_m, h_z cover lattices [0, l1);
+ * scratch sized by sfft_alias_scratch_words(h_m, l1)).  l0 > 0 adds their bits
+ * to masks holding lattices [0, l0) from an earlier call, and the stats then
+ * cover all l1 lattices: the per-prime early-exit loop of construct.py:173-181
+ * evaluated a chunk of primes at a time. */
+int sfft_alias_masks_range(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax,
+                           const int64_t* h_m, const int32_t* h_z, int l0, int l1,
+                           uint32_t* d_scratch, int64_t scratch_words,
+                           uint64_t* d_masks, int32_t* d_stats, void* stream);
 
 /* ---- per-lattice tables ----------------------------------------------------
  * tw[off_l + n] = e^{+2 pi i n / M_l}, chirp[off_l + n] = e^{-pi i (n^2 mod 2M_l)/M_l},

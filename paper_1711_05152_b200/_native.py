@@ -26,6 +26,7 @@ _SIGS = {
     "sfft_device_info": (_int, [_vp, _vp, _vp]),
     "sfft_alias_scratch_words": (_i64, [_vp, _int]),
     "sfft_alias_masks": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _i64, _vp, _vp, _vp]),
+    "sfft_alias_masks_range": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _int, _vp, _i64, _vp, _vp, _vp]),
     "sfft_lattice_tables": (_int, [_vp, _int, _vp, _vp, _vp]),
     "sfft_fft_table_len": (_i64, [_int]),
     "sfft_fft_tables": (_int, [_int, _vp, _vp]),

@@ -21,12 +21,14 @@
 
 namespace sfft {
 
+constexpr int AB = 8;  // lattices per group of independent memory operations
+
 // bitmap word offsets: lattice l owns words [bw[l], bw[l+1]) in each bitmap
 __device__ __forceinline__ int64_t bm_words(int64_t m) { return (m + 31) >> 5; }
 
 template <int DM, bool FAST>
 __global__ void __launch_bounds__(256)
-alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int l0,
                   uint32_t* __restrict__ seen1, uint32_t* __restrict__ seen2, int64_t words_total) {
   __shared__ int64_t bw[SFFT_LMAX + 1];
   if (threadIdx.x == 0) {
@@ -41,20 +43,36 @@ alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
     int32_t k[DM];
 #pragma unroll
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
-    for (int l = 0; l < lt.nlat; ++l) {
-      const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
-      const int64_t w = bw[l] + (r >> 5);
-      const uint32_t bit = 1u << (r & 31);
-      const uint32_t old = atomicOr(&seen1[w], bit);
-      if (old & bit) atomicOr(&seen2[w], bit);
+    // groups of AB lattices: the group's first-bitmap atomics are issued back
+    // to back (independent), then the rare second-bitmap ones
+    for (int lb = l0; lb < lt.nlat; lb += AB) {
+      int64_t w[AB];
+      uint32_t bit[AB], old[AB];
+#pragma unroll
+      for (int j = 0; j < AB; ++j) {
+        const int l = lb + j;
+        old[j] = 0;
+        bit[j] = 0;
+        if (l < lt.nlat) {
+          const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
+          w[j] = bw[l] + (r >> 5);
+          bit[j] = 1u << (r & 31);
+          old[j] = atomicOr(&seen1[w[j]], bit[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < AB; ++j)
+        if (old[j] & bit[j]) atomicOr(&seen2[w[j]], bit[j]);
     }
   }
 }
 
-// stats[0] = max_k first-cover index (1-based), stats[1] = #candidates with an empty mask
+// stats[0] = max_k first-cover index (1-based), stats[1] = #candidates with an empty mask.
+// Lattices [l0, nlat): l0 > 0 adds their bits to masks of lattices [0, l0)
+// computed by an earlier launch (the stats then cover all nlat lattices).
 template <int DM, bool FAST>
 __global__ void __launch_bounds__(256)
-alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
+alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int l0,
                   const uint32_t* __restrict__ seen2, uint64_t* __restrict__ masks,
                   int32_t* __restrict__ stats) {
   __shared__ int64_t bw[SFFT_LMAX + 1];
@@ -72,11 +90,24 @@ alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
     int32_t k[DM];
 #pragma unroll
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
-    uint64_t mask = 0;
-    for (int l = 0; l < lt.nlat; ++l) {
-      const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
-      const uint32_t wv = __ldg(&seen2[bw[l] + (r >> 5)]);
-      if (!((wv >> (r & 31)) & 1u)) mask |= (1ull << l);
+    uint64_t mask = l0 > 0 ? masks[i] : 0ull;
+    for (int lb = l0; lb < lt.nlat; lb += AB) {
+      uint32_t wv[AB];
+      int sh[AB];
+#pragma unroll
+      for (int j = 0; j < AB; ++j) {  // the group's loads in flight together
+        const int l = lb + j;
+        wv[j] = ~0u;
+        sh[j] = 0;
+        if (l < lt.nlat) {
+          const int64_t r = SFFT_RES(DM, FAST, k, lt, l);
+          sh[j] = (int)(r & 31);
+          wv[j] = __ldg(&seen2[bw[l] + (r >> 5)]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < AB; ++j)
+        if (!((wv[j] >> sh[j]) & 1u)) mask |= (1ull << (lb + j));
     }
     masks[i] = mask;
     if (mask) first_max = max(first_max, __ffsll((long long)mask));
@@ -106,16 +137,18 @@ int64_t alias_scratch_words(const LatTable& lt) {
 }
 
 template <int DM, bool FAST>
-static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
                            int64_t words, uint64_t* masks, int32_t* stats, int blocks,
                            cudaStream_t st) {
   prof_mark(PROF_ALIAS, true, st);
-  alias_mark_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits, bits + words / 2, words);
-  alias_mask_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, bits + words / 2, masks, stats);
+  alias_mark_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits, bits + words / 2, words);
+  alias_mask_kernel<DM, FAST><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits + words / 2, masks, stats);
   prof_mark(PROF_ALIAS, false, st);
 }
 
-int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+// Lattices [l0, lt.nlat) of the table (l0 > 0: the masks of [0, l0) are in
+// `masks` already); `words` = bitmap scratch of all lt.nlat lattices.
+int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
                  int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
                  cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
@@ -129,8 +162,8 @@ int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* 
   const int d = lt.d;
 #define SFFT_ALIAS_CASE(DMV)                                                                 \
   if (d <= DMV) {                                                                            \
-    if (fast) launch_alias_t<DMV, true>(freqs, n, lt, bits, words, masks, stats, blocks, st); \
-    else launch_alias_t<DMV, false>(freqs, n, lt, bits, words, masks, stats, blocks, st);     \
+    if (fast) launch_alias_t<DMV, true>(freqs, n, lt, l0, bits, words, masks, stats, blocks, st); \
+    else launch_alias_t<DMV, false>(freqs, n, lt, l0, bits, words, masks, stats, blocks, st);     \
     SFFT_CHECK_LAUNCHES(2);                                                                  \
     return 0;                                                                                \
   }

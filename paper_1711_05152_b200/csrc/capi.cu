@@ -405,17 +405,25 @@ int64_t sfft_alias_scratch_words(const int64_t* h_m, int L) {
   return 2 * acc;
 }
 
+int sfft_alias_masks_range(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
+                           const int32_t* h_z, int l0, int l1, uint32_t* d_scratch, int64_t scratch_words,
+                           uint64_t* d_masks, int32_t* d_stats, void* stream) {
+  if (n < 0 || t1 < 1 || l0 < 0 || l1 <= l0) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, l1, t1);
+  if (rc) return rc;
+  const int64_t need = sfft_alias_scratch_words(h_m, l1);
+  if (scratch_words < need) return E_INVAL;
+  return launch_alias(d_freqs, n, lt, l0, d_scratch, need, d_masks, d_stats,
+                      fast_i32(lt, t1, kmax, h_m, l1), num_sms_current(), S(stream));
+}
+
 int sfft_alias_masks(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m,
                      const int32_t* h_z, int L, uint32_t* d_scratch, int64_t scratch_words,
                      uint64_t* d_masks, int32_t* d_stats, void* stream) {
-  if (n < 0 || t1 < 1 || L < 1) return E_INVAL;
-  LatTable lt;
-  int rc = fill_lat(lt, h_m, h_z, L, t1);
-  if (rc) return rc;
-  const int64_t need = sfft_alias_scratch_words(h_m, L);
-  if (scratch_words < need) return E_INVAL;
-  return launch_alias(d_freqs, n, lt, d_scratch, need, d_masks, d_stats,
-                      fast_i32(lt, t1, kmax, h_m, L), num_sms_current(), S(stream));
+  if (L < 1) return E_INVAL;
+  return sfft_alias_masks_range(d_freqs, n, t1, kmax, h_m, h_z, 0, L, d_scratch, scratch_words, d_masks,
+                                d_stats, stream);
 }
 
 int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp, void* stream) {

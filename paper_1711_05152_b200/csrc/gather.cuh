@@ -3,7 +3,7 @@
 
 namespace sfft {
 
-int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, uint32_t* bits,
+int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
                  int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
                  cudaStream_t st);
 int64_t alias_scratch_words(const LatTable& lt);

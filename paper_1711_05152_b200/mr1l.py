@@ -177,6 +177,27 @@ def speculate_scheme(n: int, t1: int, seed_seq: np.random.SeedSequence, b: int,
     return SchemeGuess(primes, z)
 
 
+def first_chunk(n: int, ms, target: float = 0.05) -> int:
+    """Primes of an attempt whose alias masks are evaluated before the first
+    coverage check: the fewest for which the expected number of candidates
+    not yet alias-free on any of them, n * prod_l (1 - (1 - 1/M_l)^(n-1))
+    (residues of distinct frequencies collide with probability 1/M_l for a
+    uniform generating vector), falls below ``target``; all of them when
+    that leaves at most one over.  The reference checks coverage after every
+    prime (construct.py:173-181); evaluating a chunk and then the rest
+    gives the same early-exit L and masks for the used lattices."""
+    ms = [int(m) for m in ms]
+    if n <= 1:
+        return len(ms)
+    log_unc = math.log(n)
+    for L, m in enumerate(ms, start=1):
+        free = math.exp((n - 1) * math.log1p(-1.0 / m)) if m > 1 else 0.0
+        log_unc += math.log1p(-free) if free < 1.0 else -math.inf
+        if log_unc < math.log(target):
+            return L if L < len(ms) - 1 else len(ms)
+    return len(ms)
+
+
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
                  ctx: str = "", lazy_streams: bool = False, prepare=None,
@@ -185,10 +206,12 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
     the reference's sequential draw, SURVEY §7 hard part 1) and evaluates the
-    alias masks of all of them in one pass; the early-exit L is the largest
-    first-cover index over the candidates.  ``prepare(ms, z)``: called once the
-    first attempt's alias kernel is enqueued (host work that overlaps it); its
-    result is returned as ``DeviceScheme.prep``.  ``guess``: the first attempt
+    alias masks of a first chunk of them (``first_chunk``) in one pass, the
+    rest only when that chunk leaves candidates uncovered; the early-exit L
+    is the largest first-cover index over the candidates.  ``prepare(ms, z)``:
+    called with the first chunk's primes once the first attempt's alias
+    kernel is enqueued (host work that overlaps it); its result is returned
+    as ``DeviceScheme.prep``.  ``guess``: the first attempt
     precomputed by ``speculate_scheme`` (used when its primes all exceed the
     spread; requires ``lazy_streams``).
     """
@@ -212,6 +235,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
                                   rows=lambda: cand.to_host(dev))
     ms = np.asarray(primes, dtype=np.int64)
     torch = dev.torch
+    l_hi = first_chunk(n, ms)
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
     scratch = dev.empty((max(words, 1),), torch.int32)
     masks = dev.empty((n,), torch.int64)
@@ -229,15 +253,20 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
             # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
             z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
         zh = np.ascontiguousarray(z.astype(np.int32))
-        dev.call("sfft_alias_masks", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_max,
+        dev.call("sfft_alias_masks_range", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), 0, l_hi,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
         if prepare is not None and attempt == 1:
             # read the stats back through an event, so the preparation kernels
             # queued behind the alias kernel run while the host continues
             wait = dev.download_async(stats)
-            prep = prepare(ms, zh)
+            prep = prepare(ms[:l_hi], zh[:l_hi])
             stats_h = wait()
         else:
+            stats_h = dev.download_small(stats)
+        if int(stats_h[1]) != 0 and l_hi < l_max:
+            # not covered by the first chunk: the remaining primes of the attempt
+            dev.call("sfft_alias_masks_range", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_hi, l_max,
+                     dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
             stats_h = dev.download_small(stats)
         if int(stats_h[1]) == 0:
             return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep)

@@ -62,6 +62,47 @@ def test_alias_masks_bit_exact(P, golden):
         assert np.array_equal(got, golden["res_masks"][l])
 
 
+def test_alias_chunks_equal_one_pass(P):
+    """Masks and stats of lattices [0, l1) then [l1, L) (sfft_alias_masks_range)
+    equal one pass over all L, bit for bit."""
+    from paper_1711_05152_b200.device import dptr, get_device, hptr
+    from paper_1711_05152_b200.mr1l import DeviceFreqs
+    from paper_1711_05152_b200.primes import primes_above
+    from paper_1711_05152_b200 import _native
+    dev = get_device()
+    torch = dev.torch
+    rng = np.random.default_rng(11)
+    rows = np.unique(rng.integers(-32, 33, size=(30000, 10)), axis=0)
+    cand = DeviceFreqs.from_host(dev, rows)
+    n = len(rows)
+    ms = np.asarray(primes_above(2 * (n - 1), 22), dtype=np.int64)
+    zh = np.ascontiguousarray(rng.integers(0, ms[:, None], size=(22, 10)).astype(np.int32))
+    words = int(_native.query("sfft_alias_scratch_words", hptr(ms), 22))
+    scratch = dev.empty((words,), torch.int32)
+    out = []
+    for chunks in ([(0, 22)], [(0, 7), (7, 22)], [(0, 1), (1, 2), (2, 21), (21, 22)]):
+        masks = dev.empty((n,), torch.int64)
+        stats = dev.empty((2,), torch.int32)
+        for l0, l1 in chunks:
+            dev.call("sfft_alias_masks_range", dptr(cand.data), n, 10, cand.kmax, hptr(ms), hptr(zh), l0, l1,
+                     dptr(scratch), words, dptr(masks), dptr(stats))
+        out.append((dev.download(masks), dev.download(stats)))
+    for m, st in out[1:]:
+        assert np.array_equal(m, out[0][0])
+        assert np.array_equal(st, out[0][1])
+    from oracle import sfft_oracle as O
+    for l in (0, 7, 21):
+        ref = O.alias_free_mask(rows, zh[l].astype(np.int64), int(ms[l]))
+        assert np.array_equal(((out[0][0].view(np.uint64) >> np.uint64(l)) & np.uint64(1)).astype(bool), ref)
+
+
+def test_scheme_with_small_first_chunk(P, golden, monkeypatch):
+    """A first chunk that cannot cover forces the second alias pass: same scheme."""
+    from paper_1711_05152_b200 import mr1l
+    monkeypatch.setattr(mr1l, "first_chunk", lambda n, ms, target=0.05: 2)
+    test_scheme_bit_exact(P, golden)
+
+
 @pytest.mark.parametrize("K", [1, 2, 3, 5, 7, 33, 65, 97, 129, 1009, 6007])
 def test_dft_1d_known_answers(P, golden, K):
     v = golden[f"dft_in_{K}"]

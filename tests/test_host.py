@@ -184,6 +184,27 @@ class TestWorkloadsAndRng:
         want = np.stack([r.integers(0, m, size=6, dtype=np.int64) for m in g.primes])
         assert np.array_equal(g.z, want)
 
+    def test_first_alias_chunk(self):
+        # the first chunk of primes whose alias masks are evaluated before the
+        # coverage check: a prefix, monotone in n, all primes when nearly all
+        # would be needed; the early exit it predicts matches the oracle's
+        # typical L on a config-1-shaped set
+        from paper_1711_05152_b200.mr1l import first_chunk
+        prev = 0
+        for n in (2, 50, 1000, 20000, 100000, 650000):
+            lm = O.max_lattices(n)
+            ms = O.candidate_primes(np.zeros((1, 1), dtype=np.int64), 2 * (n - 1), lm)
+            k = first_chunk(n, ms)
+            assert 1 <= k <= lm and k != lm - 1
+            assert k >= prev
+            prev = k
+        assert first_chunk(1, [3, 5, 7]) == 3
+        rng = np.random.default_rng(5)
+        cand = O.unique_rows(rng.integers(-32, 33, size=(20000, 10)))
+        sch = O.build_with_retries(cand, 10, np.random.SeedSequence(9))
+        assert len(sch.ms) <= first_chunk(len(cand), O.candidate_primes(cand, 2 * (len(cand) - 1),
+                                                                           O.max_lattices(len(cand))))
+
     def test_spawn_is_stateful(self):
         ss = np.random.SeedSequence(1)
         a = ss.spawn(2)
