@@ -255,7 +255,7 @@ def run_ours(args):
     from paper_1711_05152_b200 import _native, workloads
     from paper_1711_05152_b200.api import reconstruct_step
     from paper_1711_05152_b200.device import get_device
-    from paper_1711_05152_b200.mr1l import DeviceFreqs, StageTimer, build_scheme, prepare_step, run_step
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, StageTimer, build_scheme, fft_size, prepare_step, run_step
 
     dev = get_device(local if world > 1 else None)
     wl = workloads.config1(seed=rank, n=args.n)
@@ -431,7 +431,7 @@ def run_ours(args):
         "config": {"workload": "config1: one MR1L reconstruction step, |J|=100000 in [-32,32]^10, "
                                "2000-term sparse polynomial oracle, b=10, delta=1e-12",
                    "lattices": len(sch.primes[: sch.L]), "nodes_per_step": sch.total_size,
-                   "fft_points": 1 << int(np.ceil(np.log2(2 * max(sch.primes[: sch.L]) - 1))),
+                   "fft_points": fft_size(max(sch.primes[: sch.L])),
                    "l2": "flushed (256 MB write) before every timed step; each step timed from after its flush "
                          f"(loop incl. flushes: {ms_with_flush / args.steps:.4f} ms/step)",
                    "parallelism": f"{world} independent step streams (weak scaling)" if world > 1 else "1 GPU"},

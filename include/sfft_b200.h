@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SFFT_B200_ABI_VERSION 1
+#define SFFT_B200_ABI_VERSION 2
 
 int sfft_abi_version(void);
 /* kernels launched by this library since load (all devices, all streams) */
@@ -78,16 +78,22 @@ int sfft_alias_masks_range(const int32_t* d_freqs, int64_t n, int t1, int64_t km
 int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp, void* stream);
 
 /* ---- K2: Bluestein prime-length DFT (transform.py:50-64, scipy.fft.fft) -----
- * P = 2^p >= 2 * max M_l - 1, 4 <= p <= 24.  sfft_fft_tables fills the FFT
- * twiddle tables (sfft_fft_table_len(p) complex values); sfft_bluestein_bhat
- * builds the transformed Bluestein kernel of each lattice (L * P complex);
- * sfft_bluestein transforms `nunits` pre-chirped buffers in place and leaves
- * the unnormalised DFT X_k (k < M of the unit's lattice) in d_buf. */
-int64_t sfft_fft_table_len(int p);
-int sfft_fft_tables(int p, double* d_ftab, void* stream);
-int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
+ * Cyclic convolution length P >= 2 * max M_l - 1: sfft_fft_size(max M_l)
+ * returns the library's choice (a power of two up to 2048; above that
+ * P = f * 2^a * 2048 with f in {1, 3, 5, 7, 9, 25}, within 1.33x of
+ * 2 M - 1; powers of two 2^23, 2^24 for the largest sizes; -1 above 2^24;
+ * SFFT_B200_FFT_POW2=1 restricts it to powers of two).  sfft_fft_tables
+ * fills the FFT twiddle tables (sfft_fft_table_len(P) complex values, -1 for
+ * an unsupported P); sfft_bluestein_bhat builds the transformed Bluestein
+ * kernel of each lattice (L * P complex); sfft_bluestein transforms `nunits`
+ * pre-chirped buffers in place and leaves the unnormalised DFT X_k (k < M of
+ * the unit's lattice) in d_buf. */
+int64_t sfft_fft_size(int64_t m_max);
+int64_t sfft_fft_table_len(int64_t P);
+int sfft_fft_tables(int64_t P, double* d_ftab, void* stream);
+int sfft_bluestein_bhat(const int64_t* h_m, int L, int64_t P, const double* d_ftab,
                         const double* d_chirp, double* d_bhat, void* stream);
-int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
+int sfft_bluestein(const int64_t* h_m, int L, int rb, int64_t P, const double* d_ftab,
                    const double* d_bhat, const double* d_chirp, double* d_buf,
                    const int32_t* h_units, int nunits, void* stream);
 

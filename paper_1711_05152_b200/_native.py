@@ -28,10 +28,11 @@ _SIGS = {
     "sfft_alias_masks": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _i64, _vp, _vp, _vp]),
     "sfft_alias_masks_range": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _int, _vp, _i64, _vp, _vp, _vp]),
     "sfft_lattice_tables": (_int, [_vp, _int, _vp, _vp, _vp]),
-    "sfft_fft_table_len": (_i64, [_int]),
-    "sfft_fft_tables": (_int, [_int, _vp, _vp]),
-    "sfft_bluestein_bhat": (_int, [_vp, _int, _int, _vp, _vp, _vp, _vp]),
-    "sfft_bluestein": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp]),
+    "sfft_fft_size": (_i64, [_i64]),
+    "sfft_fft_table_len": (_i64, [_i64]),
+    "sfft_fft_tables": (_int, [_i64, _vp, _vp]),
+    "sfft_bluestein_bhat": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp]),
+    "sfft_bluestein": (_int, [_vp, _int, _int, _i64, _vp, _vp, _vp, _vp, _vp, _int, _vp]),
     "sfft_sample_poly_scratch": (_i64, [_vp, _int, _int, _int, _vp, _int]),
     "sfft_sample_poly": (_int, [_vp, _vp, _int, _int, _int, _vp, _vp, _int, _vp, _int,
                                 _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _vp]),

@@ -246,7 +246,7 @@ def dft_1d(values, direction: str = "forward") -> np.ndarray:
         dev.call("sfft_cscale", dptr(buf), K, 1.0, 1, ctx="dft_1d conj")
     dev.call("sfft_finish_samples", hptr(tabs.ms), 1, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="dft_1d pre-chirp")
-    dev.call("sfft_bluestein", hptr(tabs.ms), 1, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+    dev.call("sfft_bluestein", hptr(tabs.ms), 1, 1, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
              dptr(tabs.chirp), dptr(buf), 0, 0, ctx="dft_1d")
     if inv:
         dev.call("sfft_cscale", dptr(buf), K, 1.0 / K, 1, ctx="dft_1d scale")
@@ -285,7 +285,7 @@ def invert_multiple(samples: Sequence[LatticeSamples], ml: MultipleRank1Lattice)
         buf[:, : host.shape[1]].copy_(torch.from_numpy(host))
     dev.call("sfft_finish_samples", hptr(ms), L, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="invert_multiple pre-chirp")
-    dev.call("sfft_bluestein", hptr(ms), L, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
+    dev.call("sfft_bluestein", hptr(ms), L, 1, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
              dptr(buf), 0, 0, ctx="invert_multiple FFT")
     cand = DeviceFreqs.from_host(dev, target.freqs)
     d_masks = dev.upload(words.view(np.int64))

@@ -16,7 +16,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libsfft_b200.so"
-SOURCES = ["capi.cu", "alias.cu", "sample.cu", "sample_ws.cu", "fft.cu", "gather.cu", "lines.cu", "points.cu",
+SOURCES = ["capi.cu", "alias.cu", "sample.cu", "sample_ws.cu", "fft.cu", "fft_mixed.cu", "gather.cu", "lines.cu", "points.cu",
            "cbc.cu", "peak.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

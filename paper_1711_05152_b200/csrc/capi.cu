@@ -434,38 +434,54 @@ int sfft_lattice_tables(const int64_t* h_m, int L, double* d_tw, double* d_chirp
   return launch_lattice_tables(lt, (double2*)d_tw, (double2*)d_chirp, S(stream));
 }
 
-int64_t sfft_fft_table_len(int p) {
-  if (p < 4 || p > 24) return -1;
-  return fft_geom(p).table_len;
+static bool fft_pow2_only() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_B200_FFT_POW2");
+    return e && strcmp(e, "1") == 0;
+  }();
+  return v;
 }
 
-int sfft_fft_tables(int p, double* d_ftab, void* stream) {
-  if (p < 4 || p > 24) return E_INVAL;
-  return launch_fft_tables(p, (double2*)d_ftab, S(stream));
+int64_t sfft_fft_size(int64_t m_max) {
+  if (m_max < 1) return -1;
+  return fft_choose_size(m_max, fft_pow2_only());
 }
 
-int sfft_bluestein_bhat(const int64_t* h_m, int L, int p, const double* d_ftab,
+int64_t sfft_fft_table_len(int64_t P) {
+  const FftGeom g = fft_geom(P);
+  return g.valid ? g.table_len : -1;
+}
+
+int sfft_fft_tables(int64_t P, double* d_ftab, void* stream) {
+  const FftGeom g = fft_geom(P);
+  if (!g.valid) return E_INVAL;
+  return launch_fft_tables(g, (double2*)d_ftab, S(stream));
+}
+
+int sfft_bluestein_bhat(const int64_t* h_m, int L, int64_t P, const double* d_ftab,
                         const double* d_chirp, double* d_bhat, void* stream) {
-  if (p < 4 || p > 24) return E_INVAL;
+  const FftGeom g = fft_geom(P);
+  if (!g.valid) return E_INVAL;
   LatTable lt;
   int rc = fill_lat(lt, h_m, nullptr, L, 0);
   if (rc) return rc;
   for (int l = 0; l < L; ++l)
-    if (2 * h_m[l] - 1 > ((int64_t)1 << p)) return E_INVAL;
-  return launch_bhat(lt, (const double2*)d_chirp, (double2*)d_bhat, p, (const double2*)d_ftab,
+    if (2 * h_m[l] - 1 > P) return E_INVAL;
+  return launch_bhat(lt, (const double2*)d_chirp, (double2*)d_bhat, g, (const double2*)d_ftab,
                      S(stream));
 }
 
-int sfft_bluestein(const int64_t* h_m, int L, int rb, int p, const double* d_ftab,
+int sfft_bluestein(const int64_t* h_m, int L, int rb, int64_t P, const double* d_ftab,
                    const double* d_bhat, const double* d_chirp, double* d_buf,
                    const int32_t* h_units, int nunits, void* stream) {
-  if (p < 4 || p > 24) return E_INVAL;
+  const FftGeom g = fft_geom(P);
+  if (!g.valid) return E_INVAL;
   UnitTable ut;
   int rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   for (int l = 0; l < L; ++l)
-    if (2 * h_m[l] - 1 > ((int64_t)1 << p)) return E_INVAL;
-  return launch_bluestein((double2*)d_buf, ut, p, (const double2*)d_ftab, (const double2*)d_bhat,
+    if (2 * h_m[l] - 1 > P) return E_INVAL;
+  return launch_bluestein((double2*)d_buf, ut, g, (const double2*)d_ftab, (const double2*)d_bhat,
                           (const double2*)d_chirp, S(stream));
 }
 

@@ -47,8 +47,7 @@ __global__ void lattice_tables_kernel(LatTable lt, double2* __restrict__ tw,
 }
 
 // FFT tables for one P: [twP1 | twP2 | Tlo | Thi], all e^{-2 pi i m / N}
-__global__ void fft_tables_kernel(int p, double2* __restrict__ out) {
-  const FftGeom g = fft_geom(p);
+__global__ void fft_tables_kernel(FftGeom g, double2* __restrict__ out) {
   const int64_t total = g.table_len;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -61,13 +60,6 @@ __global__ void fft_tables_kernel(int p, double2* __restrict__ out) {
     sincospi(2.0 * num / den, &s, &c);
     out[i] = make_double2(c, -s);
   }
-}
-
-// e^{-2 pi i m / P} from the two-level table
-__device__ __forceinline__ double2 twP(const FftGeom& g, const double2* __restrict__ tab, int64_t m) {
-  const double2 lo = __ldg(&tab[g.off_lo + (m & (g.nlo - 1))]);
-  const double2 hi = __ldg(&tab[g.off_hi + (m >> g.qlo)]);
-  return cmul(hi, lo);
 }
 
 // Bluestein kernel sequence b: b[m] = e^{+pi i (m^2 mod 2M)/M} for m < M,
@@ -93,14 +85,13 @@ __global__ void bluestein_b_kernel(LatTable lt, const double2* __restrict__ chir
 // twiddle, store transposed.  INV: inverse FFT, post-chirp, store n < M.
 template <int LOG1, bool INV, int TE>
 __global__ void __launch_bounds__(FFT_T, TE == 2048 ? 4 : 2)
-fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int mask_input,
+fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom g, int mask_input,
                const double2* __restrict__ ftab, const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
   constexpr int P1 = 1 << LOG1;
   constexpr int P2 = TE;  // the row length equals the tile size
   constexpr int C = TE / P1;
   constexpr int rstride = Tile<TE>::rstride(P1);
-  const FftGeom g = fft_geom(p);
   const int u = blockIdx.y;
   const int c0 = blockIdx.x * C;
   const int lat = ut.lat[u];
@@ -173,14 +164,13 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 // MODE 1 (fwd only, builds bhat): forward FFT, scale by 1/P.
 template <int LOG2, int MODE, int TE>
 __global__ void __launch_bounds__(FFT_T, TE == 2048 ? 4 : 2)
-fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, int total_rows,
+fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom g, int total_rows,
                const double2* __restrict__ ftab, const double2* __restrict__ bhat,
                const double2* __restrict__ chirp) {
   extern __shared__ double2 s[];
   constexpr int P2 = 1 << LOG2;
   constexpr int rows = TE / P2;
   constexpr int rstride = Tile<TE>::rstride(P2);
-  const FftGeom g = fft_geom(p);
   const int P1 = g.P1;
   const int g0 = blockIdx.x * rows;
   const bool single = (P1 == 1);
@@ -210,7 +200,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
   __syncthreads();
   block_fft<LOG2, false, TE>(s, ftab + g.off_p2);
   if (MODE == 1) {
-    const double scale = 1.0 / (double)g.P;  // exact: P is a power of two
+    const double scale = 1.0 / (double)g.P;  // exact when P is a power of two
 #pragma unroll
     for (int f = threadIdx.x; f < TE; f += FFT_T) {
       const int r = f / P2, i = f % P2;
@@ -281,7 +271,7 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int p, 
 // (the column length P1 = 2^11..2^12 of p = 23, 24 also uses 4096 tiles)
 template <bool INV>
 static int launch_col(int te, int lg, dim3 grid, size_t sm, cudaStream_t st, double2* buf, int64_t us,
-                      const UnitTable& ut, int p, int mask, const double2* ftab, const double2* chirp) {
+                      const UnitTable& ut, const FftGeom& p, int mask, const double2* ftab, const double2* chirp) {
 #define SFFT_COL(TEV, L)                                                                         \
   case L: {                                                                                      \
     cudaError_t e = cudaFuncSetAttribute((const void*)fft_col_kernel<L, INV, TEV>,               \
@@ -310,7 +300,7 @@ static int launch_col(int te, int lg, dim3 grid, size_t sm, cudaStream_t st, dou
 
 template <int MODE>
 static int launch_row(int te, int lg, unsigned blocks, size_t sm, cudaStream_t st, double2* buf, int64_t us,
-                      const UnitTable& ut, int p, int total_rows, const double2* ftab,
+                      const UnitTable& ut, const FftGeom& p, int total_rows, const double2* ftab,
                       const double2* bhat, const double2* chirp) {
 #define SFFT_ROW(TEV, L)                                                                         \
   case L: {                                                                                      \
@@ -344,11 +334,10 @@ static size_t fft_smem_bytes(int te, int rows_len) {
   return (size_t)rows * rs * sizeof(double2);
 }
 
-int launch_fft_tables(int p, double2* out, cudaStream_t st) {
-  const FftGeom g = fft_geom(p);
+int launch_fft_tables(const FftGeom& g, double2* out, cudaStream_t st) {
   int blocks = (int)((g.table_len + 255) / 256);
   if (blocks > 1024) blocks = 1024;
-  fft_tables_kernel<<<blocks, 256, 0, st>>>(p, out);
+  fft_tables_kernel<<<blocks, 256, 0, st>>>(g, out);
   SFFT_CHECK_LAUNCH();
   return 0;
 }
@@ -364,18 +353,18 @@ int launch_lattice_tables(const LatTable& lt, double2* tw, double2* chirp, cudaS
 }
 
 // forward passes on `nunits` buffers (column pass if P1 > 1, then row pass in `mode`)
-static int run_forward_cols(double2* buf, int64_t ustride, const UnitTable& ut, int p, int mask,
-                            const double2* ftab, const double2* chirp, cudaStream_t st) {
-  const FftGeom g = fft_geom(p);
+static int run_cols(bool inv, double2* buf, int64_t ustride, const UnitTable& ut, const FftGeom& g, int mask,
+                    const double2* ftab, const double2* chirp, cudaStream_t st) {
   if (g.P1 == 1) return 0;
+  dim3 grid(g.P2 / fft_col_ctas_cols(g.P1, g.te), ut.nunits);
+  if (g.f1 > 1) return launch_colx(inv, g, grid, st, buf, ustride, ut, mask, ftab, chirp);
   const size_t sm = fft_smem_bytes(g.te, g.P1);
-  dim3 grid(g.P2 / (g.te / g.P1), ut.nunits);
-  return launch_col<false>(g.te, g.p1, grid, sm, st, buf, ustride, ut, p, mask, ftab, chirp);
+  return inv ? launch_col<true>(g.te, g.a1, grid, sm, st, buf, ustride, ut, g, mask, ftab, chirp)
+             : launch_col<false>(g.te, g.a1, grid, sm, st, buf, ustride, ut, g, mask, ftab, chirp);
 }
 
-int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
+int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, const FftGeom& g,
                 const double2* ftab, cudaStream_t st) {
-  const FftGeom g = fft_geom(p);
   const int64_t P = g.P;
   int bx = (int)((P + 255) / 256);
   if (bx > 512) bx = 512;
@@ -385,33 +374,28 @@ int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, int p,
   ut.nunits = lt.nlat;
   ut.nlat = lt.nlat;
   for (int l = 0; l < lt.nlat; ++l) { ut.lat[l] = l; ut.m[l] = lt.m[l]; ut.off[l] = lt.off[l]; }
-  int rc = run_forward_cols(bhat, P, ut, p, 0, ftab, chirp, st);
+  int rc = run_cols(false, bhat, P, ut, g, 0, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
   const int rows = g.te / g.P2;
-  return launch_row<1>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, p, total_rows,
+  return launch_row<1>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, g, total_rows,
                        ftab, nullptr, chirp);
 }
 
-int launch_bluestein(double2* buf, const UnitTable& ut, int p, const double2* ftab,
+int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
                      const double2* bhat, const double2* chirp, cudaStream_t st) {
-  const FftGeom g = fft_geom(p);
   const int64_t P = g.P;
   prof_mark(PROF_FFT, true, st);
-  int rc = run_forward_cols(buf, P, ut, p, 1, ftab, chirp, st);
+  int rc = run_cols(false, buf, P, ut, g, 1, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
   const int rows = g.te / g.P2;
-  rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, p, total_rows, ftab,
+  rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, g, total_rows, ftab,
                      bhat, chirp);
   if (rc) return rc;
-  if (g.P1 > 1) {
-    const size_t smc = fft_smem_bytes(g.te, g.P1);
-    dim3 grid(g.P2 / (g.te / g.P1), ut.nunits);
-    rc = launch_col<true>(g.te, g.p1, grid, smc, st, buf, P, ut, p, 0, ftab, chirp);
-  }
+  rc = run_cols(true, buf, P, ut, g, 0, ftab, chirp, st);
   prof_mark(PROF_FFT, false, st);
   return rc;
 }

@@ -146,15 +146,15 @@ class Device:
         self.stream.synchronize()
 
     # -- cached tables ------------------------------------------------------
-    def fft_tables(self, p: int):
-        tab = self._ftab.get(p)
+    def fft_tables(self, P: int):
+        tab = self._ftab.get(P)
         if tab is None:
-            n = int(_native.query("sfft_fft_table_len", p))
+            n = int(_native.query("sfft_fft_table_len", P))
             if n <= 0:
-                raise ValueError(f"FFT size 2^{p} outside the supported range 2^4..2^24")
+                raise ValueError(f"FFT size {P} is not a supported Bluestein length")
             tab = self.empty((n, 2), self.torch.float64)
-            self.call("sfft_fft_tables", p, dptr(tab), ctx=f"fft tables p={p}")
-            self._ftab[p] = tab
+            self.call("sfft_fft_tables", P, dptr(tab), ctx=f"fft tables P={P}")
+            self._ftab[P] = tab
         return tab
 
 

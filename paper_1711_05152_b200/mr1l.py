@@ -289,39 +289,36 @@ def scheme_to_host(dev: Device, cand_rows: np.ndarray, sch: DeviceScheme) -> Mul
 # ---------------------------------------------------------------------------
 # step execution
 
-def fft_exponent(m_max: int) -> int:
-    p = max(4, int(math.ceil(math.log2(max(2 * m_max - 1, 1)))))
-    while (1 << p) < 2 * m_max - 1:
-        p += 1
-    if p > 24:
-        raise ValueError(f"lattice size {m_max} needs an FFT of 2^{p} > 2^24 points")
-    return p
+def fft_size(m_max: int) -> int:
+    """Bluestein convolution length for lattices of size <= m_max: the
+    library's smallest supported P >= 2 m_max - 1 (powers of two, or
+    f * 2^a * 2048 with f in {3, 5, 7, 9, 25}; plan.cuh fft_geom)."""
+    P = int(_native.query("sfft_fft_size", int(m_max)))
+    if P < 0:
+        raise ValueError(f"lattice size {m_max} needs an FFT of more than 2^24 points")
+    return P
 
 
 @dataclass
 class LatticeTables:
     ms: np.ndarray
     zs: np.ndarray
-    p: int
+    P: int           # Bluestein convolution length (fft_size)
     tw: object
     chirp: object
     bhat: object
     ftab: object
-
-    @property
-    def P(self) -> int:
-        return 1 << self.p
 
     def prefix(self, L: int) -> "LatticeTables | None":
         """Tables of the first L lattices (twiddles/chirps are concatenated in
         lattice order, one Bhat row per lattice: a prefix is a view), or None
         when the first L sizes need a smaller FFT than this set's."""
         ms = self.ms[:L]
-        if fft_exponent(int(ms.max())) != self.p:
+        if fft_size(int(ms.max())) != self.P:
             return None
         tot = int(ms.sum())
         zs = self.zs[:L] if self.zs is not None else None
-        return LatticeTables(ms, zs, self.p, self.tw[:tot], self.chirp[:tot], self.bhat[:L], self.ftab)
+        return LatticeTables(ms, zs, self.P, self.tw[:tot], self.chirp[:tot], self.bhat[:L], self.ftab)
 
 
 class _TableCache:
@@ -368,24 +365,23 @@ def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str 
     torch = dev.torch
     ms = np.ascontiguousarray(np.asarray(ms, dtype=np.int64))
     L = len(ms)
-    p = fft_exponent(int(ms.max()))
-    key = (p,) + tuple(int(m) for m in ms)
+    P = fft_size(int(ms.max()))
+    key = (P,) + tuple(int(m) for m in ms)
     tc = _TABLES.setdefault(dev.index, _TableCache())
     got = tc.get(key) if cache else None
-    ftab = dev.fft_tables(p)
+    ftab = dev.fft_tables(P)
     if got is not None:
         tw, chirp, bhat, _ = got
-        return LatticeTables(ms, zs, p, tw, chirp, bhat, ftab)
-    P = 1 << p
+        return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab)
     tot = int(ms.sum())
     tw = dev.empty((tot, 2), torch.float64)
     chirp = dev.empty((tot, 2), torch.float64)
     dev.call("sfft_lattice_tables", hptr(ms), L, dptr(tw), dptr(chirp), ctx=ctx)
     bhat = dev.empty((L, P, 2), torch.float64)
-    dev.call("sfft_bluestein_bhat", hptr(ms), L, p, dptr(ftab), dptr(chirp), dptr(bhat), ctx=ctx)
+    dev.call("sfft_bluestein_bhat", hptr(ms), L, P, dptr(ftab), dptr(chirp), dptr(bhat), ctx=ctx)
     if cache:
         tc.put(key, (tw, chirp, bhat), 32 * tot + 16 * L * P)
-    return LatticeTables(ms, zs, p, tw, chirp, bhat, ftab)
+    return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab)
 
 
 @dataclass
@@ -620,10 +616,10 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
     if r * L_max > UMAX or r > RBMAX:
         return None
     zs32 = np.ascontiguousarray(np.asarray(zs_all).astype(np.int32))
-    p_all = fft_exponent(int(ms_all.max()))
+    P_all = fft_size(int(ms_all.max()))
     tabs = None
     if not cached_tables_only or \
-            _TABLES.setdefault(dev.index, _TableCache()).get((p_all,) + tuple(int(m) for m in ms_all)) is not None:
+            _TABLES.setdefault(dev.index, _TableCache()).get((P_all,) + tuple(int(m) for m in ms_all)) is not None:
         tabs = lattice_tables(dev, ms_all, zs32, ctx="lattice tables (prepared)")
     n = cand.n
     keep = dev.empty((r, n), torch.uint8)
@@ -631,8 +627,8 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
     counts = dev.zeros((r,), torch.int32)
     # the transform buffer for all L_max lattices only while that is small
     # (the early-exit L is about half of L_max); otherwise run_step allocates
-    buf = dev.empty((r * L_max, 1 << p_all, 2), torch.float64) \
-        if r * L_max * (16 << p_all) <= (1 << 30) else None
+    buf = dev.empty((r * L_max, P_all, 2), torch.float64) \
+        if r * L_max * 16 * P_all <= (1 << 30) else None
     poly = None
     ready = False
     built = np.zeros(1, dtype=np.int32)
@@ -713,7 +709,7 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
                                    scratch=scratch, prepared=prepared,
                                    panels_ready=prepared and prep.panels_ready)
         with tm.span("fft"):
-            dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+            dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
                      dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"Bluestein FFT, step {step}")
         with tm.span("gather"):
             dev.call("sfft_gather_select", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,

@@ -85,7 +85,7 @@ def _local_rows(dev, oracle, cand, sch, tabs, tails_chunk, d, step, i0, world, r
         buf = dev.empty((len(mine), P, 2), torch.float64)
         nodes = _sample_units(dev, oracle, tabs, t1, d, tails_chunk, buf, step, i0, units=mine)
         uarr = np.ascontiguousarray(np.asarray(mine, dtype=np.int32))
-        dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+        dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
                  dptr(tabs.chirp), dptr(buf), hptr(uarr), len(mine), ctx=f"Bluestein FFT, step {step}")
         dev.call("sfft_gather_units", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
                  dptr(sch.masks), dptr(buf), P, rb, hptr(uarr), len(mine), dptr(rows),

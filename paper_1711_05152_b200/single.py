@@ -131,7 +131,7 @@ def invert_single(samples, I: FrequencyIndexSet) -> SparseSpectrum:
         buf[0, : lat.m].copy_(torch.from_numpy(v))
     dev.call("sfft_finish_samples", hptr(ms), 1, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="invert_single pre-chirp")
-    dev.call("sfft_bluestein", hptr(ms), 1, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
+    dev.call("sfft_bluestein", hptr(ms), 1, 1, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
              dptr(buf), 0, 0, ctx="invert_single FFT")
     cand = DeviceFreqs.from_host(dev, I.freqs)
     masks = torch.ones((n,), dtype=torch.int64, device=dev.device)
@@ -165,7 +165,7 @@ def eval_on_lattice(spectrum: SparseSpectrum, lat: Rank1Lattice):
     dev.call("sfft_cscale", dptr(buf), lat.m, 1.0, 1, ctx="eval_on_lattice conj")
     dev.call("sfft_finish_samples", hptr(ms), 1, 1, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
              ctx="eval_on_lattice pre-chirp")
-    dev.call("sfft_bluestein", hptr(ms), 1, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
+    dev.call("sfft_bluestein", hptr(ms), 1, 1, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat), dptr(tabs.chirp),
              dptr(buf), 0, 0, ctx="eval_on_lattice DFT")
     dev.call("sfft_cscale", dptr(buf), lat.m, 1.0, 1, ctx="eval_on_lattice conj")
     out = dev.download(buf[0, : lat.m])

@@ -45,13 +45,29 @@ def test_sm100a_cubin_embedded():
 def test_size_queries_without_gpu(lib):
     from paper_1711_05152_b200 import _native
     import numpy as np
-    assert _native.query("sfft_abi_version") == 1
+    assert _native.query("sfft_abi_version") == 2
     assert _native.query("sfft_fft_table_len", 3) == -1
-    n18 = _native.query("sfft_fft_table_len", 18)
+    n18 = _native.query("sfft_fft_table_len", 1 << 18)
     # [P1 | P2 | 2^9 | 2^9] with P = 2^18 = 2^7 * 2^11 (2048-point tiles up to 2^22)
     assert n18 == 128 + 2048 + 512 + 512
     # P = 2^23 = 2^11 * 2^12 (4096-point tiles), two-level table 2^12 + 2^11
-    assert _native.query("sfft_fft_table_len", 23) == 2048 + 4096 + 4096 + 2048
+    assert _native.query("sfft_fft_table_len", 1 << 23) == 2048 + 4096 + 4096 + 2048
+    # mixed radix: P = 25 * 8 * 2048 = 409600: [200 | 2048 | 2^10 | ceil(P / 2^10)]
+    assert _native.query("sfft_fft_table_len", 409600) == 200 + 2048 + 1024 + 400
+    for bad in (3 * 1024, 11 * 2048, 3 * 4096 * 2048, 1 << 25):  # odd factor / P1 / size unsupported
+        assert _native.query("sfft_fft_table_len", bad) == -1
+    # sizes: smallest supported P >= 2M - 1
+    assert _native.query("sfft_fft_size", 1) == 16
+    assert _native.query("sfft_fft_size", 1009) == 2048
+    assert _native.query("sfft_fft_size", 6007) == 3 * 2 * 2048
+    assert _native.query("sfft_fft_size", 199999) == 25 * 8 * 2048
+    assert _native.query("sfft_fft_size", 1 << 23) == 1 << 24
+    assert _native.query("sfft_fft_size", (1 << 23) + 1) == -1
+    rng = np.random.default_rng(0)
+    for m in rng.integers(1025, 2097152, 300):
+        P = _native.query("sfft_fft_size", int(m))
+        assert 2 * m - 1 <= P <= max(2 * (2 * m - 1), 4096) and _native.query("sfft_fft_table_len", P) > 0
+        assert P <= 1.34 * (2 * m - 1) or P <= 4096 or P & (P - 1) == 0
     ms = np.array([7, 64, 65], dtype=np.int64)
     assert _native.query("sfft_alias_scratch_words", ms.ctypes.data, 3) == 2 * (1 + 2 + 3)
     assert _native.query("sfft_scan_scratch_len", 0) == 1

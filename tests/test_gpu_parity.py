@@ -125,6 +125,30 @@ def test_dft_large_primes_vs_numpy(P):
         assert np.abs(back - v).max() <= 1e-12 * np.abs(v).max()
 
 
+def test_dft_mixed_radix_sizes_vs_numpy(P):
+    """Bluestein lengths P = f * 2^a * 2048 (f = 3, 5, 7, 9, 25; column
+    passes of length 3 .. 1600): forward and inverse DFTs within 1e-12."""
+    from paper_1711_05152_b200 import _native
+    rng = np.random.default_rng(2)
+    seen = set()
+    for f in (3, 5, 7, 9, 25):
+        for a in (0, 1, 3, 5, 6):
+            P1 = f << a
+            if P1 > 2048:
+                continue
+            K = (P1 * 2048 + 1) // 2
+            Pc = int(_native.query("sfft_fft_size", K))
+            odd = Pc // (Pc & -Pc)
+            seen.add(odd)
+            v = rng.normal(size=K) + 1j * rng.normal(size=K)
+            got = P.dft_1d(v)
+            ref = np.fft.fft(v)
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (K, Pc)
+            back = P.dft_1d(got, "inverse")
+            assert np.abs(back - v).max() <= 1e-12 * np.abs(v).max(), (K, Pc)
+    assert {3, 5, 7, 9, 25} <= seen
+
+
 def test_scheme_bit_exact(P, golden):
     cand = golden["step_cand"].astype(np.int64)
     I = P.FrequencyIndexSet(cand, _presorted=True)

@@ -21,3 +21,7 @@ dev.sync()
 pr.disable()
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(30)
+if "--callees" in sys.argv:
+    st.sort_stats("cumulative").print_callees("build_scheme")
+    st.sort_stats("cumulative").print_callees("run_step")
+    st.sort_stats("cumulative").print_callees("sparse_fft")

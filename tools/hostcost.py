@@ -52,5 +52,5 @@ tabs = lattice_tables(dev, sch.m_used, sch.z_used)
 t("lattice_tables (cache hit)", lambda: lattice_tables(dev, sch.m_used, sch.z_used))
 t("sample_poly_scratch query", lambda: _native.query("sfft_sample_poly_scratch", hptr(tabs.ms), L, 1, 2000, 0, 0))
 buf = dev.empty((L, tabs.P, 2), torch.float64)
-t("bluestein", lambda: dev.call("sfft_bluestein", hptr(tabs.ms), L, 1, tabs.p, dptr(tabs.ftab), dptr(tabs.bhat),
+t("bluestein", lambda: dev.call("sfft_bluestein", hptr(tabs.ms), L, 1, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
                                 dptr(tabs.chirp), dptr(buf), 0, 0), k=50)
