@@ -247,9 +247,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional smoke of the multi-rank path on a 1-GPU box only (never a
+    # measurement): every rank on cuda:0, gloo collectives
+    smoke_1gpu = os.environ.get("SFFT_B200_MULTIRANK_SMOKE") == "1"
+    if smoke_1gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if smoke_1gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1711_05152_b200 as P
     import paper_1711_05152_b200.device  # noqa: F401
     from paper_1711_05152_b200 import _native, workloads

@@ -61,14 +61,16 @@ def exchange_rows(local, world: int, group=None):
     import torch.distributed as dist
     if world == 1:
         return local
-    out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    # concatenated output layout [world * per, ...]: accepted by every backend's
+    # all_gather_into_tensor (NCCL also takes a stacked one, gloo does not)
+    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     if hasattr(dist, "all_gather_into_tensor") and local.is_cuda:
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     else:
-        parts = list(out.unbind(0))
+        parts = list(out.reshape((world,) + tuple(local.shape)).unbind(0))
         dist.all_gather(parts, local.contiguous(), group=group)
-        out = torch.stack(parts)
-    return out.reshape((world * local.shape[0],) + tuple(local.shape[1:]))
+        out = torch.cat(parts)
+    return out
 
 
 def _local_rows(dev, oracle, cand, sch, tabs, tails_chunk, d, step, i0, world, rank):
