@@ -40,27 +40,6 @@ __global__ void poly_rotate_kernel(const int32_t* __restrict__ hf, const double2
   }
 }
 
-// r_h = h_head . z_l mod M_l and r_h * J1_l mod M_l (exact, 64-bit integer path)
-__global__ void poly_residue_kernel(const int32_t* __restrict__ hf, int s, LatTable lt,
-                                    PolyPlan pp, int32_t* __restrict__ rres, int32_t* __restrict__ rj) {
-  const int l = blockIdx.y;
-  const int64_t m = lt.m[l];
-  const int t1 = lt.d;
-  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < s; h += gridDim.x * blockDim.x) {
-    int64_t acc = 0;
-    for (int c = 0; c < t1; ++c) {
-      const int64_t km = mod_slow((int64_t)hf[(int64_t)c * s + h], m);
-      acc = (acc + (int64_t)(((uint64_t)km * (uint64_t)lt.z[l * t1 + c]) % (uint64_t)m)) % m;
-    }
-    rres[(int64_t)l * s + h] = (int32_t)acc;
-    rj[(int64_t)l * s + h] = (int32_t)(((uint64_t)acc * (uint64_t)pp.J1[l]) % (uint64_t)m);
-  }
-}
-
-constexpr int PT = 64;  // output tile edge (j1 and j2)
-constexpr int KC = 16;  // terms per shared-memory stage
-constexpr int SP_T = 256;  // threads per sampling CTA
-
 // (x mod m) for any x < 2^64 by Barrett reduction with mu = floor((2^64-1)/m):
 // the quotient estimate is low by at most one, so one correction is exact.
 // Integer pipe only (keeps the FP64 pipe for the contraction).
@@ -70,6 +49,32 @@ __device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t m, uint64_t
   if (r >= m) r -= m;
   return (uint32_t)r;
 }
+
+// r_h = h_head . z_l mod M_l and r_h * J1_l mod M_l: exact for every M < 2^31
+// (componentwise-reduced inner product as lattice.py:511-517; 32-bit
+// remainder of the int32 component, Barrett reduction of each product)
+__global__ void poly_residue_kernel(const int32_t* __restrict__ hf, int s, LatTable lt,
+                                    PolyPlan pp, int32_t* __restrict__ rres, int32_t* __restrict__ rj) {
+  const int l = blockIdx.y;
+  const uint32_t m = (uint32_t)lt.m[l];
+  const uint64_t mu = pp.mu[l];
+  const int t1 = lt.d;
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < s; h += gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (int c = 0; c < t1; ++c) {
+      int32_t k = hf[(int64_t)c * s + h] % (int32_t)m;  // m <= 2^31 - 1 fits int32
+      const uint32_t km = (uint32_t)(k < 0 ? k + (int32_t)m : k);
+      acc += mod_barrett((uint64_t)km * (uint64_t)lt.z[l * t1 + c], m, mu);
+      if (acc >= m) acc -= m;  // acc + x < 2m < 2^32
+    }
+    rres[(int64_t)l * s + h] = (int32_t)acc;
+    rj[(int64_t)l * s + h] = (int32_t)mod_barrett((uint64_t)acc * (uint64_t)pp.J1[l], m, mu);
+  }
+}
+
+constexpr int PT = 64;  // output tile edge (j1 and j2)
+constexpr int KC = 16;  // terms per shared-memory stage
+constexpr int SP_T = 256;  // threads per sampling CTA
 
 // Twiddle w^n = e^{2 pi i n / M} from the two shared-memory tables of the
 // CTA's lattice: w^n = Thi[n >> bl] * Tlo[n & (2^bl - 1)].
