@@ -18,6 +18,9 @@
 // Bhat = FFT_P(b) / P with b_m = conj(c_m) wrapped cyclically is built once per
 // lattice by the same forward passes (row pass in FWD_ONLY mode), so its
 // layout matches the data after the forward row FFT by construction.
+#include <stdlib.h>
+#include <string.h>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "plan.cuh"
@@ -267,6 +270,105 @@ fft_row_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom
   }
 }
 
+// Row pass specialised for rows of P2 = 2048 in 2048-element tiles (one row
+// per CTA, thread t holds elements t + 256 q, q < 8): the radix-8 first pass
+// of each FFT reads the thread's registers (the coalesced row load, or the
+// pointwise product), and the radix-4 last pass leaves its outputs in the
+// same registers (element j + 512 r of butterfly j = t + 256 q is slot
+// q + 2 r), so the Bhat product and the final store need no shared-memory
+// round trip: 6 instead of 10 shared-memory passes per row, same arithmetic
+// (bit-identical to fft_row_kernel).
+template <bool INV>
+__device__ __forceinline__ void row2048_first_pass(double2 (&v)[8], double2* s) {
+  dft_reg<8, INV>(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) s[Tile<2048>::pad(threadIdx.x * 8 + r)] = v[bitrev_small(r, 3)];
+  __syncthreads();
+}
+
+template <bool INV>
+__device__ __forceinline__ void row2048_last_pass(double2 (&v)[8], const double2* s,
+                                                  const double2* __restrict__ twN) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = threadIdx.x + q * FFT_T;
+    double2 w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w[r] = s[Tile<2048>::pad(j + r * 512)];
+    twiddle_reg<4, INV>(w, j, 1, twN);
+    dft_reg<4, INV>(w);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[q + 2 * r] = w[bitrev_small(r, 2)];
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(FFT_T, 4)
+fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom g, int total_rows,
+                   const double2* __restrict__ ftab, const double2* __restrict__ bhat) {
+  extern __shared__ double2 s[];
+  constexpr int N = 2048;
+  constexpr int rstride = Tile<2048>::rstride(N);
+  const int grow = blockIdx.x;
+  if (grow >= total_rows) return;
+  const int P1 = g.P1;
+  const int u = grow / P1, k1 = grow - u * P1;
+  double2* row = buf + (int64_t)u * ustride + (int64_t)k1 * N;
+  const double2* twN = ftab + g.off_p2;
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = __ldcs(&row[threadIdx.x + q * FFT_T]);
+  row2048_first_pass<false>(v, s);
+  stockham_pass<8, false, 2048>(s, 1, rstride, N, 8, twN);
+  stockham_pass<8, false, 2048>(s, 1, rstride, N, 64, twN);
+  row2048_last_pass<false>(v, s, twN);
+  if (MODE == 1) {
+    const double scale = 1.0 / (double)g.P;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) row[threadIdx.x + q * FFT_T] = make_double2(v[q].x * scale, v[q].y * scale);
+    return;
+  }
+  const double2* bh = bhat + (int64_t)ut.lat[u] * ustride + (int64_t)k1 * N;
+  double2 b[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) b[q] = __ldg(&bh[threadIdx.x + q * FFT_T]);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = cmul(v[q], b[q]);
+  __syncthreads();  // every thread's last-pass reads are done before the smem is rewritten
+  row2048_first_pass<true>(v, s);
+  stockham_pass<8, true, 2048>(s, 1, rstride, N, 8, twN);
+  stockham_pass<8, true, 2048>(s, 1, rstride, N, 64, twN);
+  row2048_last_pass<true>(v, s, twN);
+  // e^{+2 pi i i k1 / P} for i = t + 256 q by a short recurrence (see the column pass)
+  double2 w = twP(g, ftab, (int64_t)threadIdx.x * k1);
+  const double2 step = twP(g, ftab, (int64_t)FFT_T * k1);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    row[threadIdx.x + q * FFT_T] = cmulc(v[q], w);
+    w = cmul(w, step);
+  }
+}
+
+template <int MODE>
+static int launch_row2048(unsigned blocks, cudaStream_t st, double2* buf, int64_t us, const UnitTable& ut,
+                          const FftGeom& g, int total_rows, const double2* ftab, const double2* bhat) {
+  const size_t sm = (size_t)Tile<2048>::rstride(2048) * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute((const void*)fft_row2048_kernel<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return (int)e;
+  fft_row2048_kernel<MODE><<<blocks, FFT_T, sm, st>>>(buf, us, ut, g, total_rows, ftab, bhat);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+static bool row2048_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_B200_FFT_ROW2048");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  return v;
+}
+
 // compile-time size dispatch: TE = 2048 for log sizes <= 11, 4096 for 12
 // (the column length P1 = 2^11..2^12 of p = 23, 24 also uses 4096 tiles)
 template <bool INV>
@@ -379,6 +481,8 @@ int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, const F
   const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
   const int rows = g.te / g.P2;
+  if (g.te == 2048 && g.P2 == 2048 && g.P1 > 1 && row2048_enabled())
+    return launch_row2048<1>(total_rows, st, bhat, P, ut, g, total_rows, ftab, nullptr);
   return launch_row<1>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, bhat, P, ut, g, total_rows,
                        ftab, nullptr, chirp);
 }
@@ -392,8 +496,11 @@ int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const 
   const size_t sm = fft_smem_bytes(g.te, g.P2);
   const int total_rows = ut.nunits * g.P1;
   const int rows = g.te / g.P2;
-  rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, g, total_rows, ftab,
-                     bhat, chirp);
+  if (g.te == 2048 && g.P2 == 2048 && g.P1 > 1 && row2048_enabled())
+    rc = launch_row2048<0>(total_rows, st, buf, P, ut, g, total_rows, ftab, bhat);
+  else
+    rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, g, total_rows, ftab,
+                       bhat, chirp);
   if (rc) return rc;
   rc = run_cols(true, buf, P, ut, g, 0, ftab, chirp, st);
   prof_mark(PROF_FFT, false, st);

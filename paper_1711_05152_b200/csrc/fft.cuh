@@ -85,6 +85,27 @@ __device__ __forceinline__ void dft_reg(double2* v) {
   }
 }
 
+// Stockham twiddles of one radix-R butterfly: v[r] *= w^r (conjugate if INV),
+// w = twN[k * tstep]; w^r for r < R from two table entries (w^1, w^4): few
+// live registers
+template <int R, bool INV>
+__device__ __forceinline__ void twiddle_reg(double2* v, int k, int tstep, const double2* __restrict__ twN) {
+  const double2 w1 = __ldg(&twN[k * tstep]);
+  double2 wl[4];
+  wl[0] = make_double2(1.0, 0.0);
+  wl[1] = w1;
+  if (R > 2) { wl[2] = cmul(w1, w1); wl[3] = cmul(wl[2], w1); }
+  double2 w4 = make_double2(1.0, 0.0);
+  if (R > 4) w4 = __ldg(&twN[4 * k * tstep]);
+  double2 wh = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    if ((r & 3) == 0) wh = (r == 4) ? w4 : cmul(wh, w4);
+    const double2 w = (r & 3) == 0 ? wh : ((r < 4) ? wl[r & 3] : cmul(wh, wl[r & 3]));
+    v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+  }
+}
+
 // One Stockham radix-R pass over `rows` rows of length N (all in smem).
 // twN[m] = e^{-2 pi i m / N}, m < N (global, read-only).
 template <int R, bool INV, int TE>
@@ -107,23 +128,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int rows, int rstride,
       const int base = row * rstride;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[q][r] = s[base + Tile<TE>::pad(j + r * per_row)];
-      if (Ns > 1) {
-        // w^r for r < R from two table entries (w^1, w^4): few live registers
-        const double2 w1 = __ldg(&twN[k * tstep]);
-        double2 wl[4];
-        wl[0] = make_double2(1.0, 0.0);
-        wl[1] = w1;
-        if (R > 2) { wl[2] = cmul(w1, w1); wl[3] = cmul(wl[2], w1); }
-        double2 w4 = make_double2(1.0, 0.0);
-        if (R > 4) w4 = __ldg(&twN[4 * k * tstep]);
-        double2 wh = make_double2(1.0, 0.0);
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          if ((r & 3) == 0) wh = (r == 4) ? w4 : cmul(wh, w4);
-          const double2 w = (r & 3) == 0 ? wh : ((r < 4) ? wl[r & 3] : cmul(wh, wl[r & 3]));
-          v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
-        }
-      }
+      if (Ns > 1) twiddle_reg<R, INV>(v[q], k, tstep, twN);
       dft_reg<R, INV>(v[q]);
       obase[q] = row * rstride + ((j - k) * R + k);  // row offset + unpadded index
     }
