@@ -201,6 +201,29 @@ def measure_fp64_peak(dev, P):
     return max(res.values()), res["sfft_fp64_peak"], res["sfft_fp64_mma_peak"]
 
 
+def measure_l2_random_peak(dev, P, words: int):
+    """Measured random 32-bit L2 operation rates (G op/s) on a bitmap of the
+    alias scratch's size: atomicOr with the old value used, and loads."""
+    torch = dev.torch
+    bits = dev.zeros((max(int(words), 1024),), torch.int32)
+    blocks, per = dev.num_sms * 8, 64
+    res = {}
+    for mode, name in ((0, "atomic_or"), (1, "load")):
+        dev.call("sfft_l2_random_peak", P.device.dptr(bits), bits.numel(), blocks, per, mode)
+        dev.sync()
+        best = 0.0
+        for _ in range(3):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(dev.stream)
+            dev.call("sfft_l2_random_peak", P.device.dptr(bits), bits.numel(), blocks, per, mode)
+            b.record(dev.stream)
+            dev.sync()
+            best = max(best, blocks * 256 * per / (a.elapsed_time(b) * 1e-3) / 1e9)
+        res[name] = best
+    return res
+
+
 def load_traffic():
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
@@ -237,6 +260,25 @@ def secondary_rooflines(dev, sch, n, d, kernels):
         out[name] = dict(bound="hbm", algorithmic_bytes=nbytes, ms=ms, achieved=gbs, peak=peak, unit="GB/s",
                          frac=gbs / peak, **extra)
     out["peak_source"] = src
+    # K3's bytes are L2-resident bitmaps: its roofline is random L2 operations.
+    # Counted: one atomicOr (first bitmap) and one load (second bitmap) per
+    # candidate and lattice of the first chunk; the rarer second-bitmap
+    # atomics are left out (the fraction below is a lower bound).
+    from paper_1711_05152_b200.mr1l import first_chunk
+    from paper_1711_05152_b200 import _native
+    from paper_1711_05152_b200.device import hptr
+    import paper_1711_05152_b200 as P
+    lhi = first_chunk(n, sch.primes)
+    ms_np = np.asarray(sch.primes, dtype=np.int64)
+    words = int(_native.query("sfft_alias_scratch_words", hptr(ms_np), lhi))
+    rates = measure_l2_random_peak(dev, P, words)
+    ops = n * lhi
+    floor_ms = (ops / (rates["atomic_or"] * 1e9) + ops / (rates["load"] * 1e9)) * 1e3
+    out["alias"]["l2_random"] = {
+        "bound": "l2_random_ops", "lattices_evaluated": lhi, "atomic_or_ops": ops, "load_ops": ops,
+        "peak_gops": rates, "floor_ms": floor_ms, "frac": floor_ms / kernels["alias"],
+        "peak_source": "measured in this run: random 32-bit atomicOr / loads on an L2-resident bitmap of the "
+                       "alias scratch's size (sfft_l2_random_peak)"}
     return out
 
 

@@ -266,6 +266,10 @@ int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream);
  * MMAs per warp (512 flop each).  K1's roofline denominator is the larger of
  * this and the DFMA loop above. */
 int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream);
+/* K3 roofline probe: blocks x 256 threads x per_thread random 32-bit
+ * operations on a bitmap of `words` words (size it like the alias scratch so
+ * it is L2-resident): mode 0 atomicOr with the old value used, mode 1 loads. */
+int sfft_l2_random_peak(uint32_t* d_bits, int64_t words, int blocks, int per_thread, int mode, void* stream);
 
 #ifdef __cplusplus
 }

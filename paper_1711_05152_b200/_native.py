@@ -72,6 +72,7 @@ _SIGS = {
     "sfft_cscale": (_int, [_vp, _i64, _dbl, _int, _vp]),
     "sfft_fp64_peak": (_int, [_vp, _int, _int, _vp]),
     "sfft_fp64_mma_peak": (_int, [_vp, _int, _int, _vp]),
+    "sfft_l2_random_peak": (_int, [_vp, _i64, _int, _int, _int, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -22,6 +22,7 @@ int launch_scatter_residues(const int32_t* freqs, int64_t n, const LatTable& lt,
                             double2* acc, int num_sms, cudaStream_t st);
 int launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t st);
 int launch_fp64_mma_peak(double* out, int iters, int blocks, cudaStream_t st);
+int launch_l2_random_peak(uint32_t* bits, uint32_t words, int blocks, int per_thread, int mode, cudaStream_t st);
 int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* hf,
                             const double2* coef, int s, double2* out, cudaStream_t st);
 int launch_eval_bspline_points(const double* pts, int64_t n, const BsplineSpec& bs, double2* out,
@@ -824,6 +825,11 @@ int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream) {
 
 int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream) {
   return launch_fp64_mma_peak(d_out, iters, blocks, S(stream));
+}
+
+int sfft_l2_random_peak(uint32_t* d_bits, int64_t words, int blocks, int per_thread, int mode, void* stream) {
+  if (words < 1 || words > 0x7fffffffLL || blocks < 1 || per_thread < 1 || (mode != 0 && mode != 1)) return E_INVAL;
+  return launch_l2_random_peak(d_bits, (uint32_t)words, blocks, per_thread, mode, S(stream));
 }
 
 }  // extern "C"
