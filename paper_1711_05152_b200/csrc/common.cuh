@@ -11,11 +11,35 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
+#include <unordered_map>
 
 #define SFFT_DMAX 64          // largest dimension handled by the device kernels
 #define SFFT_LMAX 64          // masks are one uint64 word per candidate
 
 namespace sfft {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was already granted on this device (the attribute persists;
+// setting it on every launch cost microseconds of host time per call).
+inline cudaError_t set_smem_once(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> granted[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = granted[dev].find(fn);
+    if (it != granted[dev].end() && it->second >= (int)bytes) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    int& v = granted[dev][fn];
+    if ((int)bytes > v) v = (int)bytes;
+  }
+  return e;
+}
 
 // number of kernels this library has launched (reported by sfft_launch_count)
 inline std::atomic<long long> g_launches{0};

@@ -353,8 +353,7 @@ template <int MODE>
 static int launch_row2048(unsigned blocks, cudaStream_t st, double2* buf, int64_t us, const UnitTable& ut,
                           const FftGeom& g, int total_rows, const double2* ftab, const double2* bhat) {
   const size_t sm = (size_t)Tile<2048>::rstride(2048) * sizeof(double2);
-  cudaError_t e = cudaFuncSetAttribute((const void*)fft_row2048_kernel<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = set_smem_once((const void*)fft_row2048_kernel<MODE>, sm);
   if (e != cudaSuccess) return (int)e;
   fft_row2048_kernel<MODE><<<blocks, FFT_T, sm, st>>>(buf, us, ut, g, total_rows, ftab, bhat);
   SFFT_CHECK_LAUNCH();
@@ -376,8 +375,7 @@ static int launch_col(int te, int lg, dim3 grid, size_t sm, cudaStream_t st, dou
                       const UnitTable& ut, const FftGeom& p, int mask, const double2* ftab, const double2* chirp) {
 #define SFFT_COL(TEV, L)                                                                         \
   case L: {                                                                                      \
-    cudaError_t e = cudaFuncSetAttribute((const void*)fft_col_kernel<L, INV, TEV>,               \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+    cudaError_t e = set_smem_once((const void*)fft_col_kernel<L, INV, TEV>, sm);                 \
     if (e != cudaSuccess) return (int)e;                                                         \
     fft_col_kernel<L, INV, TEV><<<grid, FFT_T, sm, st>>>(buf, us, ut, p, mask, ftab, chirp);     \
     break;                                                                                       \
@@ -406,8 +404,7 @@ static int launch_row(int te, int lg, unsigned blocks, size_t sm, cudaStream_t s
                       const double2* bhat, const double2* chirp) {
 #define SFFT_ROW(TEV, L)                                                                         \
   case L: {                                                                                      \
-    cudaError_t e = cudaFuncSetAttribute((const void*)fft_row_kernel<L, MODE, TEV>,              \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+    cudaError_t e = set_smem_once((const void*)fft_row_kernel<L, MODE, TEV>, sm);                \
     if (e != cudaSuccess) return (int)e;                                                         \
     fft_row_kernel<L, MODE, TEV><<<blocks, FFT_T, sm, st>>>(buf, us, ut, p, total_rows, ftab, bhat, \
                                                             chirp);                              \

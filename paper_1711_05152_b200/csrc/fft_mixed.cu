@@ -103,7 +103,7 @@ static int launch_colx_t(bool inv, const FftGeom& g, dim3 grid, cudaStream_t st,
   constexpr int P1 = F << A;
   const size_t sm = (size_t)fft_col_ctas_cols(P1, 2048) * Tile<2048>::rstride(P1) * sizeof(double2);
   const void* fn = inv ? (const void*)fft_colx_kernel<A, F, true> : (const void*)fft_colx_kernel<A, F, false>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = set_smem_once(fn, sm);
   if (e != cudaSuccess) return (int)e;
   if (inv) fft_colx_kernel<A, F, true><<<grid, FFT_T, sm, st>>>(buf, us, ut, g, mask, ftab, chirp);
   else fft_colx_kernel<A, F, false><<<grid, FFT_T, sm, st>>>(buf, us, ut, g, mask, ftab, chirp);

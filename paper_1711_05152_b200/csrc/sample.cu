@@ -486,8 +486,7 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
     return 0;
   }
   if (pp.ks > 1) {
-    cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem_once((const void*)sample_poly_kernel<true>, smem);
     if (e != cudaSuccess) return (int)e;
     prof_mark(PROF_SAMPLE, true, st);
     sample_poly_kernel<true><<<ctas, SP_T, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,
@@ -501,8 +500,7 @@ int launch_sample_poly(const PolyPlan& pp, const LatTable& lt, const UnitTable& 
                                                                   buf, ustride, apply_chirp ? 1 : 0);
     SFFT_CHECK_LAUNCH();
   } else {
-    cudaError_t e = cudaFuncSetAttribute((const void*)sample_poly_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem_once((const void*)sample_poly_kernel<false>, smem);
     if (e != cudaSuccess) return (int)e;
     prof_mark(PROF_SAMPLE, true, st);
     sample_poly_kernel<false><<<ctas, SP_T, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf,

@@ -859,7 +859,7 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     static std::atomic<unsigned> epochs{0x5f3a0001u};  // odd, step 2: never 0, never repeats soon
     const unsigned epoch = epochs.fetch_add(2u);
     const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
-    cudaError_t e2 = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e2 = set_smem_once(fp, smem);
     if (e2 != cudaSuccess) return (int)e2;
     prof_mark(PROF_SAMPLE, true, st);
     if (!panels_ready) poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
@@ -880,7 +880,7 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
                                    : (const void*)sample_poly_ws_kernel<true, false>)
                              : (tc ? (const void*)sample_poly_ws_kernel<false, true>
                                    : (const void*)sample_poly_ws_kernel<false, false>);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(fn, smem);
   if (e != cudaSuccess) return (int)e;
   prof_mark(PROF_SAMPLE, true, st);
 #define SFFT_WS_LAUNCH(SPLIT, TCV)                                                                      \

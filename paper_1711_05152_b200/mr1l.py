@@ -308,17 +308,28 @@ class LatticeTables:
     chirp: object
     bhat: object
     ftab: object
+    _pcache: dict = field(default_factory=dict, repr=False, compare=False)  # shared with the LRU entry
 
     def prefix(self, L: int) -> "LatticeTables | None":
         """Tables of the first L lattices (twiddles/chirps are concatenated in
         lattice order, one Bhat row per lattice: a prefix is a view), or None
-        when the first L sizes need a smaller FFT than this set's."""
-        ms = self.ms[:L]
-        if fft_size(int(ms.max())) != self.P:
+        when the first L sizes need a smaller FFT than this set's.  The views
+        are cached with the tables (the step's host path after the alias
+        read-back is on the critical path)."""
+        got = self._pcache.get(L)
+        if got is None:
+            ms = self.ms[:L]
+            if fft_size(int(ms.max())) != self.P:
+                got = False
+            else:
+                tot = int(ms.sum())
+                got = (ms, self.tw[:tot], self.chirp[:tot], self.bhat[:L])
+            self._pcache[L] = got
+        if got is False:
             return None
-        tot = int(ms.sum())
+        ms, tw, chirp, bhat = got
         zs = self.zs[:L] if self.zs is not None else None
-        return LatticeTables(ms, zs, self.P, self.tw[:tot], self.chirp[:tot], self.bhat[:L], self.ftab)
+        return LatticeTables(ms, zs, self.P, tw, chirp, bhat, self.ftab)
 
 
 class _TableCache:
@@ -371,17 +382,18 @@ def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str 
     got = tc.get(key) if cache else None
     ftab = dev.fft_tables(P)
     if got is not None:
-        tw, chirp, bhat, _ = got
-        return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab)
+        tw, chirp, bhat, pc, _ = got
+        return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab, pc)
     tot = int(ms.sum())
     tw = dev.empty((tot, 2), torch.float64)
     chirp = dev.empty((tot, 2), torch.float64)
     dev.call("sfft_lattice_tables", hptr(ms), L, dptr(tw), dptr(chirp), ctx=ctx)
     bhat = dev.empty((L, P, 2), torch.float64)
     dev.call("sfft_bluestein_bhat", hptr(ms), L, P, dptr(ftab), dptr(chirp), dptr(bhat), ctx=ctx)
+    pc: dict = {}
     if cache:
-        tc.put(key, (tw, chirp, bhat), 32 * tot + 16 * L * P)
-    return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab)
+        tc.put(key, (tw, chirp, bhat, pc), 32 * tot + 16 * L * P)
+    return LatticeTables(ms, zs, P, tw, chirp, bhat, ftab, pc)
 
 
 @dataclass

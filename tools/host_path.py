@@ -41,6 +41,27 @@ def dla(self, t, ring=8):
 
 Device.call, Device.download_async = call, dla
 
+import paper_1711_05152_b200.mr1l as _m  # noqa: E402
+
+
+def _wrap(obj, name):
+    fn = getattr(obj, name)
+
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        out = fn(*a, **k)
+        stamps.append((f"py:{name}", t0, time.perf_counter()))
+        return out
+    setattr(obj, name, w)
+
+
+_wrap(_m.LatticeTables, "prefix")
+_wrap(_m, "_sample_units")
+_wrap(_m, "run_step")
+_wrap(_m, "build_scheme")
+run_step = _m.run_step
+build_scheme = _m.build_scheme
+
 
 def step(prev=None):
     prepare = lambda ms, z: prepare_step(dev, wl.oracle, cand, 1, ms, z, tails=[np.zeros(0)], d=10)  # noqa: E731
