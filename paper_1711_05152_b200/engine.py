@@ -25,7 +25,7 @@ import numpy as np
 from .core import FrequencyIndexSet, SearchBox, SparseSpectrum
 from .device import Device, dptr, get_device, hptr
 from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact, prepare_step,
-                   evaluate_callback, product, run_step)
+                   evaluate_callback, first_attempt_rng, product, run_step)
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig
 
@@ -142,12 +142,14 @@ def _permute_oracle(oracle, order):
     return _PermutedCallback(oracle, order)
 
 
-def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarray, step: int, it0: int):
-    """Samples of r anchored axis lines of component t -> device (r, K, 2)."""
+def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarray, step: int, it0: int,
+                 out=None):
+    """Samples of r anchored axis lines of component t -> device (r, K, 2)
+    (into ``out`` when given)."""
     torch = dev.torch
     r, d = anchors.shape
     K = int(box.sizes[t])
-    vals = dev.empty((r, K, 2), torch.float64)
+    vals = dev.empty((r, K, 2), torch.float64) if out is None else out
     base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
     noisy = isinstance(oracle, NoisyOracle)
     if isinstance(base, SparsePolynomialOracle):
@@ -160,7 +162,7 @@ def _line_values(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarra
     elif isinstance(base, BSplineOracle):
         pts = np.repeat(anchors, K, axis=0)
         pts[:, t] = np.tile(np.arange(K) / K, r)
-        d_pts = dev.upload(np.ascontiguousarray(pts))
+        d_pts = dev.upload(np.ascontiguousarray(pts), asynchronous=True)  # no stream drain per component
         order, start, comps, scale = base.host_spec()
         dev.call("sfft_eval_bspline_points", dptr(d_pts), r * K, d, len(base.groups), hptr(order),
                  hptr(start), hptr(comps), hptr(scale), dptr(vals), ctx=f"line sampling, step {step}")
@@ -252,8 +254,54 @@ def _detect_all(dev: Device, oracle, cfg: DetectionConfig, streams) -> list[np.n
     detections are launched back to back and read back with one
     synchronisation.  (Noisy and host-callback oracles keep the reference's
     per-step call order.)"""
-    launched = [_detect_launch(dev, oracle, t, cfg, np.random.default_rng(streams[t]), t)
-                for t in range(cfg.box.dim)]
+    return _detect_all_collect(dev, _detect_all_launch(dev, oracle, cfg, streams))
+
+
+def _detect_all_launch(dev: Device, oracle, cfg: DetectionConfig, streams):
+    """Launch the line detections of all components.  When every component
+    has the same extent (a centred box), the r lines of all d components go
+    through one sample buffer and ONE selection launch (rows are independent
+    lines, detect.py:229-236 per line), and a B-spline oracle evaluates all
+    d * r * K nodes in one launch from one upload."""
+    box = cfg.box
+    d = box.dim
+    same = len({(int(k), int(lo)) for k, lo in zip(box.sizes, box.lows)}) == 1
+    base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
+    if not same or isinstance(oracle, NoisyOracle) or int(box.sizes[0]) > 1024 or \
+            not isinstance(base, (SparsePolynomialOracle, BSplineOracle)):
+        return [_detect_launch(dev, oracle, t, cfg, np.random.default_rng(streams[t]), t) for t in range(d)]
+    torch = dev.torch
+    zero = cfg.mode == "deterministic_zero_anchor"
+    r, K, lo = cfg.r, int(box.sizes[0]), int(box.lows[0])
+    anchors = []
+    for t in range(d):
+        rng = np.random.default_rng(streams[t])
+        anchors.append(np.stack([np.zeros(d) if zero else rng.random(d) for _ in range(r)]))
+    vals = dev.empty((d * r, K, 2), torch.float64)
+    if isinstance(base, SparsePolynomialOracle):
+        for t in range(d):
+            _line_values(dev, oracle, t, box, anchors[t], t, 0, out=vals[t * r:(t + 1) * r])
+    else:
+        pts = np.repeat(np.concatenate(anchors), K, axis=0)
+        line = np.tile(np.arange(K) / K, r)
+        for t in range(d):
+            pts[t * r * K:(t + 1) * r * K, t] = line
+        d_pts = dev.upload(np.ascontiguousarray(pts), asynchronous=True)
+        order, start, comps, scale = base.host_spec()
+        dev.call("sfft_eval_bspline_points", dptr(d_pts), d * r * K, d, len(base.groups), hptr(order),
+                 hptr(start), hptr(comps), hptr(scale), dptr(vals), ctx="line sampling, all components")
+    coefs = dev.empty((d * r, K, 2), torch.float64)
+    keep = dev.empty((d * r, K), torch.uint8)
+    dev.call("sfft_line_select", dptr(vals), d * r, K, lo, int(cfg.local_sparsity), float(cfg.component_threshold),
+             dptr(coefs), dptr(keep), ctx="line selection, all components")
+    return ("batched", np.arange(lo, lo + K, dtype=np.int64), keep, r, d)
+
+
+def _detect_all_collect(dev: Device, launched) -> list[np.ndarray]:
+    if isinstance(launched, tuple):  # one (d * r, K) keep buffer
+        _, ks, keep, r, d = launched
+        raw = dev.download_many(keep)[0].view(np.uint8).reshape(d, r, -1).astype(bool).any(axis=1)
+        return [ks[raw[t]] for t in range(d)]
     outs = dev.download_many(*[keep for _, keep in launched])
     comps = []
     for (ks, keep), raw in zip(launched, outs):
@@ -319,7 +367,20 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
 
     hoisted = None
     if _is_device_oracle(oracle) and not isinstance(oracle, NoisyOracle):
-        hoisted = _detect_all(dev, oracle, cfg, detect_streams)
+        hoisted = _detect_all_launch(dev, oracle, cfg, detect_streams)
+    # host work of every step that does not depend on the previous steps,
+    # done while the line detections run: the anchors (their own streams) and
+    # the first lattice-search attempt's generator of each step
+    zero = cfg.mode == "deterministic_zero_anchor"
+    all_tails = []
+    first_rngs = []
+    for t in range(d):
+        r_t = 1 if t == d - 1 else cfg.r
+        anchor_rng = np.random.default_rng(anchor_streams[t])
+        all_tails.append([np.zeros(d - (t + 1)) if zero else anchor_rng.random(d - (t + 1)) for _ in range(r_t)])
+        first_rngs.append(first_attempt_rng(lattice_streams[t], cfg.b) if cfg.lattice_kind != "single" else None)
+    if hoisted is not None:
+        hoisted = _detect_all_collect(dev, hoisted)
 
     for t in range(d):
         t_step = time.perf_counter()
@@ -351,14 +412,11 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             rep.prefix_counts[t] = 0
             rep.step_times.append(time.perf_counter() - t_step)
             continue
+        tails = all_tails[t]  # the anchors' own stream (independent of the lattice search)
         if cfg.lattice_kind == "single":
             from .single import single_scheme
             sch = single_scheme(dev, cand)  # CBC (reference detect.py:269-271), no RNG consumed
         else:
-            # anchors first (their own stream, independent of the lattice search)
-            anchor_rng = np.random.default_rng(anchor_streams[t])
-            tail = d - (t + 1)
-            tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
             prepare = None
             if not sharded:
                 # while the alias kernel runs: buffers, the sampling operands
@@ -366,7 +424,8 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
                 prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
                                                      cached_tables_only=True, tails=tails, d=d)
             sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
-                               ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare)
+                               ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare,
+                               first_rng=first_rngs[t])
         rep.scheme_sizes[t] = sch.total_size
         rep.lattice_attempts[t] = sch.attempts
         rep.inversion_calls[t] = r_tilde * sch.total_size
@@ -375,10 +434,6 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
                 f"step {t}: sampling scheme covers only {cand.n - sch.uncovered}/{cand.n} "
                 f"candidates after {sch.attempts} attempts"
             )
-        if cfg.lattice_kind == "single":
-            anchor_rng = np.random.default_rng(anchor_streams[t])
-            tail = d - (t + 1)
-            tails = [np.zeros(tail) if zero else anchor_rng.random(tail) for _ in range(r_tilde)]
         if sharded:
             res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
         else:

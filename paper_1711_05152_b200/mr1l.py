@@ -30,7 +30,7 @@ from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig, candidate_primes
 
 __all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "speculate_scheme", "SchemeGuess", "run_step",
-           "prepare_step", "StepPrep", "StepResult",
+           "prepare_step", "StepPrep", "StepResult", "first_attempt_rng",
            "OracleInterrupt", "OracleError", "evaluate_callback"]
 
 UMAX = 256      # (iteration, lattice) units per launch (plan.cuh SFFT_UMAX)
@@ -153,6 +153,18 @@ def _attempt_streams(seed_seq: np.random.SeedSequence, b: int, lazy: bool):
                                      pool_size=seed_seq.pool_size)
 
 
+def first_attempt_rng(seed_seq: np.random.SeedSequence, b: int) -> np.random.Generator:
+    """The generator of attempt 1 of ``build_scheme(..., lazy_streams=True)``
+    (the first lazy child of ``seed_seq``), made ahead of time by a caller
+    that has idle host time (``build_scheme(first_rng=...)``)."""
+    return np.random.default_rng(next(_attempt_streams(seed_seq, b, True)))
+
+
+# primes and first alias chunk by (n, L_max, lambda) when every prime exceeds
+# the spread (the rows are then not needed): steps of equal |J_t| repeat them
+_PRIMES_MEMO: dict = {}
+
+
 @dataclass
 class SchemeGuess:
     """The first attempt of ``build_scheme`` computed before the candidate
@@ -201,7 +213,7 @@ def first_chunk(n: int, ms, target: float = 0.05) -> int:
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
                  ctx: str = "", lazy_streams: bool = False, prepare=None,
-                 guess: SchemeGuess | None = None) -> DeviceScheme:
+                 guess: SchemeGuess | None = None, first_rng: np.random.Generator | None = None) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -228,14 +240,24 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     spread = _spread_bound(cand, box_extent)
     if guess is not None and (not lazy_streams or len(guess.primes) != l_max or guess.primes[0] <= spread):
         guess = None
+    lam = cfg.size_lower_bound(n)
+    memo = _PRIMES_MEMO.get((n, l_max, lam))
     if guess is not None:
         primes = list(guess.primes)
+    elif memo is not None and memo[0][0] > spread:
+        primes = memo[0]
     else:
-        primes = candidate_primes(None, cfg.size_lower_bound(n), l_max, spread=spread,
-                                  rows=lambda: cand.to_host(dev))
+        primes = candidate_primes(None, lam, l_max, spread=spread, rows=lambda: cand.to_host(dev))
     ms = np.asarray(primes, dtype=np.int64)
     torch = dev.torch
-    l_hi = first_chunk(n, ms)
+    if memo is not None and memo[0] == primes:
+        l_hi = memo[1]
+    else:
+        l_hi = first_chunk(n, ms)
+        if primes[0] > spread:
+            if len(_PRIMES_MEMO) > 256:
+                _PRIMES_MEMO.clear()
+            _PRIMES_MEMO[(n, l_max, lam)] = (list(primes), l_hi)
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
     scratch = dev.empty((max(words, 1),), torch.int32)
     masks = dev.empty((n,), torch.int64)
@@ -248,7 +270,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         if attempt == 1 and guess is not None:
             z = guess.z
         else:
-            rng = np.random.default_rng(child)
+            rng = first_rng if (attempt == 1 and first_rng is not None and lazy_streams) else np.random.default_rng(child)
             # one vectorised draw with per-row bounds == the reference's per-prime
             # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
             z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
@@ -792,7 +814,7 @@ def product(dev: Device, prefixes: DeviceFreqs, comp: np.ndarray) -> DeviceFreqs
     tot = prefixes.n * nc
     out = dev.empty((prefixes.ncomp + 1, max(tot, 1)), torch.int32)
     if tot:
-        d_comp = dev.upload(comp)
+        d_comp = dev.upload(comp, asynchronous=True)  # no stream drain per step
         dev.call("sfft_candidate_product", dptr(prefixes.data), prefixes.n, prefixes.ncomp,
                  dptr(d_comp), nc, dptr(out), ctx="candidate product")
     kmax = max(prefixes.kmax, int(np.abs(comp).max()) if nc else 0)
