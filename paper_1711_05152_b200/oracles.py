@@ -195,8 +195,11 @@ DEFAULT_BSPLINE_GROUPS: tuple[tuple[int, tuple[int, ...]], ...] = (
 
 
 @lru_cache(maxsize=None)
+@lru_cache(maxsize=None)
 def bspline_l2_constant(m: int) -> float:
-    """C_m with ||C_m * periodised B_m||_2 = 1 (reference testbed.py:198-212)."""
+    """C_m with ||C_m * periodised B_m||_2 = 1 (reference testbed.py:198-212).
+    Memoised: a 2e5-term series per order (it was recomputed on every
+    sampling launch)."""
     if m < 1:
         raise ValueError("spline order must be >= 1")
     k = np.arange(1, 200_001)
@@ -234,6 +237,12 @@ class BSplineOracle(_DeviceOracle):
         return BSplineOracle(groups, self.dim, _counter=self._counter)
 
     def host_spec(self):
+        got = self.__dict__.get("_host_spec")
+        if got is None:
+            got = self.__dict__["_host_spec"] = self._make_host_spec()
+        return got
+
+    def _make_host_spec(self):
         order = np.array([m for m, _ in self.groups], dtype=np.int32)
         start = np.zeros(len(self.groups) + 1, dtype=np.int32)
         comps = []
