@@ -195,11 +195,8 @@ DEFAULT_BSPLINE_GROUPS: tuple[tuple[int, tuple[int, ...]], ...] = (
 
 
 @lru_cache(maxsize=None)
-@lru_cache(maxsize=None)
 def bspline_l2_constant(m: int) -> float:
-    """C_m with ||C_m * periodised B_m||_2 = 1 (reference testbed.py:198-212).
-    Memoised: a 2e5-term series per order (it was recomputed on every
-    sampling launch)."""
+    """C_m with ||C_m * periodised B_m||_2 = 1 (reference testbed.py:198-212)."""
     if m < 1:
         raise ValueError("spline order must be >= 1")
     k = np.arange(1, 200_001)
