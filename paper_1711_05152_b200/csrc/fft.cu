@@ -360,6 +360,14 @@ static int launch_row2048(unsigned blocks, cudaStream_t st, double2* buf, int64_
   return 0;
 }
 
+static bool colx2_pow2_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_B200_FFT_COLX2");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  return v;
+}
+
 static bool row2048_enabled() {
   static const bool v = [] {
     const char* e = getenv("SFFT_B200_FFT_ROW2048");
@@ -456,7 +464,8 @@ static int run_cols(bool inv, double2* buf, int64_t ustride, const UnitTable& ut
                     const double2* ftab, const double2* chirp, cudaStream_t st) {
   if (g.P1 == 1) return 0;
   dim3 grid(g.P2 / fft_col_ctas_cols(g.P1, g.te), ut.nunits);
-  if (g.f1 > 1) return launch_colx(inv, g, grid, st, buf, ustride, ut, mask, ftab, chirp);
+  if (g.f1 > 1 || (g.te == 2048 && g.a1 >= 4 && colx2_pow2_enabled()))
+    return launch_colx(inv, g, grid, st, buf, ustride, ut, mask, ftab, chirp);
   const size_t sm = fft_smem_bytes(g.te, g.P1);
   return inv ? launch_col<true>(g.te, g.a1, grid, sm, st, buf, ustride, ut, g, mask, ftab, chirp)
              : launch_col<false>(g.te, g.a1, grid, sm, st, buf, ustride, ut, g, mask, ftab, chirp);

@@ -284,6 +284,9 @@ int launch_colx(bool inv, const FftGeom& g, dim3 grid, cudaStream_t st, double2*
                 const UnitTable& ut, int mask_input, const double2* ftab, const double2* chirp) {
   if (g.te != 2048 || g.P2 != 2048) return -22;
   switch (g.f1) {
+    case 1:  // power-of-two columns of >= 16 (two or more passes) in 2048-element tiles
+      if (g.a1 < 4) return -22;
+      return dispatch_a<1, 4>(g.a1, inv, g, grid, st, buf, ustride, ut, mask_input, ftab, chirp);
     case 3: return dispatch_a<3, 0>(g.a1, inv, g, grid, st, buf, ustride, ut, mask_input, ftab, chirp);
     case 5: return dispatch_a<5, 0>(g.a1, inv, g, grid, st, buf, ustride, ut, mask_input, ftab, chirp);
     case 7: return dispatch_a<7, 0>(g.a1, inv, g, grid, st, buf, ustride, ut, mask_input, ftab, chirp);
