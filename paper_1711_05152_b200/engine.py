@@ -290,6 +290,7 @@ def _detect_all_launch(dev: Device, oracle, cfg: DetectionConfig, streams):
         order, start, comps, scale = base.host_spec()
         dev.call("sfft_eval_bspline_points", dptr(d_pts), d * r * K, d, len(base.groups), hptr(order),
                  hptr(start), hptr(comps), hptr(scale), dptr(vals), ctx="line sampling, all components")
+        base.count_samples(d * r * K)  # the oracle's own call audit, as _line_values
     coefs = dev.empty((d * r, K, 2), torch.float64)
     keep = dev.empty((d * r, K), torch.uint8)
     dev.call("sfft_line_select", dptr(vals), d * r, K, lo, int(cfg.local_sparsity), float(cfg.component_threshold),

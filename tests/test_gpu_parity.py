@@ -336,7 +336,9 @@ def test_sparse_fft_bspline(P, golden):
     oracle = P.bspline_test_function(groups)
     cfg = P.DetectionConfig(box=P.SearchBox.centered(10, 8, check_cardinality=False), delta=1e-4, s=200, r=2,
                             b=10, rng_seed=3)
+    c0 = oracle.call_count
     rep = P.sparse_fft(oracle, cfg)
+    assert oracle.call_count - c0 == rep.oracle_calls  # the audit (detect.py:421) incl. batched line nodes
     got = set(map(tuple, rep.detected.freqs.tolist()))
     ref = set(map(tuple, golden["bs_freqs"].tolist()))
     # parity modulo exact-magnitude +-k ties at the cap boundary (SURVEY §7 hard part 5)
