@@ -51,7 +51,7 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
         const int l = __ffsll((long long)mm) - 1;
         mm &= mm - 1;
         const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
-        const double invm = 1.0 / (double)lt.m[l];
+        const double invm = lt.inv_m[l];  // == 1.0 / M (host-computed, correctly rounded)
         ++cnt;
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
@@ -169,7 +169,7 @@ gather_units_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
       double2 t = make_double2(0.0, 0.0);
       if ((mask >> l) & 1ull) {
         const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
-        const double invm = 1.0 / (double)lt.m[l];
+        const double invm = lt.inv_m[l];  // == 1.0 / M (host-computed, correctly rounded)
         const double2 v = __ldg(&buf[(int64_t)j * ustride + r]);
         t = make_double2(__dmul_rn(v.x, invm), __dmul_rn(v.y, invm));
       }
