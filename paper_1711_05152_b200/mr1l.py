@@ -160,8 +160,8 @@ def first_attempt_rng(seed_seq: np.random.SeedSequence, b: int) -> np.random.Gen
     return np.random.default_rng(next(_attempt_streams(seed_seq, b, True)))
 
 
-# primes and first alias chunk by (n, L_max, lambda) when every prime exceeds
-# the spread (the rows are then not needed): steps of equal |J_t| repeat them
+# candidate primes by (n, L_max, lambda) when every prime exceeds the spread
+# (the rows are then not needed): steps of equal |J_t| repeat them
 _PRIMES_MEMO: dict = {}
 
 
@@ -250,14 +250,11 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         primes = candidate_primes(None, lam, l_max, spread=spread, rows=lambda: cand.to_host(dev))
     ms = np.asarray(primes, dtype=np.int64)
     torch = dev.torch
-    if memo is not None and memo[0] == primes:
-        l_hi = memo[1]
-    else:
-        l_hi = first_chunk(n, ms)
-        if primes[0] > spread:
-            if len(_PRIMES_MEMO) > 256:
-                _PRIMES_MEMO.clear()
-            _PRIMES_MEMO[(n, l_max, lam)] = (list(primes), l_hi)
+    l_hi = first_chunk(n, ms)
+    if memo is None and primes[0] > spread:
+        if len(_PRIMES_MEMO) > 256:
+            _PRIMES_MEMO.clear()
+        _PRIMES_MEMO[(n, l_max, lam)] = (list(primes),)
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
     scratch = dev.empty((max(words, 1),), torch.int32)
     masks = dev.empty((n,), torch.int64)

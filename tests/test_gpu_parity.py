@@ -270,6 +270,32 @@ def test_prepared_operands_only_for_first_attempt(P, golden):
     assert np.array_equal(dev.download(got.keep[0]), dev.download(ref.keep[0]))
 
 
+def test_prepared_step_when_first_chunk_does_not_cover(P, golden, monkeypatch):
+    """A first alias chunk that leaves candidates uncovered: the second chunk
+    runs, L exceeds the prepared lattices, and the step falls back to its own
+    operands — same masks, L and results as the one-pass default."""
+    from paper_1711_05152_b200 import mr1l
+    from paper_1711_05152_b200.device import get_device
+    from paper_1711_05152_b200.mr1l import DeviceFreqs, build_scheme, prepare_step, run_step
+    dev = get_device()
+    cand = golden["step_cand"].astype(np.int64)
+    oracle = P.SparsePolynomialOracle(golden["step_hf"], golden["step_hc"])
+    dc = DeviceFreqs.from_host(dev, cand)
+    seed, b = int(golden["step_seed"][0]), int(golden["step_b"][0])
+    tails = [np.zeros(0)]
+    sch = build_scheme(dev, dc, b, np.random.SeedSequence(seed))
+    ref = run_step(dev, oracle, dc, sch, tails, 10, 1e-12, len(cand))
+    monkeypatch.setattr(mr1l, "first_chunk", lambda n, ms, target=0.05: 3)
+    sch2 = build_scheme(dev, dc, b, np.random.SeedSequence(seed), lazy_streams=False,
+                        prepare=lambda ms, z: prepare_step(dev, oracle, dc, 1, ms, z, tails=tails, d=10))
+    assert sch2.prep is not None and sch2.prep.l_max == 3 < sch2.L == sch.L
+    used = np.uint64((1 << sch.L) - 1)  # bits of lattices past L differ (evaluated by one run only), unused
+    assert np.array_equal(dev.download(sch2.masks).view(np.uint64) & used, dev.download(sch.masks).view(np.uint64) & used)
+    got = run_step(dev, oracle, dc, sch2, tails, 10, 1e-12, len(cand), prep=sch2.prep)
+    assert np.array_equal(dev.download(got.coef[0]), dev.download(ref.coef[0]))
+    assert np.array_equal(dev.download(got.keep[0]), dev.download(ref.keep[0]))
+
+
 def _check_report(golden, key, rep, exact_coef=True):
     assert np.array_equal(rep.detected.freqs, golden[f"{key}_freqs"]), key
     ref = golden[f"{key}_coef"]
