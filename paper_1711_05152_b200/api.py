@@ -196,10 +196,22 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
                        prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d),
                        guess=spec[0] if spec else None)
+    # the masks are final once the scheme is built: their copy to the host runs
+    # on a side stream while the sampling kernel runs
+    words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
+    ready = torch.cuda.Event()
+    ready.record(dev.stream)
+    side = dev.copy_stream()
+    side.wait_event(ready)
+    with torch.cuda.stream(side):
+        words_h.copy_(sch.masks.view(torch.uint8), non_blocking=True)
+    sch.masks.record_stream(side)
     res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
                    defer_cap=True, prep=sch.prep)
     res.finalize()  # cap applied (if binding) before the results are read
-    coef, keep, words = dev.download_many(res.coef[0], res.keep[0], sch.masks)
+    coef, keep = dev.download_many(res.coef[0], res.keep[0])
+    side.synchronize()
+    words = words_h.numpy()
     d2h = coef.nbytes + keep.nbytes + words.nbytes
     coef = coef.view(np.complex128).reshape(n)  # views of fresh pinned buffers: no host copy
     return StepReport(coef, words.view(np.uint64) != 0, keep.view(bool),

@@ -145,6 +145,14 @@ class Device:
     def sync(self):
         self.stream.synchronize()
 
+    def copy_stream(self):
+        """A second stream of this device for copies that overlap the engine
+        stream's kernels (callers order it with events)."""
+        st = getattr(self, "_copy_stream", None)
+        if st is None:
+            st = self._copy_stream = self.torch.cuda.Stream(self.device)
+        return st
+
     # -- cached tables ------------------------------------------------------
     def fft_tables(self, P: int):
         tab = self._ftab.get(P)
