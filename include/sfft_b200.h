@@ -106,7 +106,8 @@ int sfft_bluestein(const int64_t* h_m, int L, int rb, int64_t P, const double* d
  * _invert_candidates (detect.py:290-299): unit u = i*L + l gets
  * x_n * chirp_l[n] (n < M_l) in its buffer, x_n = p(node n of lattice l with
  * anchor tail i).  Terms: d_hfreqs component-major (d x s int32), d_hcoef s
- * complex.  h_anchor: rb x (d - t1) doubles.  Scratch: d_cprime rb*s complex,
+ * complex.  h_anchor: rb x (d - t1) doubles, rb * (d - t1) <= 512 (else
+ * -7).  Scratch: d_cprime rb*s complex,
  * d_rres and d_rj L*s int32 each, d_partial partial_len complex (term-slice
  * partial sums; sfft_sample_poly_scratch() gives the size for the best
  * split, a smaller buffer selects a smaller split, 0 disables it).

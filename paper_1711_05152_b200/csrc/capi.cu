@@ -500,7 +500,7 @@ static int sample_poly_impl(const int32_t* d_hfreqs, const double* d_hcoef, int 
   rc = fill_units(ut, h_m, L, rb, h_units, nunits);
   if (rc) return rc;
   const int tail = d - t1;
-  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  if ((int64_t)rb * tail > SFFT_ANCHOR_MAX) return E_2BIG;
   AnchorTable at;
   at.rb = rb;
   at.tail = tail;
@@ -548,7 +548,7 @@ int sfft_sample_poly_prepare(const int32_t* d_hfreqs, const double* d_hcoef, int
   rc = fill_units(ut, h_m, L, rb, nullptr, 0);
   if (rc) return rc;
   const int tail = d - t1;
-  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  if ((int64_t)rb * tail > SFFT_ANCHOR_MAX) return E_2BIG;
   AnchorTable at;
   at.rb = rb;
   at.tail = tail;
@@ -607,7 +607,7 @@ int sfft_sample_bspline(int ngroups, const int32_t* h_order, const int32_t* h_st
   rc = fill_bspline(bs, ngroups, h_order, h_start, h_comps, h_scale, d);
   if (rc) return rc;
   const int tail = d - t1;
-  if ((int64_t)rb * tail > 1024) return E_2BIG;
+  if ((int64_t)rb * tail > SFFT_ANCHOR_MAX) return E_2BIG;
   AnchorTable at;
   at.rb = rb;
   at.tail = tail;

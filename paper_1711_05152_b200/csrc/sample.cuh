@@ -4,10 +4,13 @@
 namespace sfft {
 
 // anchor tails of the iterations in one launch: a[it * tail + c]
+// anchor tails of the rb <= 8 iterations of a chunk (tail = d - t1 <= 63):
+// by value in the launch parameters, so sized to what the engine passes
+#define SFFT_ANCHOR_MAX 512
 struct AnchorTable {
   int rb;
   int tail;
-  double a[1024];
+  double a[SFFT_ANCHOR_MAX];
 };
 
 // GEMM-factored polynomial sampling plan of one step (see sample.cu)
