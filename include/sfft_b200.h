@@ -33,7 +33,10 @@
 extern "C" {
 #endif
 
-#define SFFT_B200_ABI_VERSION 2
+/* ABI history: 3 = anchor tables of the sampling entries limited to
+ * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
+ * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
+#define SFFT_B200_ABI_VERSION 3
 
 int sfft_abi_version(void);
 /* kernels launched by this library since load (all devices, all streams) */
@@ -225,9 +228,17 @@ int sfft_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const
                   const int32_t* h_z, int L, int64_t* d_out, void* stream);
 
 /* ---- line detection (detect.py:175-240) ------------------------------------
- * r lines of K points of component t (K <= 1024), anchors h_anchors (r x d). */
+ * r lines of K points of component t, anchors h_anchors (r x d, r * d <= 2048).
+ * sfft_line_select (K <= 1024): DFT, bins, threshold and cap of each line in
+ * one CTA.  Longer lines: pre-chirp + sfft_bluestein as for a lattice of size
+ * K (one unit per line), then sfft_line_bins maps the spectra (row i at
+ * d_spectra + 2 * i * P doubles) to coefficients of k = lo .. lo + K - 1
+ * (bin k mod K, times 1/K), threshold flags and per-line survivor counts;
+ * the cap is sfft_select_cap_rows with those counts. */
 int sfft_line_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t,
                           int K, const double* h_anchors, int r, double* d_values, void* stream);
+int sfft_line_bins(const double* d_spectra, int64_t P, int r, int K, int64_t lo, double delta,
+                   double* d_coefs, uint8_t* d_keep, int32_t* d_counts, void* stream);
 int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, double delta,
                      double* d_coefs, uint8_t* d_keep, void* stream);
 

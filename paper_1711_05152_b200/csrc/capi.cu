@@ -764,6 +764,12 @@ int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, 
                             d_keep, S(stream));
 }
 
+int sfft_line_bins(const double* d_spectra, int64_t P, int r, int K, int64_t lo, double delta,
+                   double* d_coefs, uint8_t* d_keep, int32_t* d_counts, void* stream) {
+  return launch_line_bins((const double2*)d_spectra, P, r, K, lo, delta, (double2*)d_coefs, d_keep, d_counts,
+                          num_sms_current(), S(stream));
+}
+
 int sfft_eval_poly_points(const double* d_pts, int64_t n, int d, const int32_t* d_hfreqs,
                           const double* d_hcoef, int s, double* d_out, void* stream) {
   if (n < 0 || d < 1 || s < 0) return E_INVAL;

@@ -6,7 +6,12 @@
 //     p(x_l) = sum_h c''_h w_K^{(h_t l) mod K},  c''_h = c_h e^{2 pi i sum_{u != t} h_u a_u},
 // then bins = DFT_K(samples) * (1/K), bin l <-> the k in [lo, hi] with
 // k = l (mod K), and the line keeps the up-to-cap largest |coefficients| >=
-// delta (ties: |c| desc, k asc).  Lines are tiny (K <= 1024), one CTA each.
+// delta (ties: |c| desc, k asc).  Lines up to K = 1024 take one CTA each for
+// sampling and for DFT + selection.  Longer lines (any K, SURVEY §8a-2 puts
+// no limit on the box) are sampled by a tiled kernel with exact per-point
+// phases; their DFT is the batched Bluestein path (transform.py:50-64) and
+// line_bins_kernel maps the spectra to thresholded coefficients, the cap
+// then being the exact row selection of the MR1L step (sfft_select_cap_rows).
 #include "common.cuh"
 #include "plan.cuh"
 #include "lines.cuh"
@@ -76,6 +81,75 @@ line_sample_poly_kernel(const int32_t* __restrict__ hf, const double2* __restric
   }
 }
 
+// K > 1024: grid (line, block of LT points); twiddles e^{2 pi i idx / K} with
+// the exact integer phase idx = (e l) mod K evaluated directly
+__global__ void __launch_bounds__(LT)
+line_sample_poly_big_kernel(const int32_t* __restrict__ hf, const double2* __restrict__ coef, int s,
+                            int d, int t, int K, LineAnchors la, double2* __restrict__ values) {
+  __shared__ double2 cs[LCH];
+  __shared__ int es[LCH];
+  const int line = blockIdx.y;
+  const double* a = la.a + line * d;
+  const int l = blockIdx.x * LT + threadIdx.x;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int h0 = 0; h0 < s; h0 += LCH) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < LCH; q += LT) {
+      const int h = h0 + q;
+      double2 cc = make_double2(0.0, 0.0);
+      int e = 0;
+      if (h < s) {
+        double ph = 0.0;
+        for (int u = 0; u < d; ++u)
+          if (u != t) ph += (double)hf[(int64_t)u * s + h] * a[u];
+        double sn, c;
+        sincospi(2.0 * ph, &sn, &c);
+        cc = cmul(coef[h], make_double2(c, sn));
+        e = (int)mod_slow((int64_t)hf[(int64_t)t * s + h], K);
+      }
+      cs[q] = cc;
+      es[q] = e;
+    }
+    __syncthreads();
+    if (l < K) {
+      for (int q = 0; q < LCH && h0 + q < s; ++q) {
+        const int64_t idx = ((int64_t)es[q] * l) % K;
+        double sn, c;
+        sincospi(2.0 * (double)idx / (double)K, &sn, &c);
+        const double2 cc = cs[q];
+        acc.x = fma(cc.x, c, acc.x);
+        acc.x = fma(-cc.y, sn, acc.x);
+        acc.y = fma(cc.x, sn, acc.y);
+        acc.y = fma(cc.y, c, acc.y);
+      }
+    }
+  }
+  if (l < K) values[(int64_t)line * K + l] = acc;
+}
+
+// K > 1024: spectra (row i at spec + i * P, the unnormalised forward DFT of
+// line i) -> coefficient of k = lo + q is bin (k mod K) * (1/K), threshold
+// flag and per-line survivor count (integer atomics: order-free, exact)
+__global__ void line_bins_kernel(const double2* __restrict__ spec, int64_t P, int K, int64_t lo, double delta,
+                                 double2* __restrict__ coefs, uint8_t* __restrict__ keep,
+                                 int32_t* __restrict__ counts) {
+  const int line = blockIdx.y;
+  const double invk = 1.0 / (double)K;
+  int cnt = 0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < K; q += gridDim.x * blockDim.x) {
+    const int bin = (int)mod_slow(lo + q, K);
+    const double2 x = spec[(int64_t)line * P + bin];
+    const double2 c = make_double2(x.x * invk, x.y * invk);
+    coefs[(int64_t)line * K + q] = c;
+    const uint8_t kf = hypot(c.x, c.y) >= delta ? 1 : 0;
+    keep[(int64_t)line * K + q] = kf;
+    cnt += kf;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&counts[line], cnt);
+}
+
 // DFT of each line, bin mapping, threshold and cap ranking
 __global__ void __launch_bounds__(LT)
 line_select_kernel(const double2* __restrict__ values, int K, int64_t lo, int cap, double delta,
@@ -132,8 +206,11 @@ line_select_kernel(const double2* __restrict__ values, int K, int64_t lo, int ca
 
 int launch_line_sample_poly(const int32_t* hf, const double2* coef, int s, int d, int t, int K,
                             const LineAnchors& la, int r, double2* values, cudaStream_t st) {
-  if (K > 1024 || r <= 0) return -22;
-  line_sample_poly_kernel<<<r, LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
+  if (K < 1 || r <= 0 || r > 65535) return -22;
+  if (K > 1024)
+    line_sample_poly_big_kernel<<<dim3((K + LT - 1) / LT, r), LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
+  else
+    line_sample_poly_kernel<<<r, LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
   SFFT_CHECK_LAUNCH();
   return 0;
 }
@@ -142,6 +219,19 @@ int launch_line_select(const double2* values, int r, int K, int64_t lo, int cap,
                        double2* coefs, uint8_t* keep, cudaStream_t st) {
   if (K > 1024 || r <= 0) return -22;
   line_select_kernel<<<r, LT, 0, st>>>(values, K, lo, cap, delta, coefs, keep);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_line_bins(const double2* spec, int64_t P, int r, int K, int64_t lo, double delta, double2* coefs,
+                     uint8_t* keep, int32_t* counts, int num_sms, cudaStream_t st) {
+  if (K < 1 || r <= 0 || r > 65535 || P < K) return -22;
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)r, st);
+  if (e != cudaSuccess) return (int)e;
+  int bx = (K + 255) / 256;
+  const int cap = (num_sms * 8 + r - 1) / r;
+  if (bx > cap) bx = cap > 0 ? cap : 1;
+  line_bins_kernel<<<dim3(bx, r), 256, 0, st>>>(spec, P, K, lo, delta, coefs, keep, counts);
   SFFT_CHECK_LAUNCH();
   return 0;
 }

@@ -12,5 +12,7 @@ int launch_line_sample_poly(const int32_t* hf, const double2* coef, int s, int d
                             const LineAnchors& la, int r, double2* values, cudaStream_t st);
 int launch_line_select(const double2* values, int r, int K, int64_t lo, int cap, double delta,
                        double2* coefs, uint8_t* keep, cudaStream_t st);
+int launch_line_bins(const double2* spec, int64_t P, int r, int K, int64_t lo, double delta, double2* coefs,
+                     uint8_t* keep, int32_t* counts, int num_sms, cudaStream_t st);
 
 }  // namespace sfft

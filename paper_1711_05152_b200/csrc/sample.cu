@@ -393,17 +393,27 @@ int launch_finish_devnoise(const UnitTable& ut, const double2* chirp, double2* b
   return 0;
 }
 
-// squared 2-norm of each unit's first M samples (for relative-noise oracles)
-__global__ void unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf, int64_t ustride,
-                                  double* __restrict__ out) {
-  __shared__ double red[32];
+// squared 2-norm of each unit's first M samples (for relative-noise oracles).
+// Deterministic: a cluster of NORM_CL CTAs per unit, each CTA a fixed
+// strided slice reduced in a fixed tree, the CTA partials summed in rank
+// order by rank 0 through distributed shared memory.  The rounding depends
+// on nothing but the unit's samples (not on which units share the launch,
+// i.e. not on the GPU count of a sharded step).
+constexpr int NORM_CL = 8;
+constexpr int NORM_NT = 512;
+
+__global__ void __cluster_dims__(NORM_CL, 1, 1) __launch_bounds__(NORM_NT)
+unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf, int64_t ustride, double* __restrict__ out) {
+  __shared__ double red[NORM_NT / 32];
+  __shared__ double part;
   const int u = blockIdx.y;
   const int64_t M = ut.m[ut.lat[u]];
   const double2* ub = buf + (int64_t)u * ustride;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   double acc = 0.0;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
-       n += (int64_t)gridDim.x * blockDim.x) {
-    const double2 v = ub[n];
+  for (int64_t n = (int64_t)rank * NORM_NT + threadIdx.x; n < M; n += (int64_t)NORM_CL * NORM_NT) {
+    const double2 v = __ldcs(&ub[n]);
     acc = fma(v.x, v.x, fma(v.y, v.y, acc));
   }
 #pragma unroll
@@ -412,9 +422,24 @@ __global__ void unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf,
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    atomicAdd(&out[u], t);
+    for (int w = 0; w < NORM_NT / 32; ++w) t += red[w];
+    part = t;
   }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (rank == 0 && threadIdx.x == 0) {
+    double t = 0.0;
+    const uint32_t local = (uint32_t)__cvta_generic_to_shared(&part);
+    for (uint32_t c = 0; c < NORM_CL; ++c) {
+      uint32_t remote;
+      double v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(c));
+      asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+      t += v;
+    }
+    out[u] = t;
+  }
+  // no CTA may exit while rank 0 still reads its shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // lattice nodes for a host-callback oracle: pts[n, c] (row-major, d columns)
@@ -546,14 +571,8 @@ int launch_finish_samples(const UnitTable& ut, const double2* chirp, double2* bu
 
 int launch_unit_norm2(const UnitTable& ut, const double2* buf, int64_t ustride, double* out,
                       int num_sms, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * ut.nunits, st);
-  if (e != cudaSuccess) return (int)e;
-  int64_t mmax = 1;
-  for (int l = 0; l < ut.nlat; ++l) mmax = ut.m[l] > mmax ? ut.m[l] : mmax;
-  int bx = (int)((mmax + 255) / 256);
-  const int cap = (num_sms * 4 + ut.nunits - 1) / ut.nunits + 1;
-  if (bx > cap) bx = cap;
-  unit_norm2_kernel<<<dim3(bx, ut.nunits), 256, 0, st>>>(ut, buf, ustride, out);
+  (void)num_sms;
+  unit_norm2_kernel<<<dim3(NORM_CL, ut.nunits), NORM_NT, 0, st>>>(ut, buf, ustride, out);
   SFFT_CHECK_LAUNCH();
   return 0;
 }

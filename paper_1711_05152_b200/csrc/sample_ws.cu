@@ -33,8 +33,8 @@ constexpr int KC = 16;       // terms per stage
 constexpr int NS = 3;        // stages
 constexpr int NCONS = 256;   // consumer threads (two warpgroups)
 constexpr int NPROD = 128;   // producer threads (one warpgroup)
-constexpr int REG_CONS = 224;  // setmaxnreg: consumers grow, producers shrink, so that
-constexpr int REG_PROD = 56;   // 2 consumer + 1 producer warps fit one SMSP's 16K registers
+constexpr int REG_CONS = 232;  // setmaxnreg: consumers grow, producers shrink: 8 x 232 + 4 x 48
+constexpr int REG_PROD = 48;   // warps = the 64K-register file exactly (no spills in either role)
 constexpr int NT = NCONS + NPROD;
 constexpr int STAGE = KC * (TJ1 + TJ2);  // complex elements per stage
 }  // namespace ws
@@ -855,25 +855,60 @@ int launch_sample_poly_ws(const PolyPlan& pp, const LatTable& lt, const double2*
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     int grid = ctas < nsm ? ctas : nsm;
     if (grid > SFFT_WS_MAX_FLAGS) grid = SFFT_WS_MAX_FLAGS;
-    // launch-unique flag value: the flags need no reset between launches
-    static std::atomic<unsigned> epochs{0x5f3a0001u};  // odd, step 2: never 0, never repeats soon
-    const unsigned epoch = epochs.fetch_add(2u);
     const void* fp = pp.ks > 1 ? (const void*)sample_poly_tcp_kernel<true> : (const void*)sample_poly_tcp_kernel<false>;
     cudaError_t e2 = set_smem_once(fp, smem);
     if (e2 != cudaSuccess) return (int)e2;
+    // The in-kernel K-split reduction spins on flags published by other CTAs
+    // of the grid, so it needs all CTAs co-resident: a cooperative launch
+    // (the driver refuses one that cannot be co-resident, e.g. under MPS
+    // limits or SMs held by other work) and the flags zeroed on the stream.
+    // Without co-residency the slices go through partials + the ordered
+    // reduce kernel instead (same rounding: the caller sees *reduced = false).
+    if (flags != nullptr && pp.ks > 1) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp, ws::NT, smem) != cudaSuccess ||
+          per_sm * nsm < grid)
+        flags = nullptr;
+    }
+    const unsigned epoch = 1u;
     prof_mark(PROF_SAMPLE, true, st);
     if (!panels_ready) poly_bpanel_kernel<<<pp.npanels, 128, 0, st>>>(pp, lt, rj, tw, panels);
-    if (pp.ks > 1)
+    int launched = panels_ready ? 0 : 1;
+    if (pp.ks > 1 && flags != nullptr) {
+      cudaError_t em = cudaMemsetAsync(flags, 0, sizeof(unsigned) * (size_t)grid, st);
+      if (em != cudaSuccess) return (int)em;
+      int apply = apply_chirp ? 1 : 0;
+      int64_t ustride_ = ustride, pstride_ = pstride;
+      unsigned epoch_ = epoch;
+      PolyPlan pp_ = pp;
+      LatTable lt_ = lt;
+      void* args[] = {(void*)&pp_, (void*)&lt_, (void*)&cprime, (void*)&rres, (void*)&rj, (void*)&tw,
+                      (void*)&chirp, (void*)&buf, (void*)&ustride_, (void*)&apply, (void*)&part,
+                      (void*)&pstride_, (void*)&panels, (void*)&flags, (void*)&epoch_};
+      cudaError_t ec = cudaLaunchCooperativeKernel(fp, dim3(grid), dim3(ws::NT), args, smem, st);
+      if (ec == cudaErrorCooperativeLaunchTooLarge) {
+        (void)cudaGetLastError();
+        flags = nullptr;
+      } else if (ec != cudaSuccess) {
+        return (int)ec;
+      } else {
+        ++launched;
+      }
+    }
+    if (pp.ks > 1 && flags == nullptr) {
       sample_poly_tcp_kernel<true><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
                                                                apply_chirp ? 1 : 0, part, pstride, panels,
-                                                               flags, epoch);
-    else
+                                                               nullptr, 0u);
+      ++launched;
+    } else if (pp.ks <= 1) {
       sample_poly_tcp_kernel<false><<<grid, ws::NT, smem, st>>>(pp, lt, cprime, rres, rj, tw, chirp, buf, ustride,
                                                                 apply_chirp ? 1 : 0, nullptr, 0, panels,
                                                                 nullptr, 0u);
+      ++launched;
+    }
     prof_mark(PROF_SAMPLE, false, st);
     *reduced = pp.ks == 1 || flags != nullptr;
-    SFFT_CHECK_LAUNCHES(panels_ready ? 1 : 2);
+    SFFT_CHECK_LAUNCHES(launched);
     return 0;
   }
   const void* fn = pp.ks > 1 ? (tc ? (const void*)sample_poly_ws_kernel<true, true>

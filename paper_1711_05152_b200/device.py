@@ -55,6 +55,7 @@ class Device:
         self.cc = (maj.value, mnr.value)
         self._ftab: dict[int, object] = {}
         self._pinned: dict[int, object] = {}
+        self._async_free: dict[int, list] = {}  # recycled download_async buffers by size
 
     # -- raw handles ------------------------------------------------------
     @property
@@ -117,29 +118,30 @@ class Device:
         self.stream.synchronize()
         return buf.numpy().view(np.dtype(str(t.dtype).replace("torch.", ""))).reshape(t.shape).copy()
 
-    def download_async(self, t, ring: int = 8):
-        """Start a copy of a small device tensor into one of `ring` reusable
-        pinned slots (round robin) and return a callable that waits for it and
-        returns the host array.  Lets a caller keep enqueuing work and read the
-        value later; the slot is reused `ring` calls later."""
+    def download_async(self, t):
+        """Start a copy of a small device tensor into a pinned buffer and
+        return a callable that waits for it and returns the host array.  Lets
+        a caller keep enqueuing work and read the value later.  Each pending
+        download owns its buffer until its wait() has run (buffers are then
+        recycled), so any number of downloads may be outstanding."""
         torch = self.torch
         nbytes = t.numel() * t.element_size()
-        self._ring_pos = (getattr(self, "_ring_pos", -1) + 1) % ring
-        key = ("ring", self._ring_pos, nbytes)
-        buf = self._pinned.get(key)
-        if buf is None:
-            buf = torch.empty((nbytes,), dtype=torch.uint8, pin_memory=True)
-            self._pinned[key] = buf
+        free = self._async_free.setdefault(nbytes, [])
+        buf = free.pop() if free else torch.empty((max(nbytes, 1),), dtype=torch.uint8, pin_memory=True)
         with torch.cuda.stream(self.stream):
-            buf.copy_(t.detach().reshape(-1).view(torch.uint8), non_blocking=True)
+            buf[:nbytes].copy_(t.detach().reshape(-1).view(torch.uint8), non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(self.stream)
         dtype = np.dtype(str(t.dtype).replace("torch.", ""))
         shape = tuple(t.shape)
+        state = {"out": None}
 
         def wait():
-            ev.synchronize()
-            return buf.numpy().view(dtype).reshape(shape).copy()
+            if state["out"] is None:
+                ev.synchronize()
+                state["out"] = buf[:nbytes].numpy().view(dtype).reshape(shape).copy()
+                free.append(buf)
+            return state["out"].copy()
         return wait
 
     def sync(self):

@@ -211,14 +211,46 @@ def _lines(dev: Device, oracle, t: int, box: SearchBox, anchors: np.ndarray, cap
     r = anchors.shape[0]
     K = int(box.sizes[t])
     lo = int(box.lows[t])
-    if K > 1024:
-        raise NotImplementedError("line detection supports component extents K_t <= 1024")
     vals = _line_values(dev, oracle, t, box, anchors, step, 0)
     coefs = dev.empty((r, K, 2), torch.float64)
     keep = dev.empty((r, K), torch.uint8)
-    dev.call("sfft_line_select", dptr(vals), r, K, lo, int(cap), float(delta), dptr(coefs), dptr(keep),
-             ctx=f"line selection, step {step}")
+    if K <= 1024:
+        dev.call("sfft_line_select", dptr(vals), r, K, lo, int(cap), float(delta), dptr(coefs), dptr(keep),
+                 ctx=f"line selection, step {step}")
+    else:
+        _long_line_select(dev, vals, r, K, lo, int(cap), float(delta), coefs, keep, step)
     return np.arange(lo, lo + K, dtype=np.int64), coefs, keep
+
+
+def _long_line_select(dev: Device, vals, r: int, K: int, lo: int, cap: int, delta: float, coefs, keep,
+                      step: int):
+    """Lines longer than 1024 points: each line is one unit of a 'lattice'
+    of size K through the MR1L step's own Bluestein kernels (dft_1d of
+    detect.py:191), then bins/threshold (sfft_line_bins) and the exact row
+    cap (sfft_select_cap_rows: |c| desc, then k asc — the lines' q order)."""
+    from . import _native
+    from .mr1l import UMAX, lattice_tables
+    torch = dev.torch
+    tabs = lattice_tables(dev, np.array([K], dtype=np.int64), None, ctx=f"line tables, step {step}")
+    counts = dev.empty((r,), torch.int32)
+    per = min(r, UMAX)
+    buf = dev.zeros((per, tabs.P, 2), torch.float64)
+    for i0 in range(0, r, per):
+        nb = min(per, r - i0)
+        with torch.cuda.stream(dev.stream):
+            buf[:nb, :K].copy_(vals[i0:i0 + nb])
+        dev.call("sfft_finish_samples", hptr(tabs.ms), 1, nb, dptr(tabs.chirp), dptr(buf), tabs.P, 0, 0, 0, 0, 0,
+                 ctx=f"line pre-chirp, step {step}")
+        dev.call("sfft_bluestein", hptr(tabs.ms), 1, nb, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
+                 dptr(tabs.chirp), dptr(buf), 0, 0, ctx=f"line DFT, step {step}")
+        dev.call("sfft_line_bins", dptr(buf), tabs.P, nb, K, lo, delta, dptr(coefs[i0:]), dptr(keep[i0:]),
+                 dptr(counts[i0:]), ctx=f"line bins, step {step}")
+    for c0 in range(0, r, 64):
+        rows = np.arange(c0, min(r, c0 + 64), dtype=np.int32)
+        sbytes = int(_native.query("sfft_select_rows_scratch_bytes", len(rows)))
+        scratch = dev.empty((max(sbytes, 1),), torch.uint8)
+        dev.call("sfft_select_cap_rows", dptr(coefs), dptr(keep), K, hptr(rows), len(rows), cap, dptr(counts),
+                 dptr(scratch), ctx=f"line cap, step {step}")
 
 
 def projected_line_coefficients(oracle, t: int, box: SearchBox, anchor: np.ndarray,

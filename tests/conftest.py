@@ -19,3 +19,14 @@ def pytest_configure(config):
 def golden():
     with np.load(GOLDEN) as z:
         return {k: z[k] for k in z.files}
+
+
+GOLDEN_EXT = ROOT / "tests" / "golden" / "golden_ext.npz"
+
+
+@pytest.fixture(scope="session")
+def golden_ext():
+    """Slow reference runs (make_golden.py --ext): retries / partial schemes,
+    config 3 reduced (d = 20, per-call relative noise), config 4 full size."""
+    with np.load(GOLDEN_EXT) as z:
+        return {k: z[k] for k in z.files}

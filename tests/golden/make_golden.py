@@ -222,6 +222,144 @@ def single_fixture(out):
                                      lattice_kind="single"))
 
 
+class _RelNoisy:
+    """Per-call relative noise around a reference oracle (the
+    harness adaptation of testbed.py:76-106 for BASELINE config 3): each call
+    draws ``standard_normal((n, 2))`` from one numpy stream in call order and
+    adds sigma_call / sqrt(2) * (e0 + i e1) with sigma_call = rel * ||p(X)|| / sqrt(n)."""
+
+    def __init__(self, inner, rel, seed):
+        self._inner = inner
+        self.rel = float(rel)
+        self.dim = inner.dim
+        self.concurrency_safe = inner.concurrency_safe
+        self._rng = np.random.default_rng(seed)
+        self._calls = 0
+
+    @property
+    def call_count(self):
+        return self._calls
+
+    def __call__(self, points):
+        values = self._inner(points)
+        n = len(values)
+        noise = self._rng.standard_normal((n, 2)) @ np.array([1.0, 1.0j])
+        self._calls += n
+        sigma = self.rel * np.sqrt(float(np.sum(np.abs(values) ** 2))) / np.sqrt(max(n, 1))
+        return values + (sigma / np.sqrt(2.0)) * noise
+
+
+def _store_run(out, key, rep, truth=None):
+    out[f"{key}_freqs"] = rep.detected.freqs
+    out[f"{key}_coef"] = rep.detected.coeffs
+    out[f"{key}_counts"] = np.array([rep.candidate_counts, rep.prefix_counts, rep.component_counts,
+                                     rep.scheme_sizes, rep.lattice_attempts, rep.inversion_calls])
+    out[f"{key}_calls"] = np.array([rep.oracle_calls])
+    out[f"{key}_warnings"] = np.array(rep.warnings if rep.warnings else [""])
+    if truth is not None:
+        out[f"{key}_err"] = np.array([sfft.relative_spectrum_l2_error(rep.detected, truth)])
+    print(f"{key}: detected {len(rep.detected)} calls {rep.oracle_calls} attempts {rep.lattice_attempts} "
+          f"warnings {rep.warnings} wall {rep.wall_time:.1f}s", flush=True)
+
+
+def retry_fixture(out):
+    """Retries and partial schemes: a first attempt that
+    fails and is recovered by a retry (test_construct.py:178-190), sparse_fft
+    runs whose steps need a second attempt (b = 10) or exhaust b = 1 and
+    omit a candidate with the "covers only" warning (detect.py:385-392,
+    test_detect.py:310-336).  Seeds found by a search over the reference."""
+    rng = np.random.default_rng(19)
+    for trial in range(300):
+        rows = np.unique(rng.integers(-16, 17, size=(64, 4)), axis=0)
+        I = sfft.FrequencyIndexSet(rows)
+        cfg = sfft.MLConfig(c=2.0, gamma=0.5, rng_seed=trial)
+        scheme, attempts = sfft.build_multiple_lattice_with_retries(I, cfg, b=20,
+                                                                    seed_seq=np.random.SeedSequence(trial))
+        if attempts >= 2:
+            assert scheme.is_reconstructing
+            out.update(rt_rows=I.freqs, rt_trial=np.array([trial]), rt_attempts=np.array([attempts]),
+                       rt_ms=np.array([lat.m for lat in scheme.lattices]),
+                       rt_zs=np.stack([lat.z for lat in scheme.lattices]),
+                       rt_masks=pack_masks(scheme.recon_masks))
+            print(f"retry scheme: trial {trial} attempts {attempts} L {len(scheme.lattices)}")
+            break
+    else:
+        raise RuntimeError("no failing first attempt found")
+    for key, seed, b in (("rtrun", 103, 10), ("partial", 955, 1)):
+        truth, _ = sfft.gen_random_sparse_poly(3, 4, 6, "box", seed=np.random.default_rng(1000 + seed))
+        out[f"{key}_hf"], out[f"{key}_hc"] = truth.freqs, truth.coeffs
+        out[f"{key}_cfg"] = np.array([seed, b])
+        rep = sfft.sparse_fft(_poly_signal(truth.freqs, truth.coeffs),
+                              sfft.DetectionConfig(box=sfft.SearchBox.centered(3, 4), delta=1e-12, s=6, r=2, b=b,
+                                                   rng_seed=seed))
+        _store_run(out, key, rep, truth)
+
+
+def long_line_fixture(out):
+    """Component extents K_t > 1024 (lines longer than one CTA's tile):
+    a d = 2 run on [-700, 700]^2 (K = 1401) and projected line coefficients."""
+    truth, _ = sfft.gen_random_sparse_poly(2, 700, 12, "box", seed=np.random.default_rng(71))
+    out.update(ll_hf=truth.freqs, ll_hc=truth.coeffs)
+    rep = sfft.sparse_fft(_poly_signal(truth.freqs, truth.coeffs),
+                          sfft.DetectionConfig(box=sfft.SearchBox.centered(2, 700), delta=1e-12, s=12, r=2, b=10,
+                                               rng_seed=5))
+    _store_run(out, "ll", rep, truth)
+    anchor = np.array([0.37, 0.81])
+    ks, c = sfft.projected_line_coefficients(_poly_signal(truth.freqs, truth.coeffs), 1,
+                                             sfft.SearchBox.centered(2, 700), anchor)
+    out.update(ll_line_anchor=anchor, ll_line_ks=ks, ll_line_c=c)
+
+
+def cfg3_reduced_fixture(out):
+    """BASELINE config 3 (d = 20, [-32, 32]^20, polar coefficients, per-call
+    1e-2 relative noise, delta = 0.1) at reduced sparsity s = 100, r = 2, run
+    by the unmodified reference through the guard-free box."""
+    wl = workloads.config3(seed=0, d=20, s=100, r=2)
+    ts, rs, ns = workloads.seeds_for(0, 3, 0)
+    out.update(c3_hf=wl.truth.freqs, c3_hc=wl.truth.coeffs, c3_seed=np.array([rs], np.uint64))
+    noisy = _RelNoisy(_poly_signal(wl.truth.freqs, wl.truth.coeffs), 1e-2, ns)
+    cfg = sfft.DetectionConfig(box=_BigBox.centered(20, 32), delta=0.1, s=100, r=2, b=10, rng_seed=rs)
+    rep = sfft.sparse_fft(noisy, cfg)
+    _store_run(out, "c3", rep, sfft.SparseSpectrum(wl.truth.freqs, wl.truth.coeffs))
+
+
+def cfg4_full_fixture(out):
+    """BASELINE config 4 at full size (N = 64, s = 2000, r = 5, delta = 1e-6)
+    with the seed-chosen partition (testbed.py:188-265)."""
+    wl = workloads.config4()
+    groups = wl.oracle.groups
+    out["c4_groups"] = np.array([[m] + list(c) + [-1] * (4 - len(c)) for m, c in groups])
+    out["c4_seed"] = np.array([wl.cfg.rng_seed], np.uint64)
+    saved = ref_testbed._BSPLINE_GROUPS
+    ref_testbed._BSPLINE_GROUPS = tuple((int(m), tuple(int(c) for c in comps)) for m, comps in groups)
+    try:
+        cfg = sfft.DetectionConfig(box=_BigBox.centered(10, 64), delta=1e-6, s=2000, r=5, b=10,
+                                   rng_seed=wl.cfg.rng_seed)
+        rep = sfft.sparse_fft(sfft.bspline_test_function(), cfg)
+        _store_run(out, "c4", rep)
+        out["c4_l2err"] = np.array([sfft.relative_l2_error(rep.detected, sfft.bspline_exact_coefficients,
+                                                           sfft.bspline_norm_sq())])
+        print("c4 l2 err", out["c4_l2err"][0])
+    finally:
+        ref_testbed._BSPLINE_GROUPS = saved
+
+
+def main_ext(which):
+    """Slow fixtures (minutes of reference CPU time) in golden_ext.npz;
+    ``which`` selects the ones to (re)generate, the others are kept."""
+    path = HERE / "golden_ext.npz"
+    out: dict = dict(np.load(path)) if path.exists() else {}
+    fns = {"retry": retry_fixture, "cfg3": cfg3_reduced_fixture, "cfg4": cfg4_full_fixture,
+           "longline": long_line_fixture}
+    for name in which or list(fns):
+        prefix = {"retry": ("rt_", "rtrun_", "partial_"), "cfg3": ("c3_",), "cfg4": ("c4_",),
+                  "longline": ("ll_",)}[name]
+        out = {k: v for k, v in out.items() if not k.startswith(prefix)}
+        fns[name](out)
+        np.savez_compressed(path, **out)
+    print("wrote", path, sum(v.nbytes for v in out.values()), "bytes raw")
+
+
 def main():
     out: dict = {}
     single_fixture(out)
@@ -236,4 +374,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--ext" in sys.argv:
+        main_ext([a for a in sys.argv[1:] if not a.startswith("--")])
+    else:
+        main()

@@ -168,3 +168,65 @@ def test_engine_bspline(golden):
     diff = got ^ ref
     assert len(diff) <= 4
     assert len(rep.freqs) == len(golden["bs_freqs"])
+
+
+# ---------------------------------------------------------------------------
+# extended reference runs (golden_ext.npz, make_golden.py --ext)
+
+def test_retry_scheme(golden_ext):
+    """A first attempt that fails, recovered by the retry (construct.py:185-206,
+    test_construct.py:178-190)."""
+    g = golden_ext
+    sch = O.build_with_retries(g["rt_rows"], 20, np.random.SeedSequence(int(g["rt_trial"][0])))
+    assert sch.attempts == int(g["rt_attempts"][0]) >= 2
+    assert sch.ms == g["rt_ms"].tolist()
+    assert np.array_equal(np.stack(sch.zs), g["rt_zs"])
+    words = np.zeros(len(g["rt_rows"]), dtype=np.uint64)
+    for l, mk in enumerate(sch.masks):
+        words |= mk.astype(np.uint64) << np.uint64(l)
+    assert np.array_equal(words, g["rt_masks"])
+
+
+def test_engine_retry_and_partial_runs(golden_ext):
+    """sparse_fft with a step that needs a second attempt (b = 10) and with a
+    step whose b = 1 attempt leaves candidates uncovered (detect.py:385-392)."""
+    for key in ("rtrun", "partial"):
+        f, c = golden_ext[f"{key}_hf"], golden_ext[f"{key}_hc"]
+        seed, b = (int(x) for x in golden_ext[f"{key}_cfg"])
+        rep = O.sparse_fft(lambda p: O.poly_eval(f, c, p), [-4] * 3, [4] * 3, 1e-12, 6, r=2, b=b, rng_seed=seed)
+        _check_run(golden_ext, key, rep)
+    assert max(golden_ext["rtrun_counts"][4]) >= 2
+    assert "covers only" in str(golden_ext["partial_warnings"][0])
+    assert len(golden_ext["partial_freqs"]) < len(golden_ext["partial_hf"])
+
+
+def test_engine_config3_reduced(golden_ext):
+    """BASELINE config 3 at reduced sparsity (d = 20, s = 100, r = 2, delta =
+    0.1) with per-call relative noise 1e-2 drawn in the reference call order."""
+    from paper_1711_05152_b200 import workloads
+    g = golden_ext
+    f, c = g["c3_hf"], g["c3_hc"]
+    _, rs, ns = workloads.seeds_for(0, 3, 0)
+    assert rs == int(g["c3_seed"][0])
+    rng = np.random.default_rng(ns)
+
+    def noisy(p):
+        v = O.poly_eval(f, c, p)
+        e = rng.standard_normal((len(p), 2)) @ np.array([1.0, 1.0j])
+        sigma = 1e-2 * np.sqrt(float(np.sum(np.abs(v) ** 2))) / np.sqrt(len(p))
+        return v + sigma / np.sqrt(2.0) * e
+
+    rep = O.sparse_fft(noisy, [-32] * 20, [32] * 20, 0.1, 100, r=2, b=10, rng_seed=rs)
+    _check_run(g, "c3", rep)
+
+
+def test_engine_long_lines(golden_ext):
+    """Component extent K = 1401 > 1024 (reference run on [-700, 700]^2)."""
+    g = golden_ext
+    f, c = g["ll_hf"], g["ll_hc"]
+    fn = lambda p: O.poly_eval(f, c, p)
+    rep = O.sparse_fft(fn, [-700] * 2, [700] * 2, 1e-12, 12, r=2, b=10, rng_seed=5)
+    _check_run(g, "ll", rep)
+    ks, got = O.line_coefficients(fn, 1, [-700] * 2, [700] * 2, g["ll_line_anchor"])
+    assert np.array_equal(ks, g["ll_line_ks"])
+    assert np.abs(got - g["ll_line_c"]).max() <= 1e-12
