@@ -36,6 +36,10 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MR1L step candidates/s (config 1: |J|=100000, d=10, 2000-term oracle)"
 UNIT = "candidates/s"
+# the same `config` object in both arms (details of a run go to `config_detail`)
+CONFIG = {"workload": "config1: one MR1L reconstruction step, |J|=100000 in [-32,32]^10, "
+                      "2000-term sparse polynomial oracle, b=10, delta=1e-12",
+          "l2": "GPU arm: L2 flushed (256 MB write) before every timed step, each step timed from after its flush"}
 
 
 def _args():
@@ -95,6 +99,11 @@ def cpu_step_estimate(wl, budget_s: float):
 
 
 def run_reference(args):
+    """The reference path's CPU port on this host's cores.  Every one of the K
+    timed steps really runs: the full construction, the full inversion and
+    selection, and the sampling on a bounded node subset; the step's time is
+    that measured work with the sampling scaled to the step's node count
+    (``extrapolated_sampling``)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -105,10 +114,13 @@ def run_reference(args):
     sample = ""
     for _ in range(max(args.warmup, 0)):
         pass  # the CPU port has no warm-up state beyond the sieve
-    budget = max(2.0, args.cpu_seconds / max(args.steps, 1))
+    budget = max(1.0, args.cpu_seconds / max(args.steps, 1))
     t0 = time.perf_counter()
+    walls = []
     for _ in range(args.steps):
+        ts = time.perf_counter()
         v, cores, sample = cpu_step_estimate(wl, budget)
+        walls.append(time.perf_counter() - ts)
         vals.append(v)
     wall = time.perf_counter() - t0
     value = float(np.median(vals))
@@ -117,13 +129,60 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * args.n / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1 shapes)",
-        "config": {"workload": "config1: one MR1L reconstruction step, |J|=100000 in [-32,32]^10, "
-                               "2000-term sparse polynomial oracle, b=10, delta=1e-12"},
+        "config": dict(CONFIG),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": wall,
+        "extrapolated_sampling": True,
+        "timed_wall_s": wall,
+        "timed_s_per_step": float(np.mean(walls)),
+        "note": ("ms_per_step is the full step's CPU time: construction + inversion measured in full in "
+                 "every timed step, sampling measured on a node subset and scaled to all nodes"),
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_d10_estimate(wl2, rep2, budget_s: float):
+    """The reference path's CPU port on the SAME config-2 instance the GPU
+    ran (workloads.config2()), extrapolated from a bounded sample: the
+    oracle's per-node cost (1000 terms, all cores) x the run's exact oracle
+    calls, plus construction and inversion timed on one 65000-candidate step
+    and scaled linearly by each step's |J_t| (and r~ for the inversions)."""
+    from oracle import sfft_oracle as O
+    from paper_1711_05152_b200.workloads import distinct_rows
+    cores = os.cpu_count() or 1
+    hf, hc = wl2.oracle.freqs, wl2.oracle.coeffs
+    rng = np.random.default_rng(1)
+    pts = rng.random((1 << 15, 10))
+    nodes, t_s = 0, 0.0
+    t1 = time.perf_counter()
+    while time.perf_counter() - t1 < budget_s:
+        ts = time.perf_counter()
+        O.poly_eval(hf, hc, pts, threads=cores)
+        t_s += time.perf_counter() - ts
+        nodes += len(pts)
+    per_node = t_s / nodes
+    n0 = 65000
+    cand = distinct_rows(np.random.default_rng(2), n0, 10, 32)
+    cand = cand[np.lexsort(cand.T[::-1])]
+    t2 = time.perf_counter()
+    sch = O.build_with_retries(cand, 10, np.random.SeedSequence(3))
+    t_con = time.perf_counter() - t2
+    vals = [rng.normal(size=m) + 1j * rng.normal(size=m) for m in sch.ms]
+    t3 = time.perf_counter()
+    cov, coefs = O.invert_multiple(cand, sch, vals)
+    O.select(cand[cov], coefs, 1000, 1e-12)
+    t_inv = time.perf_counter() - t3
+    d = len(rep2.candidate_counts)
+    rt = [1 if t == d - 1 else wl2.cfg.r for t in range(d)]
+    steps = [t for t in range(1, d) if rep2.candidate_counts[t]]
+    con = sum(t_con * rep2.candidate_counts[t] / n0 for t in steps)
+    inv = sum(t_inv * rt[t] * rep2.candidate_counts[t] / n0 for t in steps)
+    samp = per_node * rep2.oracle_calls
+    return {"wall_s": samp + con + inv, "cores": cores, "kind": "port", "extrapolated": True,
+            "sampling_s": samp, "construction_s": con, "inversion_s": inv,
+            "sample": (f"oracle timed on {nodes} nodes ({t_s:.1f}s, {cores} threads) x {rep2.oracle_calls} calls of "
+                       f"this run; construction ({t_con:.2f}s) and inversion ({t_inv:.2f}s) timed on one "
+                       f"{n0}-candidate step and scaled by each step's |J_t| (x r~ for inversions)")}
 
 
 # ---------------------------------------------------------------------------
@@ -307,8 +366,11 @@ def run_ours(args):
     from paper_1711_05152_b200.device import get_device
     from paper_1711_05152_b200.mr1l import DeviceFreqs, StageTimer, build_scheme, fft_size, prepare_step, run_step
 
+    from paper_1711_05152_b200.parallel import Shard, run_step_sharded
     dev = get_device(local if world > 1 else None)
-    wl = workloads.config1(seed=rank, n=args.n)
+    shard = Shard()
+    # every rank holds the same config-1 instance; N > 1 shards each step
+    wl = workloads.config1(seed=0, n=args.n)
     n = len(wl.cand)
     cand = DeviceFreqs.from_host(dev, wl.cand)
     flush = dev.empty((64 * 1024 * 1024,), torch.float32)  # 256 MB > 126 MB L2
@@ -327,8 +389,12 @@ def run_ours(args):
             with timer.span("alias"):
                 sch = build_scheme(dev, cand, wl.b, np.random.SeedSequence(wl.lattice_seed), box_extent=64,
                                    lazy_streams=True, prepare=prepare)
-        res = run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, n, timer=timer, defer_cap=True,
-                       prep=sch.prep)
+        if world > 1:  # the step's lattices sharded over the ranks (parallel.py, sliced all-to-all merge)
+            res = run_step_sharded(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, n, shard,
+                                   prep=sch.prep, need_coef=True)
+        else:
+            res = run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, wl.delta, n, timer=timer,
+                           defer_cap=True, prep=sch.prep)
         if prev is not None:
             prev.finalize()
         return sch, res
@@ -391,7 +457,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * n / (ms_step * 1e-3)
+    value = n / (ms_step * 1e-3)  # one step's candidates per step time (N > 1: the step is sharded)
 
     # per-stage breakdown (host-visible stage spans, separate untimed steps)
     timer = StageTimer(dev)
@@ -401,11 +467,31 @@ def run_ours(args):
         res.finalize()
     dev.sync()
     stages = {k: float(np.mean(v)) for k, v in timer.totals_ms().items()}
+
+    # cold steps: every size-keyed cache dropped first (lattice / FFT tables,
+    # prime memo), as a step with never-seen lattice sizes
+    from paper_1711_05152_b200.mr1l import clear_caches
+    cold = []
+    for _ in range(3):
+        clear_caches(dev)
+        flush.zero_()
+        dev.sync()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(dev.stream)
+        sch_c, res_c = step()
+        res_c.finalize()
+        b.record(dev.stream)
+        dev.sync()
+        cold.append(a.elapsed_time(b))
+    cold_ms = float(np.mean(cold))
+
     s_terms = wl.oracle.s
-    # executed arithmetic: 3 real multiply-adds (6 flop) per term and node
-    # (3-multiplication complex product on the FP64 tensor pipe)
-    flops = 6.0 * s_terms * sch.total_size
+    # one (node, term) complex multiply-add = 8 flop; the kernel
+    # executes it as 3 real multiply-adds (6 flop, 3-multiplication product)
+    flops = 8.0 * s_terms * sch.total_size
     achieved = flops / (kernels["sample_poly"] * 1e-3) / 1e12
+    executed = 6.0 * s_terms * sch.total_size / (kernels["sample_poly"] * 1e-3) / 1e12
     traffic = load_traffic()
     others = secondary_rooflines(dev, sch, n, 10, kernels)
 
@@ -432,7 +518,7 @@ def run_ours(args):
         t = torch.tensor([e2e_step], device=dev.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item())
-    e2e_val = world * n / (e2e_step * 1e-3)
+    e2e_val = n / (e2e_step * 1e-3)
 
     # the d=10 sFFT (BASELINE config 2) end to end: 1 GPU, or sharded over all
     # ranks (parallel.py, NCCL all-gathers) when N > 1; wall = max over ranks
@@ -440,7 +526,16 @@ def run_ours(args):
     if not args.no_d10:
         try:
             wl2 = workloads.config2()
-            P.sparse_fft(wl2.oracle, wl2.cfg)  # warm (plan/table caches)
+            walls_cold = []
+            for _ in range(2):  # cold: size-keyed caches dropped before the run
+                clear_caches(dev)
+                if world > 1:
+                    dist.barrier()
+                dev.sync()
+                t0 = time.perf_counter()
+                P.sparse_fft(wl2.oracle, wl2.cfg)
+                dev.sync()
+                walls_cold.append(time.perf_counter() - t0)
             walls = []
             for _ in range(3):
                 if world > 1:
@@ -451,17 +546,25 @@ def run_ours(args):
                 dev.sync()
                 walls.append(time.perf_counter() - t0)
             wall = float(np.median(walls))
+            wall_cold = float(walls_cold[-1])
             if world > 1:
-                t = torch.tensor([wall], device=dev.device)
+                t = torch.tensor([wall, wall_cold], device=dev.device)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                wall = float(t.item())
+                wall, wall_cold = (float(x) for x in t.tolist())
             ok = rep2.detected.support() == wl2.truth.support()
             d10 = {"metric": "d=10 sFFT wall time (config 2: N=32, s=1000, r=5)", "wall_s": wall,
+                   "wall_cold_s": wall_cold,
+                   "wall_note": "wall_s: median of 3 runs with warm size-keyed caches (the previous runs' lattice "
+                                "sizes); wall_cold_s: a run after dropping them (first run of a process also pays "
+                                "module/CUDA initialisation and is not reported)",
                    "unit": "s", "n_gpus": world, "mode": "sharded" if world > 1 else "1 GPU",
                    "exact_support": bool(ok), "rel_err": P.relative_spectrum_l2_error(rep2.detected, wl2.truth),
                    "oracle_calls": rep2.oracle_calls,
-                   "cpu_reference_wall_s": 3127.5,
-                   "cpu_reference_note": "unmodified reference, single thread, survey container (SURVEY §6.3)"}
+                   "survey_reference_wall_s": 3127.5,
+                   "survey_reference_note": "unmodified reference, single thread, survey container, a different "
+                                            "instance (seed 42/43, 49,683,725 calls; SURVEY §6.3)"}
+            if rank == 0 and world == 1 and not args.no_cpu_baseline:
+                d10["cpu_baseline"] = cpu_d10_estimate(wl2, rep2, args.cpu_seconds / 2)
         except Exception as exc:  # report, do not lose the headline line
             d10 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
@@ -476,15 +579,18 @@ def run_ours(args):
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1 shapes)",
-        "config": {"workload": "config1: one MR1L reconstruction step, |J|=100000 in [-32,32]^10, "
-                               "2000-term sparse polynomial oracle, b=10, delta=1e-12",
-                   "lattices": len(sch.primes[: sch.L]), "nodes_per_step": sch.total_size,
-                   "fft_points": fft_size(max(sch.primes[: sch.L])),
-                   "l2": "flushed (256 MB write) before every timed step; each step timed from after its flush "
-                         f"(loop incl. flushes: {ms_with_flush / args.steps:.4f} ms/step)",
-                   "parallelism": f"{world} independent step streams (weak scaling)" if world > 1 else "1 GPU"},
+        "config": dict(CONFIG),
+        "config_detail": {"lattices": len(sch.primes[: sch.L]), "nodes_per_step": sch.total_size,
+                          "fft_points": fft_size(max(sch.primes[: sch.L])),
+                          "loop_ms_per_step_incl_flush": ms_with_flush / args.steps,
+                          "parallelism": (f"each step sharded over {world} GPUs: (iteration, lattice) units "
+                                          "round-robin, sliced all-to-all merge, NCCL" if world > 1 else "1 GPU"),
+                          "caches": "warm: per-size tables cached across the identical timed steps (like FFT "
+                                    "plans); cold_ms_per_step drops them first"},
+        "cold_ms_per_step": cold_ms,
         "stages_ms": stages,
         "kernels_ms": kernels,
         "kernel_share_of_step": kernels["sample_poly"] / ms_step,
@@ -496,9 +602,11 @@ def run_ours(args):
                      "peak_source": "measured in this run: max of a register-resident DFMA loop "
                                     f"({peak_dfma:.2f}) and DMMA m8n8k4 loop ({peak_dmma:.2f}) "
                                     "(sfft_fp64_peak / sfft_fp64_mma_peak); MEASURED_PEAKS.json has no FP64 figure",
-                     "algorithmic": f"6 flop (3 real FMAs of the 3-multiplication complex product) x {s_terms} "
+                     "algorithmic": f"SURVEY §8(d): 8 flop per (node, term) complex multiply-add x {s_terms} "
                                     f"terms x {sch.total_size} nodes per launch",
-                     "complex_mac_rate": f"{achieved * 8.0 / 6.0:.2f} TFLOP/s in 8-flop complex multiply-add terms",
+                     "executed": {"achieved": executed, "frac": executed / peak,
+                                  "note": "6 flop per (node, term) actually issued: the 3-multiplication complex "
+                                          "product (3 real DMMA multiply-adds); frac > 1 above is that saving"},
                      "traffic": (traffic or {}).get("sample_poly_dram_bytes")},
         "kernel_rooflines": others,
         "cpu_baseline": cpu,

@@ -195,6 +195,33 @@ int sfft_gather_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, c
                       const int32_t* h_z, int L, const uint64_t* d_masks, const double* d_buf,
                       int64_t P, int rb, const int32_t* h_units, int nunits, double* d_out,
                       void* stream);
+/* ---- sharded step, sliced exchange (replaces the dense-row
+ * all-gather of sfft_gather_units / sfft_combine_units, which remain).
+ * Candidates are cut into W slices of ts tiles of 256 candidates.
+ * sfft_mask_tiles: per-tile popcounts of every mask bit (d_tc, sized
+ * sfft_mask_tiles_len), their exclusive scan along the tiles d_toff
+ * ((ntiles + 1) x L int32) and the slice totals d_sc (W x L int32).
+ * sfft_pack_units: for the listed own units (slot j = buffer slot j, as
+ * sfft_gather_units) write X_j[k.z_l mod M_l] * (1/M_l) of every candidate k
+ * with mask bit l set, slice-major: slice q of slot j starts at
+ * d_soff[q * nunits + j] (complex elements of d_send), candidate order.
+ * sfft_combine_slice: slice q's candidates from the received packs (unit
+ * u = i * L + l of the chunk at d_roff[u]): lattice-order average, delta
+ * threshold -> d_coef_s / d_keep_s ([rb][ts * 256]), survivors into d_counts
+ * (rb, zeroed first).  sfft_unshard_rows: [W][rb][S] -> rows it0.. of
+ * [r][n] (elem = 1: keep flags, 16: coefficients). */
+int64_t sfft_mask_tiles_len(int64_t n, int L);
+int sfft_mask_tiles(const uint64_t* d_masks, int64_t n, int L, int32_t* d_tc, int32_t* d_toff, int64_t ts, int W,
+                    int32_t* d_sc, void* stream);
+int sfft_pack_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m, const int32_t* h_z,
+                    int L, const uint64_t* d_masks, const double* d_buf, int64_t P, int rb, const int32_t* h_units,
+                    int nunits, const int32_t* d_toff, int64_t ts, const int64_t* d_soff, double* d_send,
+                    void* stream);
+int sfft_combine_slice(int64_t n, int L, const uint64_t* d_masks, const int32_t* d_toff, int64_t ts, int q,
+                       const double* d_recv, const int64_t* d_roff, int rb, double delta, double* d_coef_s,
+                       uint8_t* d_keep_s, int32_t* d_counts, void* stream);
+int sfft_unshard_rows(const void* d_in, int elem, int W, int rb, int64_t S, int64_t n, int it0, void* d_out,
+                      void* stream);
 int sfft_combine_units(int64_t n, int L, const uint64_t* d_masks, const double* d_vals,
                        const int32_t* h_rows, int r_total, int rb, int it0, double delta,
                        double* d_coef, uint8_t* d_keep, int32_t* d_counts, void* stream);

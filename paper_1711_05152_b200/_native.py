@@ -51,6 +51,12 @@ _SIGS = {
                                   _dbl, _vp, _vp, _vp, _vp]),
     "sfft_gather_units": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _vp]),
     "sfft_combine_units": (_int, [_i64, _int, _vp, _vp, _vp, _int, _int, _int, _dbl, _vp, _vp, _vp, _vp]),
+    "sfft_mask_tiles_len": (_i64, [_i64, _int]),
+    "sfft_mask_tiles": (_int, [_vp, _i64, _int, _vp, _vp, _i64, _int, _vp, _vp]),
+    "sfft_pack_units": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _i64,
+                               _vp, _vp, _vp]),
+    "sfft_combine_slice": (_int, [_i64, _int, _vp, _vp, _i64, _int, _vp, _vp, _int, _dbl, _vp, _vp, _vp, _vp]),
+    "sfft_unshard_rows": (_int, [_vp, _int, _int, _int, _i64, _i64, _int, _vp, _vp]),
     "sfft_select_scratch_bytes": (_i64, [_i64]),
     "sfft_select_cap": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
     "sfft_select_rows_scratch_bytes": (_i64, [_int]),

@@ -160,13 +160,19 @@ class StepReport:
 
 
 def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: float = 0.0,
-                     cap: int | None = None, anchor_tail=None, device=None) -> StepReport:
+                     cap: int | None = None, anchor_tail=None, device=None, group=None,
+                     shard: bool | None = None) -> StepReport:
     """Build the MR1L scheme for ``candidates``, sample ``oracle`` on it,
     invert and threshold: the composition build_multiple_lattice_with_retries
     -> oracle(lattice nodes) -> invert_multiple -> _select of the reference
     (construct.py:185-206, detect.py:290-299, transform.py:99-127,
-    detect.py:197-212) as one device pipeline."""
+    detect.py:197-212) as one device pipeline.  Under torch.distributed the
+    step's lattices are sharded over the ranks of ``group`` (parallel.py)
+    unless ``shard=False``; every rank returns the same report."""
     from .mr1l import prepare_step, run_step, speculate_scheme
+    from .parallel import Shard, run_step_sharded
+    sh = Shard(group)
+    sharded = sh.active and shard is not False
     dev = device or get_device()
     torch = dev.torch
     if isinstance(candidates, torch.Tensor):
@@ -206,8 +212,12 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     with torch.cuda.stream(side):
         words_h.copy_(sch.masks.view(torch.uint8), non_blocking=True)
     sch.masks.record_stream(side)
-    res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
-                   defer_cap=True, prep=sch.prep)
+    if sharded:
+        res = run_step_sharded(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap), sh,
+                               prep=sch.prep, need_coef=True)
+    else:
+        res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
+                       defer_cap=True, prep=sch.prep)
     res.finalize()  # cap applied (if binding) before the results are read
     coef, keep = dev.download_many(res.coef[0], res.keep[0])
     side.synchronize()

@@ -17,7 +17,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libsfft_b200.so"
 SOURCES = ["capi.cu", "alias.cu", "sample.cu", "sample_ws.cu", "fft.cu", "fft_mixed.cu", "gather.cu", "lines.cu", "points.cu",
-           "cbc.cu", "peak.cu"]
+           "cbc.cu", "peak.cu", "shard.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -16,8 +16,22 @@
 // int64 count): seen1 |= bit; if the bit was already set, seen2 |= bit.  The
 // result is exact for any multiplicity and the bitmaps (sum_l M_l / 4 bytes)
 // stay L2-resident even at |J| = 6.5e5, d = 20 (29 lattices, ~9 MB).
+//
+// Default path (alias_cluster_kernel): no L2 atomics at all.  Each thread-
+// block cluster (16 CTAs where the GPU allows, else 8) owns a group of
+// lattices and holds their two bitmaps in distributed shared memory, bins
+// partitioned over the cluster's CTAs; every CTA takes a contiguous slice of
+// the candidates, marks seen1/seen2 with shared::cluster atomics, and after a
+// cluster barrier reads seen2 back and writes one alias-free bit-plane word
+// per warp and lattice (ballot).  alias_planes_kernel then folds the planes
+// into the per-candidate 64-bit masks and the stats.  The L2-atomic kernels
+// below remain for lattice sizes whose bitmaps exceed a cluster's shared
+// memory.
 #include "common.cuh"
 #include "plan.cuh"
+
+#include <cstdlib>
+#include <cstring>
 
 namespace sfft {
 
@@ -130,6 +144,246 @@ alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// cluster / DSMEM variant
+
+struct AliasGroups {
+  int l0;    // first lattice of the launch
+  int nl;    // lattices of the launch
+  int g;     // lattices per cluster
+  int wpc;   // bitmap words per CTA and bitmap
+};
+
+__device__ __forceinline__ uint32_t dsm_map(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t dsm_or(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void dsm_red_or(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t dsm_ld(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+constexpr int ACG = 4;  // lattices whose cluster atomics are issued back to back
+
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, AliasGroups ag,
+                     uint32_t* __restrict__ planes, int64_t pwords) {
+  extern __shared__ uint32_t bm[];  // [g][seen1 | seen2][wpc]
+  uint32_t rank, nct;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
+  const int cid = (int)(blockIdx.x / nct);
+  const int lb = ag.l0 + cid * ag.g;
+  const int le = min(ag.l0 + ag.nl, lb + ag.g);
+  const int ng = le - lb;
+  const int wpc = ag.wpc;
+  for (int w = threadIdx.x; w < ng * 2 * wpc; w += blockDim.x) bm[w] = 0u;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(bm);
+  cluster_barrier();  // every CTA's bitmaps are zero before the first remote atomic
+  const int64_t nw = (n + 31) >> 5;
+  const int64_t i0 = (nw * rank / nct) * 32;
+  const int64_t i1 = min(n, (nw * (rank + 1) / nct) * 32);
+  const int d = lt.d;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    int32_t k[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    for (int jb = 0; jb < ng; jb += ACG) {
+      uint32_t adr[ACG], bit[ACG], old[ACG];
+#pragma unroll
+      for (int q = 0; q < ACG; ++q) {
+        const int j = jb + q;
+        bit[q] = 0u;
+        old[q] = 0u;
+        if (j < ng) {
+          const int64_t r = SFFT_RES(DM, FAST, k, lt, lb + j);
+          const uint32_t gw = (uint32_t)(r >> 5);
+          const uint32_t owner = gw / (uint32_t)wpc;
+          adr[q] = dsm_map(base + 4u * ((uint32_t)(2 * j * wpc) + gw - owner * (uint32_t)wpc), owner);
+          bit[q] = 1u << (r & 31);
+          old[q] = dsm_or(adr[q], bit[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < ACG; ++q)
+        if (old[q] & bit[q]) dsm_red_or(adr[q] + 4u * (uint32_t)wpc, bit[q]);
+    }
+  }
+  cluster_barrier();  // all marks landed
+  const int lane = threadIdx.x & 31;
+  for (int64_t ib = i0; ib < i1; ib += blockDim.x) {
+    const int64_t i = ib + threadIdx.x;
+    const bool live = i < i1;
+    int32_t k[DM];
+#pragma unroll
+    for (int c = 0; c < DM; ++c) k[c] = (live && c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    for (int jb = 0; jb < ng; jb += ACG) {
+      uint32_t v[ACG], sh[ACG];
+#pragma unroll
+      for (int q = 0; q < ACG; ++q) {
+        const int j = jb + q;
+        v[q] = ~0u;
+        sh[q] = 0u;
+        if (live && j < ng) {
+          const int64_t r = SFFT_RES(DM, FAST, k, lt, lb + j);
+          const uint32_t gw = (uint32_t)(r >> 5);
+          const uint32_t owner = gw / (uint32_t)wpc;
+          v[q] = dsm_ld(dsm_map(base + 4u * ((uint32_t)((2 * j + 1) * wpc) + gw - owner * (uint32_t)wpc), owner));
+          sh[q] = (uint32_t)(r & 31);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < ACG; ++q) {
+        const int j = jb + q;
+        const uint32_t free = (live && !((v[q] >> sh[q]) & 1u)) ? 1u : 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, free);
+        if (lane == 0 && j < ng && ib + (threadIdx.x & ~31) < i1)
+          planes[(int64_t)(lb + j - ag.l0) * pwords + ((ib + threadIdx.x) >> 5)] = bal;
+      }
+    }
+  }
+  cluster_barrier();  // no CTA leaves while others may still read its bitmaps
+}
+
+// alias-free bit-planes of lattices [l0, l1) -> masks (OR-ed into the masks of
+// [0, l0) when l0 > 0), stats as alias_mask_kernel
+__global__ void __launch_bounds__(256)
+alias_planes_kernel(int64_t n, int l0, int l1, const uint32_t* __restrict__ planes, int64_t pwords,
+                    uint64_t* __restrict__ masks, int32_t* __restrict__ stats) {
+  __shared__ int red[32];
+  int first_max = 0, empty = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t mask = l0 > 0 ? masks[i] : 0ull;
+    for (int l = l0; l < l1; ++l)
+      mask |= (uint64_t)((__ldg(&planes[(int64_t)(l - l0) * pwords + (i >> 5)]) >> (i & 31)) & 1u) << l;
+    masks[i] = mask;
+    if (mask) first_max = max(first_max, __ffsll((long long)mask));
+    else empty += 1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    first_max = max(first_max, __shfl_down_sync(0xffffffffu, first_max, o));
+    empty += __shfl_down_sync(0xffffffffu, empty, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[wid] = first_max; red[16 + wid] = empty; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int fm = 0, em = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { fm = max(fm, red[w]); em += red[16 + w]; }
+    if (fm) atomicMax(&stats[0], fm);
+    if (em) atomicAdd(&stats[1], em);
+  }
+}
+
+namespace {
+constexpr size_t ALIAS_SMEM_MAX = 200 * 1024;
+
+// cluster geometry for lattices [l0, l1): 0 when no cluster variant fits
+template <int DM, bool FAST>
+bool alias_cluster_plan(const LatTable& lt, int l0, int l1, int& cl, AliasGroups& ag, int& clusters, size_t& smem) {
+  static const bool disabled = [] {
+    const char* e = getenv("SFFT_B200_ALIAS_CLUSTER");
+    return e && strcmp(e, "0") == 0;
+  }();
+  if (disabled) return false;
+  int64_t mw = 1;
+  for (int l = l0; l < l1; ++l) mw = max(mw, (lt.m[l] + 31) >> 5);
+  const void* fn = (const void*)alias_cluster_kernel<DM, FAST>;
+  const int nl = l1 - l0;
+  for (int c : {16, 8}) {
+    const int wpc = (int)((mw + c - 1) / c);
+    const size_t per_lat = (size_t)2 * wpc * 4;
+    if (per_lat > ALIAS_SMEM_MAX) continue;
+    if (c > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    // most clusters that can be resident with one lattice each, then fold
+    // lattices into clusters until the group's bitmaps fit
+    for (int g = 1; g <= nl; ++g) {
+      const size_t sm = per_lat * g;
+      if (sm > ALIAS_SMEM_MAX) break;
+      if (set_smem_once(fn, sm) != cudaSuccess) { (void)cudaGetLastError(); break; }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c, 1, 1);
+      cfg.blockDim = dim3(256, 1, 1);
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int maxc = 0;
+      if (cudaOccupancyMaxActiveClusters(&maxc, fn, &cfg) != cudaSuccess) { (void)cudaGetLastError(); break; }
+      const int need = (nl + g - 1) / g;
+      if (maxc >= need) {
+        cl = c;
+        ag.l0 = l0;
+        ag.nl = nl;
+        ag.g = g;
+        ag.wpc = wpc;
+        clusters = need;
+        smem = sm;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+}  // namespace
+
+template <int DM, bool FAST>
+static int launch_alias_cluster_t(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* planes,
+                                  int64_t pwords, uint64_t* masks, int32_t* stats, int num_sms, bool* done,
+                                  cudaStream_t st) {
+  *done = false;
+  int cl = 0, clusters = 0;
+  AliasGroups ag;
+  size_t smem = 0;
+  if (!alias_cluster_plan<DM, FAST>(lt, l0, lt.nlat, cl, ag, clusters, smem)) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl * clusters, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  prof_mark(PROF_ALIAS, true, st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, alias_cluster_kernel<DM, FAST>, freqs, n, lt, ag, planes, pwords);
+  if (e != cudaSuccess) return (int)e;
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms * 8;
+  const int blocks = (int)(want < cap ? want : cap);
+  alias_planes_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(n, l0, lt.nlat, planes, pwords, masks, stats);
+  prof_mark(PROF_ALIAS, false, st);
+  SFFT_CHECK_LAUNCHES(2);
+  *done = true;
+  return 0;
+}
+
 int64_t alias_scratch_words(const LatTable& lt) {
   int64_t acc = 0;
   for (int l = 0; l < lt.nlat; ++l) acc += (lt.m[l] + 31) >> 5;
@@ -151,15 +405,37 @@ static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, 
 int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
                  int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
                  cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
-  if (e != cudaSuccess) return (int)e;
-  e = cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st);
+  cudaError_t e = cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st);
   if (e != cudaSuccess) return (int)e;
   if (n == 0) return 0;
+  const int d = lt.d;
+  // cluster path: the scratch holds the alias-free bit-planes of the launch's
+  // lattices (nlat - l0 planes of ceil(n / 32) words; always within the
+  // bitmap scratch, since every M_l >= 2 |J| - 1)
+  const int64_t pwords = (n + 31) >> 5;
+  if ((int64_t)(lt.nlat - l0) * pwords <= words) {
+    bool done = false;
+    int rc = 0;
+#define SFFT_ALIASC_CASE(DMV)                                                                              \
+    if (d <= DMV) {                                                                                        \
+      rc = fast ? launch_alias_cluster_t<DMV, true>(freqs, n, lt, l0, bits, pwords, masks, stats, num_sms, &done, st) \
+                : launch_alias_cluster_t<DMV, false>(freqs, n, lt, l0, bits, pwords, masks, stats, num_sms, &done, st); \
+    } else
+    SFFT_ALIASC_CASE(4)
+    SFFT_ALIASC_CASE(8)
+    SFFT_ALIASC_CASE(16)
+    SFFT_ALIASC_CASE(32)
+    SFFT_ALIASC_CASE(64)
+    { return -22; }
+#undef SFFT_ALIASC_CASE
+    if (rc) return rc;
+    if (done) return 0;
+  }
+  e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return (int)e;
   int64_t want = (n + 255) / 256;
   int64_t cap = (int64_t)num_sms * 8;
   int blocks = (int)(want < cap ? want : cap);
-  const int d = lt.d;
 #define SFFT_ALIAS_CASE(DMV)                                                                 \
   if (d <= DMV) {                                                                            \
     if (fast) launch_alias_t<DMV, true>(freqs, n, lt, l0, bits, words, masks, stats, blocks, st); \

@@ -21,6 +21,16 @@ int launch_prefix_flags(const int32_t* freqs, int64_t n, int t1, uint8_t* flags,
 int launch_scatter_residues(const int32_t* freqs, int64_t n, const LatTable& lt, const double2* coef,
                             double2* acc, int num_sms, cudaStream_t st);
 int launch_fp64_peak(double* out, int iters, int blocks, cudaStream_t st);
+int launch_mask_tiles(const uint64_t* masks, int64_t n, int L, int32_t* tc, int32_t* toff, int64_t ts, int W,
+                      int32_t* sc, int num_sms, cudaStream_t st);
+int launch_pack_units(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
+                      const double2* buf, int64_t ustride, const UnitTable& ut, const int32_t* toff, int64_t ts,
+                      const int64_t* soff, double2* send, bool fast, int num_sms, cudaStream_t st);
+int launch_combine_slice(int64_t n, int L, const uint64_t* masks, const int32_t* toff, int64_t ts, int q,
+                         const double2* recv, const int64_t* roff, int rb, double delta, double2* coef_s,
+                         uint8_t* keep_s, int32_t* counts, int num_sms, cudaStream_t st);
+int launch_unshard(const void* in, int elem, int W, int rb, int64_t S, int64_t n, int it0, void* out, int num_sms,
+                   cudaStream_t st);
 int launch_fp64_mma_peak(double* out, int iters, int blocks, cudaStream_t st);
 int launch_l2_random_peak(uint32_t* bits, uint32_t words, int blocks, int per_thread, int mode, cudaStream_t st);
 int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* hf,
@@ -190,6 +200,26 @@ int fill_bspline(BsplineSpec& bs, int ngroups, const int32_t* h_order, const int
   for (int q = 0; q < h_start[ngroups]; ++q) {
     if (h_comps[q] < 0 || h_comps[q] >= d) return E_INVAL;
     bs.comps[q] = h_comps[q];
+  }
+  // pieces of B_m (testbed.py:198-216 evaluates the same spline with scipy's
+  // BSpline.basis_element): P_1 = [1]; piece i of B_k in t = u - i is
+  // ((t + i) P_{k-1,i}(t) + (k - i - t) P_{k-1,i-1}(t)) / (k - 1)
+  double prev[8][8] = {{1.0}};
+  bs.pc[bs_poff(1)] = 1.0;
+  for (int k = 2; k <= 7; ++k) {
+    double cur[8][8] = {};
+    for (int i = 0; i < k; ++i) {
+      for (int e = 0; e < k - 1; ++e) {  // degree of P_{k-1} is k - 2
+        const double a = i < k - 1 ? prev[i][e] : 0.0;      // P_{k-1,i}
+        const double b = i >= 1 ? prev[i - 1][e] : 0.0;      // P_{k-1,i-1}
+        cur[i][e] += (double)i * a + (double)(k - i) * b;    // constant parts
+        cur[i][e + 1] += a - b;                              // t * a - t * b
+      }
+      for (int e = 0; e < k; ++e) cur[i][e] /= (double)(k - 1);
+    }
+    for (int i = 0; i < k; ++i)
+      for (int e = 0; e < k; ++e) bs.pc[bs_poff(k) + i * k + e] = cur[i][e];
+    memcpy(prev, cur, sizeof(prev));
   }
   return 0;
 }
@@ -686,6 +716,43 @@ int sfft_gather_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, c
   if (rc) return rc;
   return launch_gather_units(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, ut, (double2*)d_out,
                              fast_i32(lt, t1, kmax, h_m, L), num_sms_current(), S(stream));
+}
+
+int64_t sfft_mask_tiles_len(int64_t n, int L) { return ((n + 255) / 256) * (int64_t)L; }
+
+int sfft_mask_tiles(const uint64_t* d_masks, int64_t n, int L, int32_t* d_tc, int32_t* d_toff, int64_t ts, int W,
+                    int32_t* d_sc, void* stream) {
+  if (n < 0) return E_INVAL;
+  return launch_mask_tiles(d_masks, n, L, d_tc, d_toff, ts, W, d_sc, num_sms_current(), S(stream));
+}
+
+int sfft_pack_units(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const int64_t* h_m, const int32_t* h_z,
+                    int L, const uint64_t* d_masks, const double* d_buf, int64_t P, int rb, const int32_t* h_units,
+                    int nunits, const int32_t* d_toff, int64_t ts, const int64_t* d_soff, double* d_send,
+                    void* stream) {
+  if (n < 0 || !h_units || ts < 1) return E_INVAL;
+  LatTable lt;
+  int rc = fill_lat(lt, h_m, h_z, L, t1);
+  if (rc) return rc;
+  UnitTable ut;
+  rc = fill_units(ut, h_m, L, rb, h_units, nunits);
+  if (rc) return rc;
+  return launch_pack_units(d_freqs, n, lt, d_masks, (const double2*)d_buf, P, ut, d_toff, ts, d_soff,
+                           (double2*)d_send, fast_i32(lt, t1, kmax, h_m, L), num_sms_current(), S(stream));
+}
+
+int sfft_combine_slice(int64_t n, int L, const uint64_t* d_masks, const int32_t* d_toff, int64_t ts, int q,
+                       const double* d_recv, const int64_t* d_roff, int rb, double delta, double* d_coef_s,
+                       uint8_t* d_keep_s, int32_t* d_counts, void* stream) {
+  if (n < 0 || L < 1 || L > SFFT_LMAX || rb < 1 || rb > 8 || q < 0 || ts < 1) return E_INVAL;
+  return launch_combine_slice(n, L, d_masks, d_toff, ts, q, (const double2*)d_recv, d_roff, rb, delta,
+                              (double2*)d_coef_s, d_keep_s, d_counts, num_sms_current(), S(stream));
+}
+
+int sfft_unshard_rows(const void* d_in, int elem, int W, int rb, int64_t S_, int64_t n, int it0, void* d_out,
+                      void* stream) {
+  if (W < 1 || rb < 1 || S_ < 0 || n < 0 || it0 < 0) return E_INVAL;
+  return launch_unshard(d_in, elem, W, rb, S_, n, it0, d_out, num_sms_current(), S(stream));
 }
 
 int sfft_combine_units(int64_t n, int L, const uint64_t* d_masks, const double* d_vals,

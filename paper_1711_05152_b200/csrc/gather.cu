@@ -657,11 +657,9 @@ __global__ void selr_apply_kernel(const double2* __restrict__ coef, uint8_t* __r
 }
 
 // one CTA per row: the first `need` tie entries in index order are kept
-// (rank within the appended list; a sequential block scan if it overflowed)
+// (rank within the appended list; overflowed lists: the chunked kernels below)
 __global__ void __launch_bounds__(1024) selr_ties_kernel(uint8_t* __restrict__ keep, int64_t n, SelRows rows,
                                                          const SelRowState* __restrict__ st) {
-  __shared__ int wsum[32];
-  __shared__ int base;
   __shared__ int lst[SEL_TIE_LIST];
   const SelRowState& s = st[blockIdx.x];
   if (!s.active || s.count_eq == s.need) return;  // nothing capped, or every tie kept in selr_apply
@@ -679,23 +677,80 @@ __global__ void __launch_bounds__(1024) selr_ties_kernel(uint8_t* __restrict__ k
     }
     return;
   }
-  if (threadIdx.x == 0) base = 0;
+  // more ties than the list holds: selr_tiecount / selr_tiescan / selr_tiemark
+}
+
+// Overflowed tie lists (more than SEL_TIE_LIST entries equal to the threshold,
+// e.g. the +-k mirror ties of the B-spline spectrum at a binding cap): ranks
+// in index order by a chunked count / scan / mark over all CTAs; the row's
+// list storage holds the per-chunk counts (at most SEL_TIE_LIST chunks).
+__host__ __device__ inline int64_t tie_chunk(int64_t n) {
+  const int64_t per = (n + SEL_TIE_LIST - 1) / SEL_TIE_LIST;
+  return ((per + 2047) / 2048) * 2048;
+}
+
+__device__ __forceinline__ bool tie_overflow(const SelRowState& s) {
+  return s.active && s.count_eq != s.need && s.nlist > SEL_TIE_LIST;
+}
+
+__global__ void __launch_bounds__(256) selr_tiecount_kernel(const uint8_t* __restrict__ keep, int64_t n,
+                                                            SelRows rows, SelRowState* st) {
+  __shared__ int red[8];
+  SelRowState& s = st[blockIdx.y];
+  if (!tie_overflow(s)) return;
+  const int64_t ch = tie_chunk(n);
+  const int64_t i0 = (int64_t)blockIdx.x * ch, i1 = min(n, i0 + ch);
+  const uint8_t* k = keep + (int64_t)rows.row[blockIdx.y] * n;
+  int c = 0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) c += k[i] == 2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    s.list[blockIdx.x] = t;
+  }
+}
+
+__global__ void selr_tiescan_kernel(int64_t n, SelRowState* st) {
+  SelRowState& s = st[blockIdx.x];
+  if (!tie_overflow(s) || threadIdx.x != 0) return;
+  const int nch = (int)((n + tie_chunk(n) - 1) / tie_chunk(n));
+  int acc = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int v = s.list[c];
+    s.list[c] = acc;
+    acc += v;
+  }
+}
+
+__global__ void __launch_bounds__(256) selr_tiemark_kernel(uint8_t* __restrict__ keep, int64_t n, SelRows rows,
+                                                           const SelRowState* __restrict__ st) {
+  __shared__ int wsum[8];
+  const SelRowState& s = st[blockIdx.y];
+  if (!tie_overflow(s)) return;
+  const int64_t ch = tie_chunk(n);
+  const int64_t i0 = (int64_t)blockIdx.x * ch, i1 = min(n, i0 + ch);
+  uint8_t* k = keep + (int64_t)rows.row[blockIdx.y] * n;
+  const int need = s.need;
+  int base = s.list[blockIdx.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int64_t i = i0 + threadIdx.x;
-    const bool t = i < n && k[i] == 2;
+  for (int64_t b = i0; b < i1; b += blockDim.x) {
+    const int64_t i = b + threadIdx.x;
+    const bool t = i < i1 && k[i] == 2;
     const unsigned bal = __ballot_sync(0xffffffffu, t);
     if (lane == 0) wsum[w] = __popc(bal);
     __syncthreads();
     int before = 0, total = 0;
-    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
       before += j < w ? wsum[j] : 0;
       total += wsum[j];
     }
     if (t) k[i] = (base + before + __popc(bal & ((1u << lane) - 1u))) < need ? 1 : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) base += total;
+    base += total;
     __syncthreads();
   }
 }
@@ -718,7 +773,11 @@ int launch_select_cap_rows(const double2* coef, uint8_t* keep, int64_t n, const 
     selr_pass_kernel<<<dim3(blocks, nrows), 256, 0, st>>>(coef, keep, n, rows, s, dgt * 8);
   selr_apply_kernel<<<dim3(blocks, nrows), 256, 0, st>>>(coef, keep, n, rows, s);
   selr_ties_kernel<<<nrows, 1024, 0, st>>>(keep, n, rows, s);
-  SFFT_CHECK_LAUNCHES(11);
+  const unsigned nch = (unsigned)((n + tie_chunk(n) - 1) / tie_chunk(n));
+  selr_tiecount_kernel<<<dim3(nch, nrows), 256, 0, st>>>(keep, n, rows, s);
+  selr_tiescan_kernel<<<nrows, 32, 0, st>>>(n, s);
+  selr_tiemark_kernel<<<dim3(nch, nrows), 256, 0, st>>>(keep, n, rows, s);
+  SFFT_CHECK_LAUNCHES(14);
   return 0;
 }
 

@@ -20,6 +20,9 @@
 #include "plan.cuh"
 #include "sample.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace sfft {
 
 // c'[it, h] = c_h * e^{2 pi i sum_{c >= t1} h_c a[it, c - t1]}
@@ -442,6 +445,121 @@ unit_norm2_kernel(UnitTable ut, const double2* __restrict__ buf, int64_t ustride
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// B-spline sampler with the lattice work shared by the iterations
+// (K1b).  The units of one lattice differ only in the anchor tail, so per node
+// the factors of the lattice coordinates are evaluated once, grouped
+//   G_g(n) = prod_{c in A_g, c < t1} C_m m B_m(m x_c(n)),
+// and unit i gets total_i = sum_g K_{i,g} G_g(n) with the anchor factors
+// K_{i,g} = prod_{c in A_g, c >= t1} C_m m B_m(m a_{i,c}) computed once per CTA.
+// B_m is evaluated as its piecewise polynomial (Horner in t = u - floor(u),
+// bs.pc) instead of the Cox-de Boor triangle.  Grid: (node blocks, lattice).
+template <int M_>
+__device__ __forceinline__ double bs_horner_t(const double* __restrict__ pc, double u) {
+  int iv = (int)u;  // u >= 0
+  if (iv > M_ - 1) iv = M_ - 1;
+  const double t = u - (double)iv;
+  const double* c = pc + bs_poff(M_) + iv * M_;
+  double v = c[M_ - 1];
+#pragma unroll
+  for (int k = M_ - 2; k >= 0; --k) v = fma(v, t, c[k]);
+  return v;
+}
+
+__device__ __forceinline__ double bs_horner(const double* __restrict__ pc, int m, double u) {
+  switch (m) {
+    case 1: return u < 1.0 ? 1.0 : 0.0;
+    case 2: return bs_horner_t<2>(pc, u);
+    case 3: return bs_horner_t<3>(pc, u);
+    case 4: return bs_horner_t<4>(pc, u);
+    case 5: return bs_horner_t<5>(pc, u);
+    case 6: return bs_horner_t<6>(pc, u);
+    default: return bs_horner_t<7>(pc, u);
+  }
+}
+
+constexpr int BS_SLOTS = 8;
+
+template <bool FAST>
+__global__ void __launch_bounds__(256)
+sample_bspline_lat_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at,
+                          const double2* __restrict__ chirp, double2* __restrict__ buf, int64_t ustride,
+                          int apply_chirp) {
+  __shared__ double pc[140];
+  __shared__ double K[BS_SLOTS][8];
+  __shared__ int slot[SFFT_UMAX];
+  __shared__ int nslot;
+  const int l = blockIdx.y;
+  const int t1 = lt.d;
+  const int tail = bs.d - t1;
+  const int G = bs.ngroups;
+  for (int i = threadIdx.x; i < 140; i += blockDim.x) pc[i] = bs.pc[i];
+  if (threadIdx.x < 32) {  // the launch's units of this lattice, in slot order
+    int cnt = 0;
+    for (int b = 0; b < ut.nunits; b += 32) {
+      const int j = b + (int)threadIdx.x;
+      const bool hit = j < ut.nunits && ut.lat[j] == l;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) slot[cnt + __popc(bal & ((1u << threadIdx.x) - 1u))] = j;
+      cnt += __popc(bal);
+    }
+    if (threadIdx.x == 0) nslot = cnt;
+  }
+  __syncthreads();
+  const int ns = nslot;
+  if (ns == 0) return;
+  for (int c0 = 0; c0 < ns; c0 += BS_SLOTS) {
+    const int nc = min(BS_SLOTS, ns - c0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nc * G; q += blockDim.x) {  // anchor factors of slot, group
+      const int sl = q / G, g = q % G;
+      const int it = ut.it[slot[c0 + sl]];
+      const int m = bs.order[g];
+      double k = 1.0;
+      for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
+        const int c = bs.comps[e];
+        if (c >= t1) k = k * (bs.scale[g] * bs_horner(pc, m, (double)m * at.a[it * tail + (c - t1)]));
+      }
+      K[sl][g] = k;
+    }
+    __syncthreads();
+    const int64_t M = lt.m[l];
+    const double invM = lt.inv_m[l];
+    const double2* ch = chirp + lt.off[l];
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < M;
+         n += (int64_t)gridDim.x * blockDim.x) {
+      double tot[BS_SLOTS];
+#pragma unroll
+      for (int s = 0; s < BS_SLOTS; ++s) tot[s] = 0.0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (g < G) {
+          const int m = bs.order[g];
+          double gg = 1.0;
+          for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
+            const int c = bs.comps[e];
+            if (c < t1) {
+              const int64_t r = mulmod<FAST>(n, (int64_t)lt.z[l * t1 + c], M, invM);
+              const double x = (double)r * invM;  // within 1 ulp of r / M, the reference's node
+              gg = gg * (bs.scale[g] * bs_horner(pc, m, (double)m * x));
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < BS_SLOTS; ++s)
+            if (s < nc) tot[s] += K[s][g] * gg;
+        }
+      }
+      double2 cv = make_double2(1.0, 0.0);
+      if (apply_chirp) cv = __ldg(&ch[n]);
+#pragma unroll
+      for (int s = 0; s < BS_SLOTS; ++s)
+        if (s < nc) {
+          double2* ub = buf + (int64_t)slot[c0 + s] * ustride;
+          __stcs(&ub[n], apply_chirp ? make_double2(tot[s] * cv.x, tot[s] * cv.y) : make_double2(tot[s], 0.0));
+        }
+    }
+  }
+}
+
 // lattice nodes for a host-callback oracle: pts[n, c] (row-major, d columns)
 template <bool FAST>
 __global__ void lattice_nodes_kernel(LatTable lt, int l, int d, AnchorTable at, int it,
@@ -542,6 +660,24 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
                           cudaStream_t st) {
   int64_t mmax = 1;
   for (int l = 0; l < lt.nlat; ++l) mmax = lt.m[l] > mmax ? lt.m[l] : mmax;
+  static const bool legacy = [] {
+    const char* e = getenv("SFFT_B200_BSPLINE_KERNEL");
+    return e && strcmp(e, "unit") == 0;
+  }();
+  if (!legacy) {
+    // one CTA column per lattice; every CTA serves all units of its lattice
+    int bx = (int)((mmax + 255) / 256);
+    const int cap = (num_sms * 8 + lt.nlat - 1) / lt.nlat;
+    if (bx > cap) bx = cap;
+    if (fast)
+      sample_bspline_lat_kernel<true><<<dim3(bx, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
+                                                                         apply_chirp ? 1 : 0);
+    else
+      sample_bspline_lat_kernel<false><<<dim3(bx, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
+                                                                          apply_chirp ? 1 : 0);
+    SFFT_CHECK_LAUNCH();
+    return 0;
+  }
   int bx = (int)((mmax + 255) / 256);
   const int cap = (num_sms * 8 + ut.nunits - 1) / ut.nunits + 1;
   if (bx > cap) bx = cap;

@@ -50,7 +50,13 @@ struct BsplineSpec {
   int start[9];
   int comps[SFFT_DMAX];
   double scale[8];  // C_m * m
+  // piecewise-polynomial form of the cardinal B-spline of order m on [0, m]:
+  // piece iv (u in [iv, iv + 1)) is sum_k pc[bs_poff(m) + iv * m + k] t^k,
+  // t = u - iv (filled by the host from the Cox-de Boor recursion)
+  double pc[140];
 };
+
+__host__ __device__ constexpr int bs_poff(int m) { return (m - 1) * m * (2 * m - 1) / 6; }
 
 int launch_poly_prepare(const int32_t* hf, const double2* coef, int s, int d, const LatTable& lt,
                         const PolyPlan& pp, const AnchorTable& at, double2* cprime, int32_t* rres,

@@ -450,12 +450,10 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             from .single import single_scheme
             sch = single_scheme(dev, cand)  # CBC (reference detect.py:269-271), no RNG consumed
         else:
-            prepare = None
-            if not sharded:
-                # while the alias kernel runs: buffers, the sampling operands
-                # (and the tables, when this step's sizes were seen before)
-                prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
-                                                     cached_tables_only=True, tails=tails, d=d)
+            # while the alias kernel runs: buffers, the sampling operands
+            # (and the tables, when this step's sizes were seen before)
+            prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
+                                                 cached_tables_only=True, tails=tails, d=d)
             sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
                                ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare,
                                first_rng=first_rngs[t])
@@ -468,7 +466,8 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
                 f"candidates after {sch.attempts} attempts"
             )
         if sharded:
-            res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t)
+            res = run_step_sharded(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, sh, step=t,
+                                   prep=sch.prep, need_coef=last)
         else:
             res = run_step(dev, oracle, cand, sch, tails, d, cfg.delta, s_tilde, step=t, prep=sch.prep,
                            device_cap=True)

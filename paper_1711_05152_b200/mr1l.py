@@ -29,7 +29,7 @@ from .device import Device, dptr, hptr
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig, candidate_primes
 
-__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "speculate_scheme", "SchemeGuess", "run_step",
+__all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "clear_caches", "speculate_scheme", "SchemeGuess", "run_step",
            "prepare_step", "StepPrep", "StepResult", "first_attempt_rng",
            "OracleInterrupt", "OracleError", "evaluate_callback"]
 
@@ -388,6 +388,16 @@ class _TableCache:
 
 
 _TABLES: dict[int, _TableCache] = {}
+
+
+def clear_caches(dev: Device | None = None) -> None:
+    """Drop every size-keyed cache (per-size lattice tables, FFT twiddle
+    tables, the candidate-prime memo) so the next step pays what a step with
+    never-seen lattice sizes pays (the bench's cold-step figures)."""
+    _TABLES.clear()
+    _PRIMES_MEMO.clear()
+    if dev is not None:
+        dev._ftab.clear()
 
 
 def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str = "",

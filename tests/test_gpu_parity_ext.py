@@ -295,3 +295,80 @@ def test_long_lines_binding_cap_matches_oracle(P):
         kept, _ = O.select(ks[:, None], cf, 9, 1e-9)
         want.append(kept[:, 0])
     assert np.array_equal(comp.freqs[:, 0], np.unique(np.concatenate(want)))
+
+
+# ---------------------------------------------------------------------------
+# K1b: the B-spline sampler (lattice factors shared by the units of a lattice)
+
+@pytest.mark.parametrize("units", [None, [5, 0, 3], [4]])
+def test_bspline_sampler_matches_oracle(P, units):
+    """sfft_sample_bspline at lattice nodes + anchor tails (detect.py:290-297)
+    against the CPU oracle's B-spline (testbed.py:198-244), raw samples
+    (no chirp): every unit, or a unit subset in any order (sharded steps)."""
+    from oracle import sfft_oracle as O
+    from paper_1711_05152_b200.device import dptr, get_device, hptr
+    dev = get_device()
+    torch = dev.torch
+    groups = ((2, (0, 5, 7)), (4, (1, 3, 4, 9)), (6, (2, 6, 8)))
+    oracle = P.bspline_test_function(groups)
+    order, start, comps, scale = oracle.host_spec()
+    rng = np.random.default_rng(4)
+    t1, d, rb = 6, 10, 2
+    ms = np.array([10007, 7919, 4099], dtype=np.int64)
+    L = len(ms)
+    zs = np.ascontiguousarray(np.stack([rng.integers(0, m, t1) for m in ms]).astype(np.int32))
+    anchor = np.ascontiguousarray(rng.random((rb, d - t1)))
+    ulist = list(range(rb * L)) if units is None else units
+    ua = None if units is None else np.ascontiguousarray(np.asarray(units, dtype=np.int32))
+    Pl = 10240
+    buf = dev.zeros((len(ulist), Pl, 2), torch.float64)
+    chirp = dev.zeros((int(ms.sum()), 2), torch.float64)
+    dev.call("sfft_sample_bspline", len(groups), hptr(order), hptr(start), hptr(comps), hptr(scale), d, t1,
+             hptr(ms), hptr(zs), L, hptr(anchor), rb, dptr(chirp), dptr(buf), Pl, 0,
+             hptr(ua) if ua is not None else 0, len(ua) if ua is not None else 0)
+    got = dev.download(buf)
+    for j, u in enumerate(ulist):
+        i, l = divmod(u, L)
+        m = int(ms[l])
+        pts = np.empty((m, d))
+        pts[:, :t1] = O.lattice_nodes(zs[l].astype(np.int64), m)
+        pts[:, t1:] = anchor[i]
+        ref = O.bspline_eval(groups, pts)
+        v = got[j, :m, 0] + 1j * got[j, :m, 1]
+        assert np.abs(v - ref).max() <= 1e-13 * np.abs(ref).max(), (u, np.abs(v - ref).max())
+
+
+@pytest.mark.parametrize("n,nvals", [(100_000, 7), (3_000_000, 40)])
+def test_cap_selection_many_ties(P, n, nvals):
+    """The cap (detect.py:205-211: |c| descending, ties by ascending index =
+    lexicographic candidate order) when far more than 2048 entries tie at the
+    threshold (the chunked count / scan / mark path), for two rows at once."""
+    from paper_1711_05152_b200 import _native
+    from paper_1711_05152_b200.device import dptr, get_device, hptr
+    dev = get_device()
+    torch = dev.torch
+    rng = np.random.default_rng(n)
+    levels = rng.uniform(0.5, 2.0, nvals)
+    mags = levels[rng.integers(0, nvals, (2, n))]
+    quarter = rng.integers(0, 4, (2, n))  # c = level * i^q: exact magnitudes, many exact ties
+    c = np.where(quarter % 2 == 0, mags * (1 - quarter) + 0j, 1j * mags * (2 - quarter))
+    keep0 = (rng.random((2, n)) < 0.9).astype(np.uint8)
+    cap = n // 3
+    coef = torch.from_numpy(np.stack([c.real, c.imag], axis=-1)).to(dev.device)
+    keep = torch.from_numpy(keep0.copy()).to(dev.device)
+    counts = torch.from_numpy(keep0.sum(axis=1).astype(np.int32)).to(dev.device)
+    rows = np.arange(2, dtype=np.int32)
+    sb = int(_native.query("sfft_select_rows_scratch_bytes", 2))
+    scratch = dev.empty((sb,), torch.uint8)
+    dev.call("sfft_select_cap_rows", dptr(coef), dptr(keep), n, hptr(rows), 2, cap, dptr(counts), dptr(scratch))
+    got = dev.download(keep).astype(bool)
+    mag_dev = np.hypot(c.real, c.imag)
+    for y in range(2):
+        idx = np.nonzero(keep0[y])[0]
+        order = np.lexsort((idx, -mag_dev[y, idx]))[:cap]
+        want = np.zeros(n, dtype=bool)
+        want[idx[order]] = True
+        thr = mag_dev[y, idx[order[-1]]]
+        assert (mag_dev[y, idx] == thr).sum() > 2048  # the overflow path ran
+        assert np.array_equal(got[y], want), y
+    assert dev.download(counts).tolist() == [cap, cap]
