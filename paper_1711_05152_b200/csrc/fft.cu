@@ -22,6 +22,8 @@
 #include <string.h>
 
 #include "common.cuh"
+
+#include <cstdlib>
 #include "fft.cuh"
 #include "plan.cuh"
 
@@ -493,10 +495,23 @@ int launch_bhat(const LatTable& lt, const double2* chirp, double2* bhat, const F
                        ftab, nullptr, chirp);
 }
 
-int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
-                     const double2* bhat, const double2* chirp, cudaStream_t st) {
+// drop the dead tail [M, P) of a unit's buffer from L2 without writing it
+// back (discard.global.L2): after the inverse column pass only the spectrum
+// k < M is live, the tail holds row-pass data nobody reads again
+__global__ void discard_tails_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, int64_t P) {
+  const int u = blockIdx.y;
+  const int64_t M = ut.m[ut.lat[u]];
+  const uintptr_t base = (uintptr_t)(buf + (int64_t)u * ustride);
+  const uintptr_t a = (base + (uintptr_t)M * sizeof(double2) + 127) & ~(uintptr_t)127;
+  const uintptr_t e = (base + (uintptr_t)P * sizeof(double2)) & ~(uintptr_t)127;
+  for (uintptr_t p = a + ((uintptr_t)blockIdx.x * blockDim.x + threadIdx.x) * 128; p < e;
+       p += (uintptr_t)gridDim.x * blockDim.x * 128)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+static int bluestein_group(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
+                           const double2* bhat, const double2* chirp, bool discard, cudaStream_t st) {
   const int64_t P = g.P;
-  prof_mark(PROF_FFT, true, st);
   int rc = run_cols(false, buf, P, ut, g, 1, ftab, chirp, st);
   if (rc) return rc;
   const size_t sm = fft_smem_bytes(g.te, g.P2);
@@ -509,6 +524,44 @@ int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const 
                        bhat, chirp);
   if (rc) return rc;
   rc = run_cols(true, buf, P, ut, g, 0, ftab, chirp, st);
+  if (rc || !discard) return rc;
+  discard_tails_kernel<<<dim3(64, ut.nunits), 256, 0, st>>>(buf, P, ut, P);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+// The three passes run on groups of units whose P-length buffers fit in L2
+// together (SFFT_B200_FFT_GROUP_MB, default 40 MB): the column pass's output
+// is then read back by the row pass, and the row pass's by the inverse
+// column pass, from L2 instead of HBM; the dead tails are discarded.
+int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
+                     const double2* bhat, const double2* chirp, cudaStream_t st) {
+  const int64_t P = g.P;
+  static const int64_t budget = [] {
+    const char* e = getenv("SFFT_B200_FFT_GROUP_MB");
+    return (int64_t)(e ? atof(e) : 40.0) << 20;
+  }();
+  const int64_t unit_bytes = P * (int64_t)sizeof(double2);
+  int per = budget > 0 ? (int)(budget / unit_bytes) : ut.nunits;
+  if (per < 1) per = 1;
+  const bool grouped = per < ut.nunits && P >= (1 << 18);
+  prof_mark(PROF_FFT, true, st);
+  int rc = 0;
+  if (!grouped) {
+    rc = bluestein_group(buf, ut, g, ftab, bhat, chirp, false, st);
+  } else {
+    UnitTable* sub = new UnitTable(ut);
+    for (int u0 = 0; u0 < ut.nunits && !rc; u0 += per) {
+      const int nu = ut.nunits - u0 < per ? ut.nunits - u0 : per;
+      sub->nunits = nu;
+      for (int j = 0; j < nu; ++j) {
+        sub->lat[j] = ut.lat[u0 + j];
+        sub->it[j] = ut.it[u0 + j];
+      }
+      rc = bluestein_group(buf + (int64_t)u0 * P, *sub, g, ftab, bhat, chirp, true, st);
+    }
+    delete sub;
+  }
   prof_mark(PROF_FFT, false, st);
   return rc;
 }

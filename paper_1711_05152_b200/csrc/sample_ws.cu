@@ -33,8 +33,10 @@ constexpr int KC = 16;       // terms per stage
 constexpr int NS = 3;        // stages
 constexpr int NCONS = 256;   // consumer threads (two warpgroups)
 constexpr int NPROD = 128;   // producer threads (one warpgroup)
-constexpr int REG_CONS = 232;  // setmaxnreg: consumers grow, producers shrink: 8 x 232 + 4 x 48
-constexpr int REG_PROD = 48;   // warps = the 64K-register file exactly (no spills in either role)
+constexpr int REG_CONS = 224;  // setmaxnreg: consumers grow, producers shrink within the launch's
+constexpr int REG_PROD = 56;   // 384 x 168 registers: 256 x (224 - 168) = 128 x (168 - 56).  (232 / 48
+                               // would remove the epilogue's 136 B spill but needs 1024 registers more
+                               // than the CTA owns: setmaxnreg.inc then waits forever.)
 constexpr int NT = NCONS + NPROD;
 constexpr int STAGE = KC * (TJ1 + TJ2);  // complex elements per stage
 }  // namespace ws

@@ -310,6 +310,18 @@ def long_line_fixture(out):
     out.update(ll_line_anchor=anchor, ll_line_ks=ks, ll_line_c=c)
 
 
+def harness_fixture(out):
+    """The reference's experiment grid (cli.py:349-418) on two small specs:
+    the emitted CSV text."""
+    from sfft.cli import ExperimentSpec, emit, run_experiment
+    from make_golden_specs import HARNESS_SPECS
+    for key, kw in HARNESS_SPECS.items():
+        rows, code = run_experiment(ExperimentSpec(**kw))
+        out[f"{key}_csv"] = np.array([emit(rows, "csv")])
+        out[f"{key}_code"] = np.array([code])
+        print(emit(rows, "csv"))
+
+
 def cfg3_reduced_fixture(out):
     """BASELINE config 3 (d = 20, [-32, 32]^20, polar coefficients, per-call
     1e-2 relative noise, delta = 0.1) at reduced sparsity s = 100, r = 2, run
@@ -350,10 +362,10 @@ def main_ext(which):
     path = HERE / "golden_ext.npz"
     out: dict = dict(np.load(path)) if path.exists() else {}
     fns = {"retry": retry_fixture, "cfg3": cfg3_reduced_fixture, "cfg4": cfg4_full_fixture,
-           "longline": long_line_fixture}
+           "longline": long_line_fixture, "harness": harness_fixture}
     for name in which or list(fns):
         prefix = {"retry": ("rt_", "rtrun_", "partial_"), "cfg3": ("c3_",), "cfg4": ("c4_",),
-                  "longline": ("ll_",)}[name]
+                  "longline": ("ll_",), "harness": ("hx_", "hn_")}[name]
         out = {k: v for k, v in out.items() if not k.startswith(prefix)}
         fns[name](out)
         np.savez_compressed(path, **out)
