@@ -148,10 +148,12 @@ alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int
 // cluster / DSMEM variant
 
 struct AliasGroups {
-  int l0;    // first lattice of the launch
-  int nl;    // lattices of the launch
-  int g;     // lattices per cluster
-  int wpc;   // bitmap words per CTA and bitmap
+  int l0;      // first lattice of the launch
+  int nl;      // lattices of the launch
+  int g;       // lattices per cluster
+  int wpc;     // bitmap words per CTA and bitmap
+  int keep;    // residues of pass 1 kept in shared memory for pass 2
+  int64_t sl;  // candidates per CTA slice (multiple of 32)
 };
 
 __device__ __forceinline__ uint32_t dsm_map(uint32_t local, uint32_t rank) {
@@ -176,13 +178,14 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-constexpr int ACG = 4;  // lattices whose cluster atomics are issued back to back
+constexpr int ACG = 4;     // lattices whose cluster atomics are issued back to back
+constexpr int ACT = 1024;  // threads per CTA (one CTA per SM; latency hiding by width)
 
 template <int DM, bool FAST>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(ACT)
 alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, AliasGroups ag,
                      uint32_t* __restrict__ planes, int64_t pwords) {
-  extern __shared__ uint32_t bm[];  // [g][seen1 | seen2][wpc]
+  extern __shared__ uint32_t bm[];  // [g][seen1 | seen2][wpc], then (keep) residues [g][sl]
   uint32_t rank, nct;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
@@ -191,12 +194,12 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
   const int le = min(ag.l0 + ag.nl, lb + ag.g);
   const int ng = le - lb;
   const int wpc = ag.wpc;
+  uint32_t* res_s = bm + 2 * ag.g * wpc;
   for (int w = threadIdx.x; w < ng * 2 * wpc; w += blockDim.x) bm[w] = 0u;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(bm);
   cluster_barrier();  // every CTA's bitmaps are zero before the first remote atomic
-  const int64_t nw = (n + 31) >> 5;
-  const int64_t i0 = (nw * rank / nct) * 32;
-  const int64_t i1 = min(n, (nw * (rank + 1) / nct) * 32);
+  const int64_t i0 = min(n, (int64_t)rank * ag.sl);
+  const int64_t i1 = min(n, i0 + ag.sl);
   const int d = lt.d;
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     int32_t k[DM];
@@ -210,8 +213,9 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
         bit[q] = 0u;
         old[q] = 0u;
         if (j < ng) {
-          const int64_t r = SFFT_RES(DM, FAST, k, lt, lb + j);
-          const uint32_t gw = (uint32_t)(r >> 5);
+          const uint32_t r = (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
+          if (ag.keep) res_s[(int64_t)j * ag.sl + (i - i0)] = r;
+          const uint32_t gw = r >> 5;
           const uint32_t owner = gw / (uint32_t)wpc;
           adr[q] = dsm_map(base + 4u * ((uint32_t)(2 * j * wpc) + gw - owner * (uint32_t)wpc), owner);
           bit[q] = 1u << (r & 31);
@@ -229,8 +233,10 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
     const int64_t i = ib + threadIdx.x;
     const bool live = i < i1;
     int32_t k[DM];
+    if (!ag.keep) {
 #pragma unroll
-    for (int c = 0; c < DM; ++c) k[c] = (live && c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+      for (int c = 0; c < DM; ++c) k[c] = (live && c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    }
     for (int jb = 0; jb < ng; jb += ACG) {
       uint32_t v[ACG], sh[ACG];
 #pragma unroll
@@ -239,11 +245,12 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
         v[q] = ~0u;
         sh[q] = 0u;
         if (live && j < ng) {
-          const int64_t r = SFFT_RES(DM, FAST, k, lt, lb + j);
-          const uint32_t gw = (uint32_t)(r >> 5);
+          const uint32_t r = ag.keep ? res_s[(int64_t)j * ag.sl + (i - i0)]
+                                     : (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
+          const uint32_t gw = r >> 5;
           const uint32_t owner = gw / (uint32_t)wpc;
           v[q] = dsm_ld(dsm_map(base + 4u * ((uint32_t)((2 * j + 1) * wpc) + gw - owner * (uint32_t)wpc), owner));
-          sh[q] = (uint32_t)(r & 31);
+          sh[q] = r & 31u;
         }
       }
 #pragma unroll
@@ -294,9 +301,14 @@ alias_planes_kernel(int64_t n, int l0, int l1, const uint32_t* __restrict__ plan
 namespace {
 constexpr size_t ALIAS_SMEM_MAX = 200 * 1024;
 
-// cluster geometry for lattices [l0, l1): 0 when no cluster variant fits
+// Cluster geometry for lattices [l0, l1): the largest cluster (16 CTAs where
+// allowed, else 8) and the fewest lattices per cluster g such that the
+// clusters are resident at once (one wave, one CTA per SM) and a group's
+// bitmaps fit in its shared memory; residues are kept for pass 2 when they
+// fit too.  False when no geometry fits (the L2-atomic kernels then run).
 template <int DM, bool FAST>
-bool alias_cluster_plan(const LatTable& lt, int l0, int l1, int& cl, AliasGroups& ag, int& clusters, size_t& smem) {
+bool alias_cluster_plan(const LatTable& lt, int64_t n, int l0, int l1, int& cl, AliasGroups& ag, int& clusters,
+                        size_t& smem) {
   static const bool disabled = [] {
     const char* e = getenv("SFFT_B200_ALIAS_CLUSTER");
     return e && strcmp(e, "0") == 0;
@@ -314,15 +326,18 @@ bool alias_cluster_plan(const LatTable& lt, int l0, int l1, int& cl, AliasGroups
       (void)cudaGetLastError();
       continue;
     }
-    // most clusters that can be resident with one lattice each, then fold
-    // lattices into clusters until the group's bitmaps fit
+    const int64_t sl = (((n + 31) / 32 + c - 1) / c) * 32;
     for (int g = 1; g <= nl; ++g) {
-      const size_t sm = per_lat * g;
+      const int need = (nl + g - 1) / g;
+      size_t sm = per_lat * g;
       if (sm > ALIAS_SMEM_MAX) break;
+      const size_t with_res = sm + (size_t)g * sl * 4;
+      const bool keep = with_res <= ALIAS_SMEM_MAX;
+      if (keep) sm = with_res;
       if (set_smem_once(fn, sm) != cudaSuccess) { (void)cudaGetLastError(); break; }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c, 1, 1);
-      cfg.blockDim = dim3(256, 1, 1);
+      cfg.blockDim = dim3(ACT, 1, 1);
       cfg.dynamicSmemBytes = sm;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -333,13 +348,14 @@ bool alias_cluster_plan(const LatTable& lt, int l0, int l1, int& cl, AliasGroups
       cfg.numAttrs = 1;
       int maxc = 0;
       if (cudaOccupancyMaxActiveClusters(&maxc, fn, &cfg) != cudaSuccess) { (void)cudaGetLastError(); break; }
-      const int need = (nl + g - 1) / g;
       if (maxc >= need) {
         cl = c;
         ag.l0 = l0;
         ag.nl = nl;
         ag.g = g;
         ag.wpc = wpc;
+        ag.keep = keep ? 1 : 0;
+        ag.sl = sl;
         clusters = need;
         smem = sm;
         return true;
@@ -358,10 +374,10 @@ static int launch_alias_cluster_t(const int32_t* freqs, int64_t n, const LatTabl
   int cl = 0, clusters = 0;
   AliasGroups ag;
   size_t smem = 0;
-  if (!alias_cluster_plan<DM, FAST>(lt, l0, lt.nlat, cl, ag, clusters, smem)) return 0;
+  if (!alias_cluster_plan<DM, FAST>(lt, n, l0, lt.nlat, cl, ag, clusters, smem)) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cl * clusters, 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
+  cfg.blockDim = dim3(ACT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -373,7 +389,11 @@ static int launch_alias_cluster_t(const int32_t* freqs, int64_t n, const LatTabl
   cfg.numAttrs = 1;
   prof_mark(PROF_ALIAS, true, st);
   cudaError_t e = cudaLaunchKernelEx(&cfg, alias_cluster_kernel<DM, FAST>, freqs, n, lt, ag, planes, pwords);
-  if (e != cudaSuccess) return (int)e;
+  if (e != cudaSuccess) {  // e.g. a cluster shape the context cannot place: the L2-atomic kernels
+    (void)cudaGetLastError();
+    prof_mark(PROF_ALIAS, false, st);
+    return 0;
+  }
   int64_t want = (n + 255) / 256;
   int64_t cap = (int64_t)num_sms * 8;
   const int blocks = (int)(want < cap ? want : cap);

@@ -530,16 +530,17 @@ static int bluestein_group(double2* buf, const UnitTable& ut, const FftGeom& g, 
   return 0;
 }
 
-// The three passes run on groups of units whose P-length buffers fit in L2
-// together (SFFT_B200_FFT_GROUP_MB, default 40 MB): the column pass's output
-// is then read back by the row pass, and the row pass's by the inverse
-// column pass, from L2 instead of HBM; the dead tails are discarded.
+// SFFT_B200_FFT_GROUP_MB=<MB> runs the three passes on groups of units whose
+// P-length buffers fit in L2 together (the column pass's output read back by
+// the row pass from L2, dead tails discarded).  Off by default: at config 1
+// it cut DRAM traffic but the smaller launches' tails cost more than the
+// traffic saved (K2 0.184 -> 0.225 ms with 40 MB groups, profiles/r02_*).
 int launch_bluestein(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
                      const double2* bhat, const double2* chirp, cudaStream_t st) {
   const int64_t P = g.P;
   static const int64_t budget = [] {
     const char* e = getenv("SFFT_B200_FFT_GROUP_MB");
-    return (int64_t)(e ? atof(e) : 40.0) << 20;
+    return (int64_t)(e ? atof(e) : 0.0) << 20;
   }();
   const int64_t unit_bytes = P * (int64_t)sizeof(double2);
   int per = budget > 0 ? (int)(budget / unit_bytes) : ut.nunits;

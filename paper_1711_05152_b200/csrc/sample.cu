@@ -560,6 +560,168 @@ sample_bspline_lat_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable
   }
 }
 
+// K1b main variant: the lattice-shared sampler with the per-coordinate work
+// made incremental.  Coordinate c of node n has u = m x = m (n z_c mod M) / M;
+// the thread walks its nodes n0, n0 + S, n0 + 2S, ... (S = grid stride) and
+// carries, per lattice coordinate, Q = m (n z_c mod M) as (piece iv, rem) with
+// Q = iv M + rem: one step adds m (S z_c mod M) = Dq M + Dr with integer
+// carries, so B_m(u) is the piece iv polynomial at t = rem / M (exact rational,
+// one multiply by 1/M) -- no modular product, no float floor per node.
+// Coordinates are laid out group-major ("positions") so the registers of
+// every position have compile-time indices (NP = 16 positions at most).
+constexpr int BSC_NP = 16;
+
+__global__ void __launch_bounds__(256)
+sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at,
+                            const double2* __restrict__ chirp, double2* __restrict__ buf, int64_t ustride,
+                            int apply_chirp) {
+  __shared__ double pcg[8][49];      // group g's piece polynomials of order m_g, scaled by C_m m
+  __shared__ double K[BS_SLOTS][8];  // anchor factors per slot and group
+  __shared__ double C0[BS_SLOTS];    // groups without lattice coordinates: their constant terms
+  __shared__ int slot[SFFT_UMAX];
+  __shared__ int nslot, npos;
+  __shared__ int pmeta[BSC_NP];      // m | group << 4 | (last position of its group) << 8
+  __shared__ uint32_t pz[BSC_NP], pdq[BSC_NP], pdr[BSC_NP];
+  const int l = blockIdx.y;
+  const int t1 = lt.d;
+  const int tail = bs.d - t1;
+  const int G = bs.ngroups;
+  const int64_t M = lt.m[l];
+  const uint32_t Mu = (uint32_t)M;
+  const double invM = lt.inv_m[l];
+  for (int i = threadIdx.x; i < 8 * 49; i += blockDim.x) {
+    const int g = i / 49, e = i % 49;
+    double v = 0.0;
+    if (g < G) {
+      const int m = bs.order[g];
+      if (e < m * m) v = bs.scale[g] * bs.pc[bs_poff(m) + e];
+    }
+    pcg[g][e] = v;
+  }
+  if (threadIdx.x < 32) {  // this lattice's units, in slot order
+    int cnt = 0;
+    for (int b = 0; b < ut.nunits; b += 32) {
+      const int j = b + (int)threadIdx.x;
+      const bool hit = j < ut.nunits && ut.lat[j] == l;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) slot[cnt + __popc(bal & ((1u << threadIdx.x) - 1u))] = j;
+      cnt += __popc(bal);
+    }
+    if (threadIdx.x == 0) {
+      nslot = cnt;
+      int np = 0;
+      const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+      for (int g = 0; g < G; ++g) {
+        int last = -1;
+        for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
+          const int c = bs.comps[e];
+          if (c >= t1) continue;
+          const int m = bs.order[g];
+          const uint64_t z = (uint64_t)lt.z[l * t1 + c];
+          const uint64_t dl = ((S % (uint64_t)M) * z) % (uint64_t)M;  // (S z) mod M
+          const uint64_t md = (uint64_t)m * dl;
+          pz[np] = (uint32_t)z;
+          pdq[np] = (uint32_t)(md / (uint64_t)M);
+          pdr[np] = (uint32_t)(md % (uint64_t)M);
+          pmeta[np] = m | (g << 4);
+          last = np++;
+        }
+        if (last >= 0) pmeta[last] |= 1 << 8;
+      }
+      npos = np;
+    }
+  }
+  __syncthreads();
+  const int ns = nslot, np = npos;
+  if (ns == 0) return;
+  const int64_t n0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int c0 = 0; c0 < ns; c0 += BS_SLOTS) {
+    const int nc = min(BS_SLOTS, ns - c0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nc * G; q += blockDim.x) {  // anchor factors; groups w/o lattice coords
+      const int sl = q / G, g = q % G;
+      const int it = ut.it[slot[c0 + sl]];
+      const int m = bs.order[g];
+      double k = 1.0;
+      for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
+        const int c = bs.comps[e];
+        if (c >= t1) {
+          double u = (double)m * at.a[it * tail + (c - t1)];
+          int iv = (int)u;
+          if (iv > m - 1) iv = m - 1;
+          const double t = u - (double)iv;
+          const double* cf = &pcg[g][iv * m];
+          double v = cf[m - 1];
+          for (int kk = m - 2; kk >= 0; --kk) v = fma(v, t, cf[kk]);
+          k = k * v;
+        }
+      }
+      K[sl][g] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      double c = 0.0;
+      for (int g = 0; g < G; ++g) {
+        bool has = false;
+        for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) has |= bs.comps[e] < t1;
+        if (!has) c += K[threadIdx.x][g];
+      }
+      C0[threadIdx.x] = c;
+    }
+    __syncthreads();
+    if (n0 >= M) continue;  // no barrier below: every thread meets the next slot chunk's barriers
+    uint32_t iv[BSC_NP], rem[BSC_NP];
+#pragma unroll
+    for (int p = 0; p < BSC_NP; ++p) {
+      iv[p] = 0u;
+      rem[p] = 0u;
+      if (p < np) {  // exact start: Q = m (n0 z mod M) = iv M + rem
+        const uint64_t r = ((uint64_t)n0 * pz[p]) % (uint64_t)M;
+        const uint64_t Q = (uint64_t)(pmeta[p] & 15) * r;
+        iv[p] = (uint32_t)(Q / (uint64_t)M);
+        rem[p] = (uint32_t)(Q - (uint64_t)iv[p] * (uint64_t)M);
+      }
+    }
+    for (int64_t n = n0; n < M; n += (int64_t)gridDim.x * blockDim.x) {
+      double tot[BS_SLOTS];
+#pragma unroll
+      for (int s = 0; s < BS_SLOTS; ++s) tot[s] = s < nc ? C0[s] : 0.0;
+      double term = 1.0;
+#pragma unroll
+      for (int p = 0; p < BSC_NP; ++p) {
+        if (p < np) {
+          const int meta = pmeta[p];
+          const int m = meta & 15, g = (meta >> 4) & 15;
+          const double t = (double)rem[p] * invM;
+          const double* cf = &pcg[g][iv[p] * m];
+          double v = cf[m - 1];
+          for (int kk = m - 2; kk >= 0; --kk) v = fma(v, t, cf[kk]);
+          term = term * v;
+          if (meta & 256) {
+#pragma unroll
+            for (int s = 0; s < BS_SLOTS; ++s)
+              if (s < nc) tot[s] += K[s][g] * term;
+            term = 1.0;
+          }
+          const uint32_t r2 = rem[p] + pdr[p];
+          const uint32_t cy = r2 >= Mu ? 1u : 0u;
+          rem[p] = r2 - (cy ? Mu : 0u);
+          const uint32_t i2 = iv[p] + pdq[p] + cy;
+          iv[p] = i2 >= (uint32_t)m ? i2 - (uint32_t)m : i2;
+        }
+      }
+      double2 cv = make_double2(1.0, 0.0);
+      if (apply_chirp) cv = __ldg(&chirp[lt.off[l] + n]);
+#pragma unroll
+      for (int s = 0; s < BS_SLOTS; ++s)
+        if (s < nc) {
+          double2* ub = buf + (int64_t)slot[c0 + s] * ustride;
+          __stcs(&ub[n], apply_chirp ? make_double2(tot[s] * cv.x, tot[s] * cv.y) : make_double2(tot[s], 0.0));
+        }
+    }
+  }
+}
+
 // lattice nodes for a host-callback oracle: pts[n, c] (row-major, d columns)
 template <bool FAST>
 __global__ void lattice_nodes_kernel(LatTable lt, int l, int d, AnchorTable at, int it,
@@ -669,12 +831,24 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
     int bx = (int)((mmax + 255) / 256);
     const int cap = (num_sms * 8 + lt.nlat - 1) / lt.nlat;
     if (bx > cap) bx = cap;
-    if (fast)
+    int npos = 0;
+    for (int g = 0; g < bs.ngroups; ++g)
+      for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) npos += bs.comps[e] < lt.d;
+    prof_mark(PROF_SAMPLE, true, st);
+    if (npos <= BSC_NP && bs.ngroups <= 8) {
+      // chains: a grid of about two CTAs per SM in total, so each thread walks many nodes
+      int bxc = (int)((mmax + 255) / 256);
+      const int capc = (num_sms * 2 + lt.nlat - 1) / lt.nlat;
+      if (bxc > capc) bxc = capc;
+      sample_bspline_chain_kernel<<<dim3(bxc, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
+                                                                     apply_chirp ? 1 : 0);
+    } else if (fast)
       sample_bspline_lat_kernel<true><<<dim3(bx, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
                                                                          apply_chirp ? 1 : 0);
     else
       sample_bspline_lat_kernel<false><<<dim3(bx, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
                                                                           apply_chirp ? 1 : 0);
+    prof_mark(PROF_SAMPLE, false, st);
     SFFT_CHECK_LAUNCH();
     return 0;
   }
