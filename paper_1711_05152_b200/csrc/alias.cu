@@ -17,16 +17,18 @@
 // result is exact for any multiplicity and the bitmaps (sum_l M_l / 4 bytes)
 // stay L2-resident even at |J| = 6.5e5, d = 20 (29 lattices, ~9 MB).
 //
-// Default path (alias_cluster_kernel): no L2 atomics at all.  Each thread-
-// block cluster (16 CTAs where the GPU allows, else 8) owns a group of
-// lattices and holds their two bitmaps in distributed shared memory, bins
-// partitioned over the cluster's CTAs; every CTA takes a contiguous slice of
-// the candidates, marks seen1/seen2 with shared::cluster atomics, and after a
-// cluster barrier reads seen2 back and writes one alias-free bit-plane word
-// per warp and lattice (ballot).  alias_planes_kernel then folds the planes
-// into the per-candidate 64-bit masks and the stats.  The L2-atomic kernels
-// below remain for lattice sizes whose bitmaps exceed a cluster's shared
-// memory.
+// Default path (alias_cluster_kernel), when a lattice's two bitmaps fit in a
+// CTA's shared memory (M up to ~880k): no global atomics.  A thread-block
+// cluster (16 CTAs where the GPU allows, else 8) owns a group of lattices;
+// each CTA takes a contiguous slice of the candidates and builds the full
+// 2-bit histograms of its slice with shared-memory atomics (A); the cluster
+// then folds the 16 partial histograms through distributed shared memory,
+// each CTA one range of words (B: seen2 |= s2_c | (seen1 & s1_c), seen1 |=
+// s1_c, 16-byte DSMEM loads), copies the folded seen2 of every range back
+// from its owner (C) and reads each candidate's alias-free bit locally (D),
+// writing one bit-plane word per warp and lattice.  alias_planes_kernel then
+// folds the planes into the per-candidate 64-bit masks and the stats.
+// Larger lattices (config 3, M ~ 1.3e6) use the L2-atomic kernels below.
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -161,31 +163,18 @@ __device__ __forceinline__ uint32_t dsm_map(uint32_t local, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
 }
-__device__ __forceinline__ uint32_t dsm_or(uint32_t addr, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.shared::cluster.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void dsm_red_or(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t dsm_ld(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
-}
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-constexpr int ACG = 4;     // lattices whose cluster atomics are issued back to back
 constexpr int ACT = 1024;  // threads per CTA (one CTA per SM; latency hiding by width)
 
 template <int DM, bool FAST>
 __global__ void __launch_bounds__(ACT)
 alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, AliasGroups ag,
                      uint32_t* __restrict__ planes, int64_t pwords) {
-  extern __shared__ uint32_t bm[];  // [g][seen1 | seen2][wpc], then (keep) residues [g][sl]
+  // [g][seen1 | seen2][W] full bitmaps of this CTA's candidates, then (keep) residues [g][sl]
+  extern __shared__ uint32_t bm[];
   uint32_t rank, nct;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
@@ -193,41 +182,63 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
   const int lb = ag.l0 + cid * ag.g;
   const int le = min(ag.l0 + ag.nl, lb + ag.g);
   const int ng = le - lb;
-  const int wpc = ag.wpc;
-  uint32_t* res_s = bm + 2 * ag.g * wpc;
-  for (int w = threadIdx.x; w < ng * 2 * wpc; w += blockDim.x) bm[w] = 0u;
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(bm);
-  cluster_barrier();  // every CTA's bitmaps are zero before the first remote atomic
+  const int W = ag.wpc;  // words per bitmap (multiple of 4 * cluster size)
+  uint32_t* res_s = bm + 2 * ag.g * W;
+  for (int w = threadIdx.x; w < ng * 2 * W; w += blockDim.x) bm[w] = 0u;
+  __syncthreads();
   const int64_t i0 = min(n, (int64_t)rank * ag.sl);
   const int64_t i1 = min(n, i0 + ag.sl);
   const int d = lt.d;
+  // A: local 2-bit saturating histograms of this CTA's candidates
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     int32_t k[DM];
 #pragma unroll
     for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
-    for (int jb = 0; jb < ng; jb += ACG) {
-      uint32_t adr[ACG], bit[ACG], old[ACG];
-#pragma unroll
-      for (int q = 0; q < ACG; ++q) {
-        const int j = jb + q;
-        bit[q] = 0u;
-        old[q] = 0u;
-        if (j < ng) {
-          const uint32_t r = (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
-          if (ag.keep) res_s[(int64_t)j * ag.sl + (i - i0)] = r;
-          const uint32_t gw = r >> 5;
-          const uint32_t owner = gw / (uint32_t)wpc;
-          adr[q] = dsm_map(base + 4u * ((uint32_t)(2 * j * wpc) + gw - owner * (uint32_t)wpc), owner);
-          bit[q] = 1u << (r & 31);
-          old[q] = dsm_or(adr[q], bit[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < ACG; ++q)
-        if (old[q] & bit[q]) dsm_red_or(adr[q] + 4u * (uint32_t)wpc, bit[q]);
+    for (int j = 0; j < ng; ++j) {
+      const uint32_t r = (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
+      if (ag.keep) res_s[(int64_t)j * ag.sl + (i - i0)] = r;
+      uint32_t* s1 = bm + 2 * j * W;
+      const uint32_t bit = 1u << (r & 31);
+      const uint32_t old = atomicOr(&s1[r >> 5], bit);
+      if (old & bit) atomicOr(&s1[W + (r >> 5)], bit);
     }
   }
-  cluster_barrier();  // all marks landed
+  cluster_barrier();
+  // B: fold the cluster's histograms on this CTA's quarter-words
+  // (seen2 |= s2_c | (seen1 & s1_c); seen1 |= s1_c), result into local seen2
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(bm);
+  const int q4 = W / 4 / (int)nct;  // uint4 words per CTA and bitmap
+  for (int x = threadIdx.x; x < ng * q4; x += blockDim.x) {
+    const int j = x / q4;
+    const int w4 = (int)rank * q4 + x % q4;
+    const uint32_t o1 = 4u * (uint32_t)(2 * j * W + 4 * w4), o2 = o1 + 4u * (uint32_t)W;
+    uint4 a1 = make_uint4(0, 0, 0, 0), a2 = make_uint4(0, 0, 0, 0);
+    for (uint32_t c = 0; c < nct; ++c) {
+      uint4 x1, x2;
+      asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(x1.x), "=r"(x1.y), "=r"(x1.z), "=r"(x1.w) : "r"(dsm_map(base + o1, c)) : "memory");
+      asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(x2.x), "=r"(x2.y), "=r"(x2.z), "=r"(x2.w) : "r"(dsm_map(base + o2, c)) : "memory");
+      a2.x |= x2.x | (a1.x & x1.x); a2.y |= x2.y | (a1.y & x1.y);
+      a2.z |= x2.z | (a1.z & x1.z); a2.w |= x2.w | (a1.w & x1.w);
+      a1.x |= x1.x; a1.y |= x1.y; a1.z |= x1.z; a1.w |= x1.w;
+    }
+    *(uint4*)(bm + 2 * j * W + W + 4 * w4) = a2;  // only this CTA reads this range of its seen2
+  }
+  cluster_barrier();
+  // C: the folded seen2 of every range, from its owner, into local seen1
+  for (int x = threadIdx.x; x < ng * (W / 4); x += blockDim.x) {
+    const int j = x / (W / 4);
+    const int w4 = x % (W / 4);
+    const uint32_t owner = (uint32_t)(w4 / q4);
+    uint4 v;
+    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(dsm_map(base + 4u * (uint32_t)(2 * j * W + W + 4 * w4), owner)) : "memory");
+    *(uint4*)(bm + 2 * j * W + 4 * w4) = v;
+  }
+  __syncthreads();
+  // D: alias-free bits (final seen2 clear), one bit-plane word per warp and lattice
   const int lane = threadIdx.x & 31;
   for (int64_t ib = i0; ib < i1; ib += blockDim.x) {
     const int64_t i = ib + threadIdx.x;
@@ -237,33 +248,19 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
 #pragma unroll
       for (int c = 0; c < DM; ++c) k[c] = (live && c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
     }
-    for (int jb = 0; jb < ng; jb += ACG) {
-      uint32_t v[ACG], sh[ACG];
-#pragma unroll
-      for (int q = 0; q < ACG; ++q) {
-        const int j = jb + q;
-        v[q] = ~0u;
-        sh[q] = 0u;
-        if (live && j < ng) {
-          const uint32_t r = ag.keep ? res_s[(int64_t)j * ag.sl + (i - i0)]
-                                     : (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
-          const uint32_t gw = r >> 5;
-          const uint32_t owner = gw / (uint32_t)wpc;
-          v[q] = dsm_ld(dsm_map(base + 4u * ((uint32_t)((2 * j + 1) * wpc) + gw - owner * (uint32_t)wpc), owner));
-          sh[q] = r & 31u;
-        }
+    for (int j = 0; j < ng; ++j) {
+      uint32_t free = 0u;
+      if (live) {
+        const uint32_t r = ag.keep ? res_s[(int64_t)j * ag.sl + (i - i0)]
+                                   : (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
+        free = ((bm[2 * j * W + (r >> 5)] >> (r & 31)) & 1u) ? 0u : 1u;
       }
-#pragma unroll
-      for (int q = 0; q < ACG; ++q) {
-        const int j = jb + q;
-        const uint32_t free = (live && !((v[q] >> sh[q]) & 1u)) ? 1u : 0u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, free);
-        if (lane == 0 && j < ng && ib + (threadIdx.x & ~31) < i1)
-          planes[(int64_t)(lb + j - ag.l0) * pwords + ((ib + threadIdx.x) >> 5)] = bal;
-      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, free);
+      if (lane == 0 && ib + (threadIdx.x & ~31) < i1)
+        planes[(int64_t)(lb + j - ag.l0) * pwords + ((ib + threadIdx.x) >> 5)] = bal;
     }
   }
-  cluster_barrier();  // no CTA leaves while others may still read its bitmaps
+  cluster_barrier();  // no CTA leaves while others may still read its seen2
 }
 
 // alias-free bit-planes of lattices [l0, l1) -> masks (OR-ed into the masks of
@@ -299,7 +296,7 @@ alias_planes_kernel(int64_t n, int l0, int l1, const uint32_t* __restrict__ plan
 }
 
 namespace {
-constexpr size_t ALIAS_SMEM_MAX = 200 * 1024;
+constexpr size_t ALIAS_SMEM_MAX = 220 * 1024;
 
 // Cluster geometry for lattices [l0, l1): the largest cluster (16 CTAs where
 // allowed, else 8) and the fewest lattices per cluster g such that the
@@ -319,7 +316,7 @@ bool alias_cluster_plan(const LatTable& lt, int64_t n, int l0, int l1, int& cl, 
   const void* fn = (const void*)alias_cluster_kernel<DM, FAST>;
   const int nl = l1 - l0;
   for (int c : {16, 8}) {
-    const int wpc = (int)((mw + c - 1) / c);
+    const int wpc = (int)((mw + 4 * c - 1) / (4 * c)) * 4 * c;  // full bitmap words, a multiple of 4 c
     const size_t per_lat = (size_t)2 * wpc * 4;
     if (per_lat > ALIAS_SMEM_MAX) continue;
     if (c > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {

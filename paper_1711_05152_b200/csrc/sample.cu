@@ -562,17 +562,30 @@ sample_bspline_lat_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable
 
 // K1b main variant: the lattice-shared sampler with the per-coordinate work
 // made incremental.  Coordinate c of node n has u = m x = m (n z_c mod M) / M;
-// the thread walks its nodes n0, n0 + S, n0 + 2S, ... (S = grid stride) and
-// carries, per lattice coordinate, Q = m (n z_c mod M) as (piece iv, rem) with
-// Q = iv M + rem: one step adds m (S z_c mod M) = Dq M + Dr with integer
-// carries, so B_m(u) is the piece iv polynomial at t = rem / M (exact rational,
-// one multiply by 1/M) -- no modular product, no float floor per node.
-// Coordinates are laid out group-major ("positions") so the registers of
-// every position have compile-time indices (NP = 16 positions at most).
-constexpr int BSC_NP = 16;
+// each CTA owns a contiguous node range of one lattice (CTAs dealt to the
+// lattices in proportion to M_l) and each thread walks n0, n0 + 256, ...,
+// carrying per lattice coordinate Q = m (n z_c mod M) as (piece iv, rem),
+// Q = iv M + rem: one step adds m (256 z_c mod M) = Dq M + Dr with integer
+// carries, so B_m(u) is the piece iv polynomial at t = rem / M (exact
+// rational, one multiply by 1/M) -- no modular product, no float floor per
+// node.  Coordinates are laid out group-major ("positions") so that the
+// registers of every position have compile-time indices (NP positions at most).
+struct BsGrid {
+  int ncta;                    // CTAs of the launch
+  int start[SFFT_LMAX + 1];    // first CTA of lattice l
+};
 
+// x mod M for x < 2^63, M < 2^31 (double quotient, off by at most one)
+__device__ __forceinline__ uint64_t mod_u64(uint64_t x, uint64_t M, double invM) {
+  int64_t r = (int64_t)x - (int64_t)((uint64_t)__dmul_rn((double)x, invM) * M);
+  if (r < 0) r += (int64_t)M;
+  if (r >= (int64_t)M) r -= (int64_t)M;
+  return (uint64_t)r;
+}
+
+template <int NP>
 __global__ void __launch_bounds__(256)
-sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at,
+sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at, BsGrid bg,
                             const double2* __restrict__ chirp, double2* __restrict__ buf, int64_t ustride,
                             int apply_chirp) {
   __shared__ double pcg[8][49];      // group g's piece polynomials of order m_g, scaled by C_m m
@@ -580,15 +593,20 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
   __shared__ double C0[BS_SLOTS];    // groups without lattice coordinates: their constant terms
   __shared__ int slot[SFFT_UMAX];
   __shared__ int nslot, npos;
-  __shared__ int pmeta[BSC_NP];      // m | group << 4 | (last position of its group) << 8
-  __shared__ uint32_t pz[BSC_NP], pdq[BSC_NP], pdr[BSC_NP];
-  const int l = blockIdx.y;
+  __shared__ int pmeta[NP];          // m | group << 4 | (last position of its group) << 8
+  __shared__ uint32_t pz[NP], pdq[NP], pdr[NP];
+  int l = 0;
+  while (l + 1 < lt.nlat && (int)blockIdx.x >= bg.start[l + 1]) ++l;
   const int t1 = lt.d;
   const int tail = bs.d - t1;
   const int G = bs.ngroups;
   const int64_t M = lt.m[l];
   const uint32_t Mu = (uint32_t)M;
   const double invM = lt.inv_m[l];
+  // this CTA's node range of lattice l (contiguous, a multiple of 256 wide)
+  const int cl = (int)blockIdx.x - bg.start[l], ncl = bg.start[l + 1] - bg.start[l];
+  const int64_t span = ((M + ncl - 1) / ncl + 255) / 256 * 256;
+  const int64_t nb = (int64_t)cl * span, ne = min(M, nb + span);
   for (int i = threadIdx.x; i < 8 * 49; i += blockDim.x) {
     const int g = i / 49, e = i % 49;
     double v = 0.0;
@@ -610,15 +628,14 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
     if (threadIdx.x == 0) {
       nslot = cnt;
       int np = 0;
-      const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
       for (int g = 0; g < G; ++g) {
         int last = -1;
         for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
           const int c = bs.comps[e];
-          if (c >= t1) continue;
+          if (c >= t1 || np >= NP) continue;
           const int m = bs.order[g];
           const uint64_t z = (uint64_t)lt.z[l * t1 + c];
-          const uint64_t dl = ((S % (uint64_t)M) * z) % (uint64_t)M;  // (S z) mod M
+          const uint64_t dl = (256u * z) % (uint64_t)M;  // (256 z) mod M
           const uint64_t md = (uint64_t)m * dl;
           pz[np] = (uint32_t)z;
           pdq[np] = (uint32_t)(md / (uint64_t)M);
@@ -634,11 +651,11 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
   __syncthreads();
   const int ns = nslot, np = npos;
   if (ns == 0) return;
-  const int64_t n0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n0 = nb + threadIdx.x;
   for (int c0 = 0; c0 < ns; c0 += BS_SLOTS) {
     const int nc = min(BS_SLOTS, ns - c0);
     __syncthreads();
-    for (int q = threadIdx.x; q < nc * G; q += blockDim.x) {  // anchor factors; groups w/o lattice coords
+    for (int q = threadIdx.x; q < nc * G; q += blockDim.x) {  // anchor factors
       const int sl = q / G, g = q % G;
       const int it = ut.it[slot[c0 + sl]];
       const int m = bs.order[g];
@@ -646,7 +663,7 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
       for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) {
         const int c = bs.comps[e];
         if (c >= t1) {
-          double u = (double)m * at.a[it * tail + (c - t1)];
+          const double u = (double)m * at.a[it * tail + (c - t1)];
           int iv = (int)u;
           if (iv > m - 1) iv = m - 1;
           const double t = u - (double)iv;
@@ -659,7 +676,7 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
       K[sl][g] = k;
     }
     __syncthreads();
-    if (threadIdx.x < nc) {
+    if (threadIdx.x < nc) {  // groups without lattice coordinates contribute their anchor product
       double c = 0.0;
       for (int g = 0; g < G; ++g) {
         bool has = false;
@@ -669,26 +686,27 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
       C0[threadIdx.x] = c;
     }
     __syncthreads();
-    if (n0 >= M) continue;  // no barrier below: every thread meets the next slot chunk's barriers
-    uint32_t iv[BSC_NP], rem[BSC_NP];
+    if (n0 >= ne) continue;  // no barrier below: every thread meets the next slot chunk's barriers
+    uint32_t iv[NP], rem[NP];
 #pragma unroll
-    for (int p = 0; p < BSC_NP; ++p) {
+    for (int p = 0; p < NP; ++p) {
       iv[p] = 0u;
       rem[p] = 0u;
       if (p < np) {  // exact start: Q = m (n0 z mod M) = iv M + rem
-        const uint64_t r = ((uint64_t)n0 * pz[p]) % (uint64_t)M;
+        const uint64_t r = mod_u64((uint64_t)n0 * pz[p], (uint64_t)M, invM);
         const uint64_t Q = (uint64_t)(pmeta[p] & 15) * r;
-        iv[p] = (uint32_t)(Q / (uint64_t)M);
-        rem[p] = (uint32_t)(Q - (uint64_t)iv[p] * (uint64_t)M);
+        const uint64_t qr = mod_u64(Q, (uint64_t)M, invM);
+        iv[p] = (uint32_t)__double2ll_rn((double)(Q - qr) * invM);  // exact: Q - qr = iv M, iv < 8
+        rem[p] = (uint32_t)qr;
       }
     }
-    for (int64_t n = n0; n < M; n += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t n = n0; n < ne; n += 256) {
       double tot[BS_SLOTS];
 #pragma unroll
       for (int s = 0; s < BS_SLOTS; ++s) tot[s] = s < nc ? C0[s] : 0.0;
       double term = 1.0;
 #pragma unroll
-      for (int p = 0; p < BSC_NP; ++p) {
+      for (int p = 0; p < NP; ++p) {
         if (p < np) {
           const int meta = pmeta[p];
           const int m = meta & 15, g = (meta >> 4) & 15;
@@ -835,13 +853,27 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
     for (int g = 0; g < bs.ngroups; ++g)
       for (int e = bs.start[g]; e < bs.start[g + 1]; ++e) npos += bs.comps[e] < lt.d;
     prof_mark(PROF_SAMPLE, true, st);
-    if (npos <= BSC_NP && bs.ngroups <= 8) {
-      // chains: a grid of about two CTAs per SM in total, so each thread walks many nodes
-      int bxc = (int)((mmax + 255) / 256);
-      const int capc = (num_sms * 2 + lt.nlat - 1) / lt.nlat;
-      if (bxc > capc) bxc = capc;
-      sample_bspline_chain_kernel<<<dim3(bxc, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
-                                                                     apply_chirp ? 1 : 0);
+    if (npos <= 16 && bs.ngroups <= 8) {
+      // CTAs dealt to the lattices in proportion to their sizes; one wave
+      // (resident CTAs per SM: 3 for <= 8 positions, 2 for <= 16, by registers)
+      BsGrid bg;
+      int64_t tot = 0;
+      for (int l = 0; l < lt.nlat; ++l) tot += lt.m[l];
+      const int per_sm = npos <= 8 ? 3 : 2;
+      const int ncta = num_sms * per_sm > lt.nlat ? num_sms * per_sm : lt.nlat;
+      int64_t acc = 0;
+      for (int l = 0; l < lt.nlat; ++l) {
+        bg.start[l] = (int)((acc * (ncta - lt.nlat)) / tot) + l;  // at least one CTA per lattice
+        acc += lt.m[l];
+      }
+      bg.start[lt.nlat] = ncta;
+      bg.ncta = ncta;
+      if (npos <= 8)
+        sample_bspline_chain_kernel<8><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
+                                                            apply_chirp ? 1 : 0);
+      else
+        sample_bspline_chain_kernel<16><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
+                                                             apply_chirp ? 1 : 0);
     } else if (fast)
       sample_bspline_lat_kernel<true><<<dim3(bx, lt.nlat), 256, 0, st>>>(ut, lt, bs, at, chirp, buf, ustride,
                                                                          apply_chirp ? 1 : 0);

@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--rep")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--no-shares", action="store_true", help="do not replace launch_shares in ncu_summary.json")
     a = ap.parse_args()
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
@@ -68,7 +69,8 @@ def main():
             w.writerow(["kernel", "launches", "total_us", "mean_us", "share"])
             for k in sorted(tot, key=lambda k: -tot[k]):
                 w.writerow([k, cnt[k], f"{tot[k] / 1e3:.1f}", f"{tot[k] / cnt[k] / 1e3:.2f}", f"{tot[k] / allns:.4f}"])
-        summary["launch_shares"] = {k: tot[k] / allns for k in tot}
+        if not a.no_shares:
+            summary["launch_shares"] = {k: tot[k] / allns for k in tot}
         print(out.read_text())
     if a.rep:
         recs, units = raw_metrics(Path(a.rep))
