@@ -57,8 +57,7 @@ alias_mark_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t k[DM];
-#pragma unroll
-    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    load_cand<DM>(k, freqs, n, i, d);
     // groups of AB lattices: the group's first-bitmap atomics are issued back
     // to back (independent), then the rare second-bitmap ones
     for (int lb = l0; lb < lt.nlat; lb += AB) {
@@ -104,8 +103,7 @@ alias_mask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t k[DM];
-#pragma unroll
-    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    load_cand<DM>(k, freqs, n, i, d);
     uint64_t mask = l0 > 0 ? masks[i] : 0ull;
     for (int lb = l0; lb < lt.nlat; lb += AB) {
       uint32_t wv[AB];
@@ -192,8 +190,7 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
   // A: local 2-bit saturating histograms of this CTA's candidates
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     int32_t k[DM];
-#pragma unroll
-    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    load_cand<DM>(k, freqs, n, i, d);
     for (int j = 0; j < ng; ++j) {
       const uint32_t r = (uint32_t)SFFT_RES(DM, FAST, k, lt, lb + j);
       if (ag.keep) res_s[(int64_t)j * ag.sl + (i - i0)] = r;
@@ -245,8 +242,7 @@ alias_cluster_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, 
     const bool live = i < i1;
     int32_t k[DM];
     if (!ag.keep) {
-#pragma unroll
-      for (int c = 0; c < DM; ++c) k[c] = (live && c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+      load_cand<DM>(k, freqs, n, i, d, live);
     }
     for (int j = 0; j < ng; ++j) {
       uint32_t free = 0u;

@@ -85,6 +85,20 @@ __device__ __forceinline__ int64_t mulmod(int64_t a, int64_t b, int64_t m, doubl
   return (int64_t)(((uint64_t)a * (uint64_t)b) % (uint64_t)m);
 }
 
+// Components of candidate i of a component-major (d x n) int32 set into
+// registers: one pointer walk (a 64-bit add per component) instead of a
+// 64-bit multiply-add address per component.
+template <int DM>
+__device__ __forceinline__ void load_cand(int32_t (&k)[DM], const int32_t* __restrict__ freqs, int64_t n,
+                                          int64_t i, int d, bool live = true) {
+  const int32_t* p = freqs + i;
+#pragma unroll
+  for (int c = 0; c < DM; ++c) {
+    k[c] = (live && c < d) ? __ldg(p) : 0;
+    p += n;
+  }
+}
+
 // Residue k . z mod M of one candidate (components in registers).
 // FAST requires sum_c |k_c| * z_c < 2^52 (host-checked); with i32 != 0 the
 // host has also checked d * kmax * M < 2^31, and the sum runs in int32 plus a

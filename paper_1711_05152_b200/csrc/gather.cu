@@ -44,8 +44,7 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
     int cnt = 0;
     if (mask) {
       int32_t kv[DM];
-#pragma unroll
-      for (int c = 0; c < DM; ++c) kv[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + k]) : 0;
+      load_cand<DM>(kv, freqs, n, k, d);
       uint64_t mm = mask;
       while (mm) {
         const int l = __ffsll((long long)mm) - 1;
@@ -162,8 +161,7 @@ gather_units_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
        k += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t mask = masks[k];
     int32_t kv[DM];
-#pragma unroll
-    for (int c = 0; c < DM; ++c) kv[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + k]) : 0;
+    load_cand<DM>(kv, freqs, n, k, d);
     for (int j = 0; j < ut.nunits; ++j) {
       const int l = ut.lat[j];
       double2 t = make_double2(0.0, 0.0);
@@ -813,8 +811,7 @@ __global__ void residues_kernel(const int32_t* __restrict__ freqs, int64_t n, La
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t k[DM];
-#pragma unroll
-    for (int c = 0; c < DM; ++c) k[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + i]) : 0;
+    load_cand<DM>(k, freqs, n, i, d);
     for (int l = 0; l < lt.nlat; ++l)
       out[(int64_t)l * n + i] = SFFT_RES(DM, FAST, k, lt, l);
   }

@@ -138,8 +138,7 @@ pack_units_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, con
     const int64_t t0 = (int64_t)q * ts;
     if (m) {
       int32_t kv[DM];
-#pragma unroll
-      for (int c = 0; c < DM; ++c) kv[c] = (c < d) ? __ldg(&freqs[(int64_t)c * n + k]) : 0;
+      load_cand<DM>(kv, freqs, n, k, d);
       int lprev = -1;
       int64_t r = 0;
       for (int j = 0; j < ut.nunits; ++j) {
