@@ -17,8 +17,11 @@
 // result is exact for any multiplicity and the bitmaps (sum_l M_l / 4 bytes)
 // stay L2-resident even at |J| = 6.5e5, d = 20 (29 lattices, ~9 MB).
 //
-// Default path (alias_cluster_kernel), when a lattice's two bitmaps fit in a
-// CTA's shared memory (M up to ~880k): no global atomics.  A thread-block
+// Cluster path (alias_cluster_kernel, opt-in: SFFT_B200_ALIAS_CLUSTER=1; at
+// config 1 it measured 60 us against the L2-atomic kernels' 43 us, the
+// per-cluster re-reads of J and the DSMEM fold outweigh the atomics saved),
+// when a lattice's two bitmaps fit in a CTA's shared memory (M up to ~880k):
+// no global atomics.  A thread-block
 // cluster (16 CTAs where the GPU allows, else 8) owns a group of lattices;
 // each CTA takes a contiguous slice of the candidates and builds the full
 // 2-bit histograms of its slice with shared-memory atomics (A); the cluster
@@ -28,7 +31,8 @@
 // from its owner (C) and reads each candidate's alias-free bit locally (D),
 // writing one bit-plane word per warp and lattice.  alias_planes_kernel then
 // folds the planes into the per-candidate 64-bit masks and the stats.
-// Larger lattices (config 3, M ~ 1.3e6) use the L2-atomic kernels below.
+// The default, and larger lattices (config 3, M ~ 1.3e6): the L2-atomic
+// kernels below.
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -302,9 +306,11 @@ constexpr size_t ALIAS_SMEM_MAX = 220 * 1024;
 template <int DM, bool FAST>
 bool alias_cluster_plan(const LatTable& lt, int64_t n, int l0, int l1, int& cl, AliasGroups& ag, int& clusters,
                         size_t& smem) {
+  // opt-in (SFFT_B200_ALIAS_CLUSTER=1): measured 60 us against the L2-atomic
+  // kernels' 43 us at config 1 (tools/alias_ab.py, profiles/r02_alias_ab.jsonl)
   static const bool disabled = [] {
     const char* e = getenv("SFFT_B200_ALIAS_CLUSTER");
-    return e && strcmp(e, "0") == 0;
+    return !(e && strcmp(e, "1") == 0);
   }();
   if (disabled) return false;
   int64_t mw = 1;

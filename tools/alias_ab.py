@@ -1,7 +1,7 @@
 """K3 alias kernels A/B: mean device time of sfft_alias_masks_range over the
 first chunk of lattices (library CUDA events), at config-1 size (|J| = 1e5,
 d = 10) and config-3 size (|J| = 6.5e5, d = 20).  The path is chosen by
-SFFT_B200_ALIAS_CLUSTER (unset: cluster/DSMEM where it fits; 0: L2 atomics)."""
+SFFT_B200_ALIAS_CLUSTER (unset: L2 atomics; 1: cluster/DSMEM where it fits)."""
 import ctypes
 import json
 import os
@@ -21,7 +21,7 @@ def main():
     from paper_1711_05152_b200.workloads import distinct_rows
     dev = get_device()
     torch = dev.torch
-    out = {"path": "l2" if os.environ.get("SFFT_B200_ALIAS_CLUSTER") == "0" else "cluster"}
+    out = {"path": "cluster" if os.environ.get("SFFT_B200_ALIAS_CLUSTER") == "1" else "l2"}
     for name, n, d in (("config1", 100_000, 10), ("config3", 650_000, 20)):
         rows = distinct_rows(np.random.default_rng(1), n, d, 32)
         cand = DeviceFreqs.from_host(dev, rows)
