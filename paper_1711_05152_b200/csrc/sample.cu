@@ -584,11 +584,11 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t x, uint64_t M, double invM)
 }
 
 template <int NP>
-__global__ void __launch_bounds__(256, NP <= 10 ? 3 : 2)
+__global__ void __launch_bounds__(256)
 sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at, BsGrid bg,
                             const double2* __restrict__ chirp, double2* __restrict__ buf, int64_t ustride,
                             int apply_chirp) {
-  __shared__ __align__(16) double pcg[8][7][8];  // group g, piece iv: degree-6 padded polynomial, x C_m m
+  __shared__ double pcg[8][49];      // group g's piece polynomials of order m_g, scaled by C_m m
   __shared__ double K[BS_SLOTS][8];  // anchor factors per slot and group
   __shared__ double C0[BS_SLOTS];    // groups without lattice coordinates: their constant terms
   __shared__ int slot[SFFT_UMAX];
@@ -607,14 +607,14 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
   const int cl = (int)blockIdx.x - bg.start[l], ncl = bg.start[l + 1] - bg.start[l];
   const int64_t span = ((M + ncl - 1) / ncl + 255) / 256 * 256;
   const int64_t nb = (int64_t)cl * span, ne = min(M, nb + span);
-  for (int i = threadIdx.x; i < 8 * 7 * 8; i += blockDim.x) {
-    const int g = i / 56, iv = (i / 8) % 7, e = i % 8;
+  for (int i = threadIdx.x; i < 8 * 49; i += blockDim.x) {
+    const int g = i / 49, e = i % 49;
     double v = 0.0;
     if (g < G) {
       const int m = bs.order[g];
-      if (iv < m && e < m) v = bs.scale[g] * bs.pc[bs_poff(m) + iv * m + e];
+      if (e < m * m) v = bs.scale[g] * bs.pc[bs_poff(m) + e];
     }
-    pcg[g][iv][e] = v;
+    pcg[g][e] = v;
   }
   if (threadIdx.x < 32) {  // this lattice's units, in slot order
     int cnt = 0;
@@ -667,9 +667,9 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
           int iv = (int)u;
           if (iv > m - 1) iv = m - 1;
           const double t = u - (double)iv;
-          const double* cf = pcg[g][iv];
-          double v = cf[6];
-          for (int kk = 5; kk >= 0; --kk) v = fma(v, t, cf[kk]);
+          const double* cf = &pcg[g][iv * m];
+          double v = cf[m - 1];
+          for (int kk = m - 2; kk >= 0; --kk) v = fma(v, t, cf[kk]);
           k = k * v;
         }
       }
@@ -701,25 +701,6 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
       }
     }
     for (int64_t n = n0; n < ne; n += 256) {
-      // every position's factor independently (branch-free degree-6 Horner on
-      // the padded pieces), then the group products and the slot sums
-      double v[NP];
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        v[p] = 1.0;
-        if (p < np) {
-          const int g = (pmeta[p] >> 4) & 15;
-          const double t = (double)rem[p] * invM;
-          const double2* cf = reinterpret_cast<const double2*>(pcg[g][iv[p]]);
-          const double2 c01 = cf[0], c23 = cf[1], c45 = cf[2], c67 = cf[3];
-          double w = fma(c67.x, t, c45.y);
-          w = fma(w, t, c45.x);
-          w = fma(w, t, c23.y);
-          w = fma(w, t, c23.x);
-          w = fma(w, t, c01.y);
-          v[p] = fma(w, t, c01.x);
-        }
-      }
       double tot[BS_SLOTS];
 #pragma unroll
       for (int s = 0; s < BS_SLOTS; ++s) tot[s] = s < nc ? C0[s] : 0.0;
@@ -729,7 +710,11 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
         if (p < np) {
           const int meta = pmeta[p];
           const int m = meta & 15, g = (meta >> 4) & 15;
-          term = term * v[p];
+          const double t = (double)rem[p] * invM;
+          const double* cf = &pcg[g][iv[p] * m];
+          double v = cf[m - 1];
+          for (int kk = m - 2; kk >= 0; --kk) v = fma(v, t, cf[kk]);
+          term = term * v;
           if (meta & 256) {
 #pragma unroll
             for (int s = 0; s < BS_SLOTS; ++s)
@@ -874,7 +859,7 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
       BsGrid bg;
       int64_t tot = 0;
       for (int l = 0; l < lt.nlat; ++l) tot += lt.m[l];
-      const int per_sm = npos <= 10 ? 3 : 2;  // resident CTAs per SM (launch bounds)
+      const int per_sm = npos <= 8 ? 3 : 2;
       const int ncta = num_sms * per_sm > lt.nlat ? num_sms * per_sm : lt.nlat;
       int64_t acc = 0;
       for (int l = 0; l < lt.nlat; ++l) {
@@ -883,12 +868,9 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
       }
       bg.start[lt.nlat] = ncta;
       bg.ncta = ncta;
-      if (npos <= 4)
-        sample_bspline_chain_kernel<4><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
+      if (npos <= 8)
+        sample_bspline_chain_kernel<8><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
                                                             apply_chirp ? 1 : 0);
-      else if (npos <= 10)
-        sample_bspline_chain_kernel<10><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
-                                                             apply_chirp ? 1 : 0);
       else
         sample_bspline_chain_kernel<16><<<ncta, 256, 0, st>>>(ut, lt, bs, at, bg, chirp, buf, ustride,
                                                              apply_chirp ? 1 : 0);
