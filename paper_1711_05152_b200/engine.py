@@ -306,14 +306,14 @@ def _detect_all_launch(dev: Device, oracle, cfg: DetectionConfig, streams):
     zero = cfg.mode == "deterministic_zero_anchor"
     r, K, lo = cfg.r, int(box.sizes[0]), int(box.lows[0])
     anchors = []
+    vals = dev.empty((d * r, K, 2), torch.float64)
+    poly = isinstance(base, SparsePolynomialOracle)
     for t in range(d):
         rng = np.random.default_rng(streams[t])
         anchors.append(np.stack([np.zeros(d) if zero else rng.random(d) for _ in range(r)]))
-    vals = dev.empty((d * r, K, 2), torch.float64)
-    if isinstance(base, SparsePolynomialOracle):
-        for t in range(d):
+        if poly:  # launched as soon as the component's anchors exist (the GPU starts early)
             _line_values(dev, oracle, t, box, anchors[t], t, 0, out=vals[t * r:(t + 1) * r])
-    else:
+    if not poly:
         pts = np.repeat(np.concatenate(anchors), K, axis=0)
         line = np.tile(np.arange(K) / K, r)
         for t in range(d):

@@ -190,6 +190,19 @@ def speculate_scheme(n: int, t1: int, seed_seq: np.random.SeedSequence, b: int,
 
 
 def first_chunk(n: int, ms, target: float = 0.05) -> int:
+    key = (int(n), tuple(int(m) for m in ms), float(target))
+    got = _FIRST_CHUNK.get(key)
+    if got is None:
+        if len(_FIRST_CHUNK) > 1024:
+            _FIRST_CHUNK.clear()
+        got = _FIRST_CHUNK[key] = _first_chunk(*key)
+    return got
+
+
+_FIRST_CHUNK: dict = {}
+
+
+def _first_chunk(n: int, ms, target: float = 0.05) -> int:
     """Primes of an attempt whose alias masks are evaluated before the first
     coverage check: the fewest for which the expected number of candidates
     not yet alias-free on any of them, n * prod_l (1 - (1 - 1/M_l)^(n-1))
@@ -433,6 +446,7 @@ class StepResult:
     nodes: int                # oracle samples taken
     timings: dict = field(default_factory=dict)
     _finish: object = None    # pending cap check (run_step(defer_cap=True))
+    _lazy: object = None      # counts read back only when asked for (the cap could not bind)
 
     def finalize(self) -> "StepResult":
         """Apply the cap (detect.py:205-211) if it is still pending: waits for
@@ -445,7 +459,10 @@ class StepResult:
 
     @property
     def counts(self) -> np.ndarray:
-        return self.finalize()._counts
+        self.finalize()
+        if self._counts is None and self._lazy is not None:
+            self._counts = self._lazy()
+        return self._counts
 
 
 def _unit_arg(units):
@@ -759,6 +776,8 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     def apply_cap(counts_h):
         return apply_cap_rows(dev, coef, keep, n, counts_h, cap, step)
 
+    if cap >= n:  # the cap cannot bind: no selection, nothing to wait for
+        return StepResult(keep, coef, None, nodes, _lazy=lambda: dev.download_small(counts).astype(np.int64))
     if device_cap:
         for c0 in range(0, r, 64):
             rows = np.arange(c0, min(r, c0 + 64), dtype=np.int32)
