@@ -147,6 +147,14 @@ def build_multiple_lattice_with_retries(I: FrequencyIndexSet, cfg: MLConfig, b: 
 # one MR1L reconstruction step with a known candidate set (BASELINE config 1)
 
 @dataclass
+class _Shape:
+    """The (n, t+1) of a candidate set before it is on the device (prepare_step
+    needs only the shape)."""
+    n: int
+    ncomp: int
+
+
+@dataclass
 class StepReport:
     coeffs: np.ndarray        # (n,) complex; 0 where uncovered
     covered: np.ndarray       # (n,) bool
@@ -194,14 +202,35 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
-    spec = []
-    # the first attempt's primes and draw while the rows are in flight (valid
-    # unless the set's spread exceeds lambda; lazy streams only)
-    guess_fn = (lambda: spec.append(speculate_scheme(n, t1, seed_seq, b))) if fresh else None
-    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=guess_fn)
+    spec, early = [], {}
+
+    def ahead():
+        """While the rows are in flight: the first attempt's primes and draw
+        (valid unless the set's spread exceeds lambda; lazy streams only),
+        the alias buffers, and the step preparation for that attempt (its
+        kernels need no candidate data, so they are queued before the
+        read-back of the rows' extent)."""
+        from . import _native
+        g = speculate_scheme(n, t1, seed_seq, b)
+        spec.append(g)
+        ms = np.asarray(g.primes, dtype=np.int64)
+        words = int(_native.query("sfft_alias_scratch_words", hptr(ms), len(ms)))
+        early["bufs"] = (dev.empty((max(words, 1),), torch.int32), dev.empty((n,), torch.int64),
+                         dev.empty((2,), torch.int32))
+        from .mr1l import first_chunk
+        lhi = first_chunk(n, ms)
+        shape = _Shape(n, t1)
+        early["prep"] = prepare_step(dev, oracle, shape, 1, ms[:lhi],
+                                     np.ascontiguousarray(g.z[:lhi].astype(np.int32)), tails=[tail], d=d)
+
+    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None)
+    guess = spec[0] if spec else None
     sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                       prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d),
-                       guess=spec[0] if spec else None)
+                       prepare=None if guess is not None else
+                       (lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)),
+                       guess=guess, bufs=early.get("bufs"))
+    if guess is not None and sch.prep is None and sch.attempts == 1 and sch.z is guess.z:
+        sch.prep = early.get("prep")  # made for exactly this attempt's lattices
     # the masks are final once the scheme is built: their copy to the host runs
     # on a side stream while the sampling kernel runs
     words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)

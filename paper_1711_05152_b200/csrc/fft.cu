@@ -313,8 +313,11 @@ fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, Fft
   constexpr int rstride = Tile<2048>::rstride(N);
   const int grow = blockIdx.x;
   if (grow >= total_rows) return;
-  const int P1 = g.P1;
-  const int u = grow / P1, k1 = grow - u * P1;
+  // k1 outer, unit inner: the rows of all units at one k1 run in neighbouring
+  // CTAs, so the units that share a lattice (the r~ iterations of a step)
+  // read its Bhat row from L2 -- one HBM read per lattice instead of per unit
+  const int nu = ut.nunits;
+  const int k1 = grow / nu, u = grow - k1 * nu;
   double2* row = buf + (int64_t)u * ustride + (int64_t)k1 * N;
   const double2* twN = ftab + g.off_p2;
   double2 v[8];

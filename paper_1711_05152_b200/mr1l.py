@@ -226,7 +226,8 @@ def _first_chunk(n: int, ms, target: float = 0.05) -> int:
 def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.SeedSequence,
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
                  ctx: str = "", lazy_streams: bool = False, prepare=None,
-                 guess: SchemeGuess | None = None, first_rng: np.random.Generator | None = None) -> DeviceScheme:
+                 guess: SchemeGuess | None = None, first_rng: np.random.Generator | None = None,
+                 bufs: tuple | None = None) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -238,7 +239,8 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     kernel is enqueued (host work that overlaps it); its result is returned
     as ``DeviceScheme.prep``.  ``guess``: the first attempt
     precomputed by ``speculate_scheme`` (used when its primes all exceed the
-    spread; requires ``lazy_streams``).
+    spread; requires ``lazy_streams``).  ``bufs``: (scratch, masks, stats)
+    allocated by the caller (used when large enough).
     """
     if b < 1:
         raise ValueError("retry cap b must be >= 1")
@@ -269,9 +271,12 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
             _PRIMES_MEMO.clear()
         _PRIMES_MEMO[(n, l_max, lam)] = (list(primes),)
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms), l_max))
-    scratch = dev.empty((max(words, 1),), torch.int32)
-    masks = dev.empty((n,), torch.int64)
-    stats = dev.empty((2,), torch.int32)
+    if bufs is not None and bufs[0].numel() >= words and bufs[1].numel() == n:
+        scratch, masks, stats = bufs  # allocated by the caller ahead of time
+    else:
+        scratch = dev.empty((max(words, 1),), torch.int32)
+        masks = dev.empty((n,), torch.int64)
+        stats = dev.empty((2,), torch.int32)
     z = None
     stats_h = None
     attempt = 0
