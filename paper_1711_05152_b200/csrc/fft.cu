@@ -305,7 +305,7 @@ __device__ __forceinline__ void row2048_last_pass(double2 (&v)[8], const double2
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(FFT_T, 4)
+__global__ void __launch_bounds__(FFT_T, MODE == 0 ? 3 : 4)  // MODE 0: + 32 KB Bhat staging -> 3 CTAs/SM
 fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom g, int total_rows,
                    const double2* __restrict__ ftab, const double2* __restrict__ bhat) {
   extern __shared__ double2 s[];
@@ -320,6 +320,17 @@ fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, Fft
   const int k1 = grow / nu, u = grow - k1 * nu;
   double2* row = buf + (int64_t)u * ustride + (int64_t)k1 * N;
   const double2* twN = ftab + g.off_p2;
+  double2* bsm = s + rstride;  // MODE 0: the Bhat row, prefetched into shared memory (cp.async)
+  if (MODE == 0) {
+    const double2* bh = bhat + (int64_t)ut.lat[u] * ustride + (int64_t)k1 * N;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&bsm[threadIdx.x + q * FFT_T]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&bh[threadIdx.x + q * FFT_T])
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   double2 v[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) v[q] = __ldcs(&row[threadIdx.x + q * FFT_T]);
@@ -333,12 +344,9 @@ fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, Fft
     for (int q = 0; q < 8; ++q) row[threadIdx.x + q * FFT_T] = make_double2(v[q].x * scale, v[q].y * scale);
     return;
   }
-  const double2* bh = bhat + (int64_t)ut.lat[u] * ustride + (int64_t)k1 * N;
-  double2 b[8];
+  asm volatile("cp.async.wait_all;" ::: "memory");  // each thread reads back its own copies only
 #pragma unroll
-  for (int q = 0; q < 8; ++q) b[q] = __ldg(&bh[threadIdx.x + q * FFT_T]);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = cmul(v[q], b[q]);
+  for (int q = 0; q < 8; ++q) v[q] = cmul(v[q], bsm[threadIdx.x + q * FFT_T]);
   __syncthreads();  // every thread's last-pass reads are done before the smem is rewritten
   row2048_first_pass<true>(v, s);
   stockham_pass<8, true, 2048>(s, 1, rstride, N, 8, twN);
@@ -357,7 +365,7 @@ fft_row2048_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, Fft
 template <int MODE>
 static int launch_row2048(unsigned blocks, cudaStream_t st, double2* buf, int64_t us, const UnitTable& ut,
                           const FftGeom& g, int total_rows, const double2* ftab, const double2* bhat) {
-  const size_t sm = (size_t)Tile<2048>::rstride(2048) * sizeof(double2);
+  const size_t sm = ((size_t)Tile<2048>::rstride(2048) + (MODE == 0 ? 2048 : 0)) * sizeof(double2);
   cudaError_t e = set_smem_once((const void*)fft_row2048_kernel<MODE>, sm);
   if (e != cudaSuccess) return (int)e;
   fft_row2048_kernel<MODE><<<blocks, FFT_T, sm, st>>>(buf, us, ut, g, total_rows, ftab, bhat);
