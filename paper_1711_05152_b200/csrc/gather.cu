@@ -46,39 +46,20 @@ gather_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt,
       int32_t kv[DM];
       load_cand<DM>(kv, freqs, n, k, d);
       uint64_t mm = mask;
-      // lattices in batches of GB: the batch's residues and bin loads are
-      // issued together (independent), then accumulated in lattice order
-      constexpr int GB = RB >= 8 ? 1 : (RB >= 4 ? 2 : 8);
       while (mm) {
-        int lb[GB];
-        double2 vb[GB][RB];
+        const int l = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
+        const double invm = lt.inv_m[l];  // == 1.0 / M (host-computed, correctly rounded)
+        ++cnt;
 #pragma unroll
-        for (int q = 0; q < GB; ++q) {
-          lb[q] = -1;
-          if (mm) {
-            const int l = __ffsll((long long)mm) - 1;
-            mm &= mm - 1;
-            lb[q] = l;
-            const int64_t r = SFFT_RES(DM, FAST, kv, lt, l);
-#pragma unroll
-            for (int i = 0; i < RB; ++i)
-              if (i < rb) vb[q][i] = __ldg(&buf[(int64_t)(i * L + l) * ustride + r]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < GB; ++q) {
-          if (lb[q] >= 0) {
-            const double invm = lt.inv_m[lb[q]];  // == 1.0 / M (host-computed, correctly rounded)
-            ++cnt;
-#pragma unroll
-            for (int i = 0; i < RB; ++i) {
-              if (i < rb) {
-                // spectrum_hat = X / M rounded, then accumulated (no FMA contraction),
-                // exactly the numpy sequence of transform.py:121-123
-                sums[i].x = __dadd_rn(sums[i].x, __dmul_rn(vb[q][i].x, invm));
-                sums[i].y = __dadd_rn(sums[i].y, __dmul_rn(vb[q][i].y, invm));
-              }
-            }
+        for (int i = 0; i < RB; ++i) {
+          if (i < rb) {
+            // spectrum_hat = X / M rounded, then accumulated (no FMA contraction),
+            // exactly the numpy sequence of transform.py:121-123
+            const double2 v = __ldg(&buf[(int64_t)(i * L + l) * ustride + r]);
+            sums[i].x = __dadd_rn(sums[i].x, __dmul_rn(v.x, invm));
+            sums[i].y = __dadd_rn(sums[i].y, __dmul_rn(v.y, invm));
           }
         }
       }
