@@ -1,6 +1,7 @@
 // extern "C" boundary (include/sfft_b200.h): validates arguments, builds the
 // by-value launch structs and dispatches to the kernels.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -344,6 +345,19 @@ int build_poly_plan(PolyPlan* pp, const int64_t* h_m, int L, const UnitTable& ut
     double eff = (double)units / (double)(waves * slots);
     if (kse > 1) eff *= 0.97;  // partial-sum write/read + reduce kernel
     if (eff > best_eff + 1e-9) { best_eff = eff; best_ks = kse; best_kper = kper; }
+  }
+  static const int force_ks = [] {  // measurement override (tools): SFFT_B200_KSPLIT=<1..8>
+    const char* e = getenv("SFFT_B200_KSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  if (force_ks >= 1 && force_ks <= 8) {
+    int kper = (((s + force_ks - 1) / force_ks + 15) / 16) * 16;
+    if (kper < 16) kper = 16;
+    const int kse = (s + kper - 1) / kper > 0 ? (s + kper - 1) / kper : 1;
+    if (kse == 1 || partial_cap < 0 || (int64_t)kse * pp->nunits * mmax <= partial_cap) {
+      best_kper = kper;
+      best_ks = kse;
+    }
   }
   pp->ks = best_ks;
   pp->kper = best_kper;
