@@ -71,6 +71,15 @@ def _free_port():
     return port
 
 
+def _noisy_runs(P):
+    """Noisy oracles through a sharded step: every rank consumes the whole
+    numpy noise stream / the whole call-index range (parallel._align_noise)."""
+    truth, poly = P.gen_random_sparse_poly(4, 8, 20, "unit_modulus", seed=np.random.default_rng(9))
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(4, 8), delta=0.3, s=20, r=3, b=10, rng_seed=5)
+    return [(P.NoisyOracle(poly, P.sigma_for_snr(20, 30.0), seed=123), cfg),
+            (P.RelativeNoisyOracle(poly, 1e-2, seed=7, device_rng=True), cfg)]
+
+
 def _mp_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
@@ -92,8 +101,9 @@ def _mp_worker(rank, world, port, q):
         coef, keep = dev.download(res.coef), dev.download(res.keep)
         w0 = workloads.config0()
         rep = P.sparse_fft(w0.oracle, w0.cfg)  # sharded over the process group
+        noisy = [P.sparse_fft(o, c).detected for o, c in _noisy_runs(P)]
         q.put((rank, coef, keep, rep.detected.freqs, rep.detected.coeffs, rep.oracle_calls,
-               rep.candidate_counts, rep.scheme_sizes))
+               rep.candidate_counts, rep.scheme_sizes, [(x.freqs, x.coeffs) for x in noisy]))
     except Exception as exc:  # surface the worker's error in the test
         q.put((rank, repr(exc)))
         raise
@@ -126,10 +136,13 @@ def test_two_process_group_on_one_gpu_bit_identical():
     ref = run_step(dev, wl.oracle, cand, sch, [np.zeros(0)], 10, 1e-12, cand.n)
     w0 = workloads.config0()
     rep = P.sparse_fft(w0.oracle, w0.cfg)
-    for rank, coef, keep, f, c, calls, cc, ss in got:
+    noisy = [P.sparse_fft(o, c).detected for o, c in _noisy_runs(P)]
+    for rank, coef, keep, f, c, calls, cc, ss, nz in got:
         assert np.array_equal(coef, dev.download(ref.coef)), rank
         assert np.array_equal(keep, dev.download(ref.keep)), rank
         assert np.array_equal(f, rep.detected.freqs) and np.array_equal(c, rep.detected.coeffs), rank
         assert calls == rep.oracle_calls and cc == rep.candidate_counts and ss == rep.scheme_sizes
+        for (nf, nc), one in zip(nz, noisy):
+            assert np.array_equal(nf, one.freqs) and np.array_equal(nc, one.coeffs), rank
     for p in procs:
         assert p.exitcode == 0
