@@ -217,6 +217,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         words = int(_native.query("sfft_alias_scratch_words", hptr(ms), len(ms)))
         early["bufs"] = (dev.empty((max(words, 1),), torch.int32), dev.empty((n,), torch.int64),
                          dev.empty((2,), torch.int32))
+        early["words_h"] = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
         from .mr1l import first_chunk
         lhi = first_chunk(n, ms)
         shape = _Shape(n, t1)
@@ -232,21 +233,24 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     if guess is not None and sch.prep is None and sch.attempts == 1 and sch.z is guess.z:
         sch.prep = early.get("prep")  # made for exactly this attempt's lattices
     # the masks are final once the scheme is built: their copy to the host runs
-    # on a side stream while the sampling kernel runs
-    words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
+    # on a side stream while the sampling kernel runs (enqueued after the
+    # sampling launch, so the launch is not delayed by it)
     ready = torch.cuda.Event()
     ready.record(dev.stream)
-    side = dev.copy_stream()
-    side.wait_event(ready)
-    with torch.cuda.stream(side):
-        words_h.copy_(sch.masks.view(torch.uint8), non_blocking=True)
-    sch.masks.record_stream(side)
     if sharded:
         res = run_step_sharded(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap), sh,
                                prep=sch.prep, need_coef=True)
     else:
         res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
                        defer_cap=True, prep=sch.prep)
+    words_h = early.get("words_h")
+    if words_h is None:
+        words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
+    side = dev.copy_stream()
+    side.wait_event(ready)
+    with torch.cuda.stream(side):
+        words_h.copy_(sch.masks.view(torch.uint8), non_blocking=True)
+    sch.masks.record_stream(side)
     res.finalize()  # cap applied (if binding) before the results are read
     coef, keep = dev.download_many(res.coef[0], res.keep[0])
     side.synchronize()
