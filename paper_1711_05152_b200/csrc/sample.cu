@@ -700,7 +700,13 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
         rem[p] = (uint32_t)qr;
       }
     }
+    const double2* chn = chirp + lt.off[l];
+    double2 cv = make_double2(1.0, 0.0);
+    if (apply_chirp) cv = __ldg(&chn[n0]);
     for (int64_t n = n0; n < ne; n += 256) {
+      // the next node's chirp is requested now (its latency hides behind this node's work)
+      double2 cnext = make_double2(1.0, 0.0);
+      if (apply_chirp && n + 256 < ne) cnext = __ldg(&chn[n + 256]);
       double tot[BS_SLOTS];
 #pragma unroll
       for (int s = 0; s < BS_SLOTS; ++s) tot[s] = s < nc ? C0[s] : 0.0;
@@ -728,14 +734,13 @@ sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTab
           iv[p] = i2 >= (uint32_t)m ? i2 - (uint32_t)m : i2;
         }
       }
-      double2 cv = make_double2(1.0, 0.0);
-      if (apply_chirp) cv = __ldg(&chirp[lt.off[l] + n]);
 #pragma unroll
       for (int s = 0; s < BS_SLOTS; ++s)
         if (s < nc) {
           double2* ub = buf + (int64_t)slot[c0 + s] * ustride;
           __stcs(&ub[n], apply_chirp ? make_double2(tot[s] * cv.x, tot[s] * cv.y) : make_double2(tot[s], 0.0));
         }
+      cv = cnext;
     }
   }
 }
@@ -859,7 +864,14 @@ int launch_sample_bspline(const UnitTable& ut, const LatTable& lt, const Bspline
       BsGrid bg;
       int64_t tot = 0;
       for (int l = 0; l < lt.nlat; ++l) tot += lt.m[l];
-      const int per_sm = npos <= 8 ? 3 : 2;
+      // one wave: resident CTAs per SM from the occupancy calculator
+      const void* fk = npos <= 8 ? (const void*)sample_bspline_chain_kernel<8>
+                                 : (const void*)sample_bspline_chain_kernel<16>;
+      int per_sm = 2;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, 256, 0) != cudaSuccess || per_sm < 1) {
+        (void)cudaGetLastError();
+        per_sm = 2;
+      }
       const int ncta = num_sms * per_sm > lt.nlat ? num_sms * per_sm : lt.nlat;
       int64_t acc = 0;
       for (int l = 0; l < lt.nlat; ++l) {
