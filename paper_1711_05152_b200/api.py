@@ -224,12 +224,30 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         early["prep"] = prepare_step(dev, oracle, shape, 1, ms[:lhi],
                                      np.ascontiguousarray(g.z[:lhi].astype(np.int32)), tails=[tail], d=d)
 
-    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None)
+    def defer_extent():
+        """Skip the read-back of the rows' extent before the alias kernel when
+        the guessed lattices make the exact double-quotient residue path valid
+        for ANY int32 component (t+1 * (2^31 - 1) * max M < 2^52); the extent
+        then comes back with the alias stats and is checked there."""
+        return bool(spec) and t1 * float(2**31 - 1) * float(max(spec[0].primes)) < 4.0e15
+
+    cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None,
+                                                defer=defer_extent)
     guess = spec[0] if spec else None
-    sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                       prepare=None if guess is not None else
-                       (lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)),
-                       guess=guess, bufs=early.get("bufs"))
+    if hi is None:  # deferred: alias with the guess, extent read back with the stats
+        sch = build_scheme(dev, cand, b, seed_seq, box_extent=0, lazy_streams=fresh, guess=guess,
+                           bufs=early.get("bufs"), also=lo)
+        lo, hi, kmax = DeviceFreqs.extent_of(sch.extra.view(np.int32), t1, n)
+        cand.kmax = kmax
+        if not (sch.attempts == 1 and sch.z is guess.z and guess.primes[0] > int((hi - lo).max())):
+            # the guess did not hold (spread >= lambda): the reference's construction
+            sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
+                               prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d))
+    else:
+        sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
+                           prepare=None if guess is not None else
+                           (lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)),
+                           guess=guess, bufs=early.get("bufs"))
     if guess is not None and sch.prep is None and sch.attempts == 1 and sch.z is guess.z:
         sch.prep = early.get("prep")  # made for exactly this attempt's lattices
     # the masks are final once the scheme is built: their copy to the host runs

@@ -83,11 +83,14 @@ class DeviceFreqs:
         return cls(t, rows.shape[0], kmax)
 
     @classmethod
-    def from_rows_tensor(cls, dev: Device, rows, before_sync=None) -> tuple["DeviceFreqs", np.ndarray, np.ndarray]:
+    def from_rows_tensor(cls, dev: Device, rows, before_sync=None,
+                         defer: bool = False) -> tuple["DeviceFreqs", object, object]:
         """Upload (n, d) int64 rows (a CPU tensor; pinned memory makes the copy
         asynchronous DMA) and pack them on the device; also returns the
         per-component minima and maxima.  ``before_sync()`` runs while the
-        copy is in flight."""
+        copy is in flight.  ``defer``: no read-back; returns (set with kmax =
+        the int32 bound, the device extent tensor, None) and the caller reads
+        the extent later with ``extent_of`` (one synchronisation fewer)."""
         torch = dev.torch
         n, d = (int(x) for x in rows.shape)
         with torch.cuda.stream(dev.stream):
@@ -97,12 +100,20 @@ class DeviceFreqs:
         dev.call("sfft_pack_rows", dptr(d_rows), n, d, dptr(out), dptr(mm), ctx="pack rows")
         if before_sync is not None:
             before_sync()
-        mmh = dev.download_small(mm).astype(np.int64)
+        if defer() if callable(defer) else defer:
+            return cls(out, n, 2**31 - 1), mm, None
+        lo, hi, kmax = cls.extent_of(dev.download_small(mm), d, n)
+        return cls(out, n, kmax), lo, hi
+
+    @staticmethod
+    def extent_of(mmh, d: int, n: int):
+        """(minima, maxima, kmax) from sfft_pack_rows' extent words."""
+        mmh = np.asarray(mmh).astype(np.int64)
         if mmh[2 * d]:
             raise ValueError("frequency components must satisfy |k_t| <= 2147483647")
         lo, hi = mmh[:d], mmh[d:2 * d]
         kmax = int(max(np.abs(lo).max(), np.abs(hi).max())) if n else 0
-        return cls(out, n, kmax), lo, hi
+        return lo, hi, kmax
 
     def to_host(self, dev: Device) -> np.ndarray:
         return dev.download(self.data).T.astype(np.int64)
@@ -117,6 +128,7 @@ class DeviceScheme:
     attempts: int
     uncovered: int
     prep: object = None         # build_scheme(prepare=...) result
+    extra: object = None        # build_scheme(also=...) read back with the first attempt's stats
 
     @property
     def m_used(self) -> np.ndarray:
@@ -227,7 +239,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
                  ctx: str = "", lazy_streams: bool = False, prepare=None,
                  guess: SchemeGuess | None = None, first_rng: np.random.Generator | None = None,
-                 bufs: tuple | None = None) -> DeviceScheme:
+                 bufs: tuple | None = None, also=None) -> DeviceScheme:
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -298,6 +310,10 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
             wait = dev.download_async(stats)
             prep = prepare(ms[:l_hi], zh[:l_hi])
             stats_h = wait()
+        elif also is not None and attempt == 1:
+            stats_h, extra = dev.download_many(stats, also)
+            stats_h = stats_h.view(np.int32)
+            also = extra  # handed back in DeviceScheme.extra
         else:
             stats_h = dev.download_small(stats)
         if int(stats_h[1]) != 0 and l_hi < l_max:
@@ -306,8 +322,10 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
                      dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
             stats_h = dev.download_small(stats)
         if int(stats_h[1]) == 0:
-            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep)
-    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep)
+            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep,
+                                extra=also if isinstance(also, np.ndarray) else None)
+    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep,
+                        extra=also if isinstance(also, np.ndarray) else None)
 
 
 def scheme_to_host(dev: Device, cand_rows: np.ndarray, sch: DeviceScheme) -> MultipleRank1Lattice:
