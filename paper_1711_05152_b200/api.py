@@ -229,7 +229,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         the guessed lattices make the exact double-quotient residue path valid
         for ANY int32 component (t+1 * (2^31 - 1) * max M < 2^52); the extent
         then comes back with the alias stats and is checked there."""
-        return bool(spec) and t1 * float(2**31 - 1) * float(max(spec[0].primes)) < 4.0e15
+        return bool(spec) and t1 * float(2**31 - 1) * float(max(spec[0].primes)) < 4503599627370496.0
 
     cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None,
                                                 defer=defer_extent)

@@ -158,7 +158,7 @@ bool residue_fast(int t1, int64_t kmax, const int64_t* h_m, int L) {
   int64_t mmax = 1;
   for (int l = 0; l < L; ++l) mmax = h_m[l] > mmax ? h_m[l] : mmax;
   const double bound = (double)t1 * (double)(kmax < 0 ? -kmax : kmax) * (double)mmax;
-  return bound < 4.0e15;  // < 2^52 with margin
+  return bound < 4503599627370496.0;  // every |k . z| < 2^52: exact in a double, mod_fast's domain
 }
 
 // Enable the int32 residue path when every |k . z| < d * kmax * M < 2^31.

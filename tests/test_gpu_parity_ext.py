@@ -372,3 +372,46 @@ def test_cap_selection_many_ties(P, n, nvals):
         assert (mag_dev[y, idx] == thr).sum() > 2048  # the overflow path ran
         assert np.array_equal(got[y], want), y
     assert dev.download(counts).tolist() == [cap, cap]
+
+
+# ---------------------------------------------------------------------------
+# api.reconstruct_step (the e2e entry): speculative first attempt, deferred
+# extent read-back, and its fallbacks
+
+@pytest.mark.parametrize("kind", ["config1", "wide", "int64_rows"])
+def test_reconstruct_step_matches_oracle(P, kind):
+    """The composed step (construction + sampling + inversion + threshold)
+    against the oracle's mr1l_step: same lattices, masks, coefficients.
+    'wide': components spanning more than lambda = 2(|J| - 1), so the
+    speculated primes are invalid and the reference's construction runs."""
+    from oracle import sfft_oracle as O
+    from paper_1711_05152_b200 import workloads
+    if kind == "config1":
+        wl = workloads.config1(seed=4, n=5000, nnz=90)
+        cand, oracle, seed = wl.cand, wl.oracle, wl.lattice_seed
+    else:
+        rng = np.random.default_rng(12)
+        cand = np.unique(rng.integers(-3000, 3001, size=(300, 3)), axis=0)
+        hf = cand[rng.choice(len(cand), 20, replace=False)]
+        hc = rng.uniform(-1, 1, 20) + 1j * rng.uniform(-1, 1, 20)
+        oracle = P.SparsePolynomialOracle(hf, hc)
+        seed = 77
+    arg = cand
+    if kind == "int64_rows":  # a pinned torch tensor, as the bench passes it
+        import torch
+        arg = torch.from_numpy(np.ascontiguousarray(cand, dtype=np.int64)).pin_memory()
+    rep = P.api.reconstruct_step(arg, oracle, b=10, seed_seq=seed, delta=1e-12)
+    sch = O.build_with_retries(np.asarray(cand, np.int64), 10, np.random.SeedSequence(seed))
+    assert rep.lattice_sizes == sch.ms and rep.attempts == sch.attempts
+    assert np.array_equal(np.asarray(rep.generating_vectors), np.stack(sch.zs))
+    vals = [O.poly_eval(oracle.freqs, oracle.coeffs, O.lattice_nodes(z, m)) for m, z in zip(sch.ms, sch.zs)]
+    cov, coefs = O.invert_multiple(np.asarray(cand, np.int64), sch, vals)
+    assert np.array_equal(rep.covered, cov)
+    assert _rel(rep.coeffs[cov], coefs) <= COEF_RTOL
+
+
+def test_reconstruct_step_rejects_out_of_range_components(P):
+    rows = np.array([[0, 1], [2**31, 0]], dtype=np.int64)
+    with pytest.raises(ValueError, match="2147483647"):
+        P.api.reconstruct_step(rows, P.SparsePolynomialOracle(np.array([[0, 1]]), np.array([1.0 + 0j])), b=5,
+                               seed_seq=1, delta=1e-12)
