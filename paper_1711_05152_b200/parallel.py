@@ -176,15 +176,11 @@ def _all_gather_flat(dev, out, local, group):
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
         return
-    dev.sync()
-    parts = [t for t in out.new_empty(out.shape, device="cpu").chunk(dist.get_world_size(group))]
-    dist.all_gather(parts, local.contiguous().cpu(), group=group)
-    out.copy_(torch_cat(parts))
-
-
-def torch_cat(parts):
     import torch
-    return torch.cat(parts)
+    dev.sync()
+    parts = list(out.new_empty(out.shape, device="cpu").chunk(dist.get_world_size(group)))
+    dist.all_gather(parts, local.contiguous().cpu(), group=group)
+    out.copy_(torch.cat(parts))
 
 
 def _all_reduce_sum(dev, t, group):
@@ -196,14 +192,6 @@ def _all_reduce_sum(dev, t, group):
     h = t.cpu()
     dist.all_reduce(h, group=group)
     t.copy_(h)
-
-
-class _SimGroup:
-    """In-process stand-in for ``world`` ranks (tests without a process
-    group): the collectives concatenate / sum the per-rank buffers."""
-
-    def __init__(self, world):
-        self.world = world
 
 
 def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: list,
