@@ -1,7 +1,10 @@
 """K3 alias kernels A/B: mean device time of sfft_alias_masks_range over the
 first chunk of lattices (library CUDA events), at config-1 size (|J| = 1e5,
 d = 10) and config-3 size (|J| = 6.5e5, d = 20).  The path is chosen by
-SFFT_B200_ALIAS_CLUSTER (unset: L2 atomics; 1: cluster/DSMEM where it fits)."""
+SFFT_B200_ALIAS_CLUSTER (1: cluster/DSMEM where it fits) and
+SFFT_B200_ALIAS_FUSED (0: the two-kernel L2-atomic path; default: the fused
+cooperative kernel where it fits).  ``call_ms``: CUDA events around the whole
+call (memsets included)."""
 import ctypes
 import json
 import os
@@ -21,7 +24,8 @@ def main():
     from paper_1711_05152_b200.workloads import distinct_rows
     dev = get_device()
     torch = dev.torch
-    out = {"path": "cluster" if os.environ.get("SFFT_B200_ALIAS_CLUSTER") == "1" else "l2"}
+    out = {"path": "cluster" if os.environ.get("SFFT_B200_ALIAS_CLUSTER") == "1" else
+           ("l2" if os.environ.get("SFFT_B200_ALIAS_FUSED") == "0" else "fused")}
     for name, n, d in (("config1", 100_000, 10), ("config3", 650_000, 20)):
         rows = distinct_rows(np.random.default_rng(1), n, d, 32)
         cand = DeviceFreqs.from_host(dev, rows)
@@ -45,13 +49,20 @@ def main():
         tot, cnt = ctypes.c_double(0.0), ctypes.c_int(0)
         _native.call("sfft_profile_collect", 2, ctypes.addressof(tot), ctypes.addressof(cnt))
         _native.query("sfft_profile_enable", 1)
+        evs = []
         for _ in range(20):
             flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(dev.stream)
             run()
+            b.record(dev.stream)
+            evs.append((a, b))
         dev.sync()
         _native.call("sfft_profile_collect", 2, ctypes.addressof(tot), ctypes.addressof(cnt))
         _native.query("sfft_profile_enable", 0)
         out[name] = {"n": n, "d": d, "lattices": lhi, "ms": tot.value / max(cnt.value, 1),
+                     "call_ms": float(np.mean([a.elapsed_time(b) for a, b in evs])),
                      "masks_sum": int(dev.download(masks).view(np.uint64).sum() % (1 << 61))}
     print(json.dumps(out))
 
