@@ -24,7 +24,8 @@ import numpy as np
 
 from .core import FrequencyIndexSet, SearchBox, SparseSpectrum
 from .device import Device, dptr, get_device, hptr
-from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact, prepare_step,
+from .mr1l import (DeviceFreqs, OracleError, OracleInterrupt, build_scheme, compact, compact_count, compact_finish,
+                   compact_start, prepare_step,
                    evaluate_callback, first_attempt_rng, product, run_step)
 from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig
@@ -357,6 +358,62 @@ def detect_component(oracle, t: int, cfg: DetectionConfig, rng: np.random.Genera
 # ---------------------------------------------------------------------------
 # the engine
 
+def _overlap_enabled() -> bool:
+    """SFFT_B200_ENGINE_OVERLAP=0 runs every step after its predecessor's
+    synchronisation (the A/B of tools/run_configs.py)."""
+    import os
+    return os.environ.get("SFFT_B200_ENGINE_OVERLAP", "1") != "0"
+
+
+@dataclass
+class _NextStep:
+    """Step t+1 started during step t for a guessed prefix count ``cnt``: the
+    prefixes gathered with that count, their product with the next
+    component, the first lattice-search attempt's alias kernel (pending) and
+    the step preparation.  Valid when step t's compaction count equals
+    ``cnt``; otherwise discarded (its kernels only wrote their own buffers)."""
+    cnt: int
+    prefixes: DeviceFreqs
+    cand: DeviceFreqs
+    pending: object
+    guess: object
+    prep: object
+
+
+def _start_next_step(dev: Device, oracle, prefixes: DeviceFreqs | None, pend, cnt: int, comp, t_next: int,
+                     tails, d: int, seed_seq, b: int, spread: int) -> "_NextStep | None":
+    """Enqueue step t_next up to its first alias kernel without host
+    synchronisation.  ``prefixes``: the exact prefix set (step 1), or None
+    with ``pend`` (step t's pending compaction) and the guessed count."""
+    from . import _native
+    from .mr1l import first_chunk, product, speculate_scheme
+    torch = dev.torch
+    n = cnt * len(comp)
+    if n < 1 or cnt < 1:
+        return None
+    g = speculate_scheme(n, t_next + 1, seed_seq, b)
+    if g.primes[0] <= spread:  # build_scheme would not take the guessed attempt
+        return None
+    if prefixes is None:
+        # the compaction's gather with the guessed count, into zeroed rows (a
+        # wrong guess leaves valid, if meaningless, frequencies behind)
+        _, prev, idx, total, _, _ = pend
+        out = dev.zeros((prev.ncomp, cnt), torch.int32)
+        dev.call("sfft_gather_rows", dptr(prev.data), prev.n, prev.ncomp, dptr(idx), dptr(total), cnt, dptr(out),
+                 cnt, 0, 0, ctx="row gather (next step)")
+        prefixes = DeviceFreqs(out, cnt, prev.kmax)
+    cand = product(dev, prefixes, comp)
+    ms = np.asarray(g.primes, dtype=np.int64)
+    words = int(_native.query("sfft_alias_scratch_words", hptr(ms), len(ms)))
+    bufs = (dev.empty((max(words, 1),), torch.int32), dev.empty((n,), torch.int64), dev.empty((2,), torch.int32))
+    pending = build_scheme(dev, cand, b, seed_seq, box_extent=spread, ctx=f"lattice search, step {t_next}",
+                           lazy_streams=True, guess=g, bufs=bufs, defer=True)
+    lhi = first_chunk(n, ms)
+    prep = prepare_step(dev, oracle, cand, len(tails), ms[:lhi], np.ascontiguousarray(g.z[:lhi].astype(np.int32)),
+                        cached_tables_only=True, tails=tails, d=d)
+    return _NextStep(cnt, prefixes, cand, pending, g, prep)
+
+
 def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
                group=None, shard: bool | None = None) -> DetectionReport:
     """Reconstruct support and coefficients of a sparse periodic signal
@@ -414,6 +471,24 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
         first_rngs.append(first_attempt_rng(lattice_streams[t], cfg.b) if cfg.lattice_kind != "single" else None)
     if hoisted is not None:
         hoisted = _detect_all_collect(dev, hoisted)
+    # step t+1 is enqueued during step t, up to its first alias kernel, for
+    # a guessed prefix count (this step's, exact for step 1): the compaction,
+    # product, lattice search and preparation then follow each other on the
+    # device without host synchronisation in between.  Device oracles with
+    # hoisted line detections; nothing of it draws from a stream the steps
+    # draw from (speculate_scheme uses each attempt's own lazy child).
+    # (a replaced scheme builder — the reference tests' seam — sees every step)
+    from . import mr1l as _mr1l
+    can_start = (hoisted is not None and cfg.lattice_kind != "single" and box.member is None and not sharded
+                 and build_scheme is _mr1l.build_scheme and _overlap_enabled())
+    nxt = None
+    prev_count = None  # the prefix count of the step before the current one
+
+    def start_next(t_next: int, prefixes_exact, pend, cnt):
+        if not can_start or t_next >= d:
+            return None
+        return _start_next_step(dev, oracle, prefixes_exact, pend, cnt, hoisted[t_next], t_next, all_tails[t_next],
+                                d, lattice_streams[t_next], cfg.b, int(extents[: t_next + 1].max()))
 
     for t in range(d):
         t_step = time.perf_counter()
@@ -423,13 +498,18 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             comp = _detect(dev, oracle, t, cfg, np.random.default_rng(detect_streams[t]), t)
         rep.component_counts[t] = len(comp)
         rep.detection_calls[t] = cfg.r * int(box.sizes[t])
+        started, nxt = nxt, None
         if t == 0:
             prefixes = DeviceFreqs.from_host(dev, comp[:, None])
             rep.prefix_counts[0] = rep.candidate_counts[0] = len(comp)
             if d > 1:
+                nxt = start_next(1, prefixes, None, prefixes.n)
                 rep.step_times.append(time.perf_counter() - t_step)
                 continue
             cand = prefixes
+        elif started is not None:
+            cand = started.cand  # enqueued during the previous step (its count was right)
+            rep.candidate_counts[t] = cand.n
         else:
             cand = product(dev, prefixes, comp)
             if box.member is not None and cand.n:
@@ -454,9 +534,14 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             # (and the tables, when this step's sizes were seen before)
             prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
                                                  cached_tables_only=True, tails=tails, d=d)
-            sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
-                               ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare,
-                               first_rng=first_rngs[t])
+            if started is not None:
+                sch = started.pending.finish()
+                if sch.prep is None and sch.attempts == 1 and sch.z is started.guess.z:
+                    sch.prep = started.prep  # made for exactly this attempt's lattices
+            else:
+                sch = build_scheme(dev, cand, cfg.b, lattice_streams[t], box_extent=int(extents[: t + 1].max()),
+                                   ctx=f"lattice search, step {t}", lazy_streams=True, prepare=prepare,
+                                   first_rng=first_rngs[t])
         rep.scheme_sizes[t] = sch.total_size
         rep.lattice_attempts[t] = sch.attempts
         rep.inversion_calls[t] = r_tilde * sch.total_size
@@ -478,7 +563,18 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             final_coef = c[:, 0] + 1j * c[:, 1]
             rep.prefix_counts[t] = len(final_rows)
         else:
-            prefixes, _ = compact(dev, cand, res.keep, r_tilde)
+            pend = compact_start(dev, cand, res.keep, r_tilde)
+            # the next step for as many prefixes as this step had, once the
+            # counts have settled (the last two steps' equal, as when the caps
+            # bind); the host work hides behind this step's sampling
+            settled = prev_count is not None and prev_count == prefixes.n
+            nxt = start_next(t + 1, None, pend, prefixes.n) if settled else None
+            prev_count = prefixes.n
+            if nxt is not None and compact_count(pend) == nxt.cnt:
+                prefixes = nxt.prefixes
+            else:
+                nxt = None
+                prefixes, _ = compact_finish(pend)
             rep.prefix_counts[t] = prefixes.n
         rep.step_times.append(time.perf_counter() - t_step)
 

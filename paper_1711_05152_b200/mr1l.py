@@ -30,7 +30,8 @@ from .oracles import BSplineOracle, NoisyOracle, SparsePolynomialOracle
 from .primes import MLConfig, candidate_primes
 
 __all__ = ["DeviceFreqs", "DeviceScheme", "build_scheme", "clear_caches", "speculate_scheme", "SchemeGuess", "run_step",
-           "prepare_step", "StepPrep", "StepResult", "first_attempt_rng",
+           "prepare_step", "StepPrep", "StepResult", "first_attempt_rng", "compact_start", "compact_finish",
+           "compact_count", "PendingScheme",
            "OracleInterrupt", "OracleError", "evaluate_callback"]
 
 UMAX = 256      # (iteration, lattice) units per launch (plan.cuh SFFT_UMAX)
@@ -239,7 +240,7 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
                  *, cfg: MLConfig | None = None, box_extent: int | None = None,
                  ctx: str = "", lazy_streams: bool = False, prepare=None,
                  guess: SchemeGuess | None = None, first_rng: np.random.Generator | None = None,
-                 bufs: tuple | None = None, also=None) -> DeviceScheme:
+                 bufs: tuple | None = None, also=None, defer: bool = False):
     """Algorithm 1 with retries (reference construct.py:146-206) on the device.
 
     Every attempt pre-draws its L_max generating vectors (stream-identical to
@@ -252,7 +253,11 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
     as ``DeviceScheme.prep``.  ``guess``: the first attempt
     precomputed by ``speculate_scheme`` (used when its primes all exceed the
     spread; requires ``lazy_streams``).  ``bufs``: (scratch, masks, stats)
-    allocated by the caller (used when large enough).
+    allocated by the caller (used when large enough).  ``defer``: return a
+    ``PendingScheme`` right after the first attempt's alias kernel is
+    enqueued (when it comes from ``guess`` and neither ``prepare`` nor
+    ``also`` is given; otherwise the search runs now); ``.finish()`` gives
+    the DeviceScheme.
     """
     if b < 1:
         raise ValueError("retry cap b must be >= 1")
@@ -289,43 +294,80 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
         scratch = dev.empty((max(words, 1),), torch.int32)
         masks = dev.empty((n,), torch.int64)
         stats = dev.empty((2,), torch.int32)
-    z = None
-    stats_h = None
-    attempt = 0
-    prep = None
-    for attempt, child in enumerate(_attempt_streams(seed_seq, b, lazy_streams), start=1):
-        if attempt == 1 and guess is not None:
-            z = guess.z
-        else:
-            rng = first_rng if (attempt == 1 and first_rng is not None and lazy_streams) else np.random.default_rng(child)
-            # one vectorised draw with per-row bounds == the reference's per-prime
-            # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
-            z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
-        zh = np.ascontiguousarray(z.astype(np.int32))
-        dev.call("sfft_alias_masks_range", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), 0, l_hi,
+    streams = _attempt_streams(seed_seq, b, lazy_streams)
+
+    def alias(zh, l0, l1):
+        dev.call("sfft_alias_masks_range", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l0, l1,
                  dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
-        if prepare is not None and attempt == 1:
-            # read the stats back through an event, so the preparation kernels
-            # queued behind the alias kernel run while the host continues
+
+    def run(first=None):
+        z = None
+        stats_h = None
+        attempt = 0
+        prep = None
+        extra = also
+        for attempt, child in enumerate(streams, start=1):
+            if first is not None and attempt == 1:
+                z, zh, wait = first  # launched by the deferred call
+                stats_h = wait()
+            else:
+                if attempt == 1 and guess is not None:
+                    z = guess.z
+                else:
+                    rng = first_rng if (attempt == 1 and first_rng is not None and lazy_streams) \
+                        else np.random.default_rng(child)
+                    # one vectorised draw with per-row bounds == the reference's per-prime
+                    # rng.integers(0, m, size=d) calls, element for element (tests/test_host.py)
+                    z = rng.integers(0, ms[:, None], size=(l_max, t1), dtype=np.int64)
+                zh = np.ascontiguousarray(z.astype(np.int32))
+                alias(zh, 0, l_hi)
+                if prepare is not None and attempt == 1:
+                    # read the stats back through an event, so the preparation kernels
+                    # queued behind the alias kernel run while the host continues
+                    wait = dev.download_async(stats)
+                    prep = prepare(ms[:l_hi], zh[:l_hi])
+                    stats_h = wait()
+                elif extra is not None and attempt == 1:
+                    stats_h, extra = dev.download_many(stats, extra)  # extra handed back in DeviceScheme.extra
+                    stats_h = stats_h.view(np.int32)
+                else:
+                    stats_h = dev.download_small(stats)
+            if int(stats_h[1]) != 0 and l_hi < l_max:
+                # not covered by the first chunk: the remaining primes of the attempt
+                alias(zh, l_hi, l_max)
+                stats_h = dev.download_small(stats)
+            if int(stats_h[1]) == 0:
+                return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep,
+                                    extra=extra if isinstance(extra, np.ndarray) else None)
+        return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep,
+                            extra=extra if isinstance(extra, np.ndarray) else None)
+
+    if defer:
+        if guess is not None and prepare is None and also is None:
+            # the first attempt's alias kernel now, its stats (and everything
+            # after them) when the caller finishes
+            zh = np.ascontiguousarray(guess.z.astype(np.int32))
+            alias(zh, 0, l_hi)
             wait = dev.download_async(stats)
-            prep = prepare(ms[:l_hi], zh[:l_hi])
-            stats_h = wait()
-        elif also is not None and attempt == 1:
-            stats_h, extra = dev.download_many(stats, also)
-            stats_h = stats_h.view(np.int32)
-            also = extra  # handed back in DeviceScheme.extra
-        else:
-            stats_h = dev.download_small(stats)
-        if int(stats_h[1]) != 0 and l_hi < l_max:
-            # not covered by the first chunk: the remaining primes of the attempt
-            dev.call("sfft_alias_masks_range", dptr(cand.data), n, t1, cand.kmax, hptr(ms), hptr(zh), l_hi, l_max,
-                     dptr(scratch), words, dptr(masks), dptr(stats), ctx=ctx or "alias masks")
-            stats_h = dev.download_small(stats)
-        if int(stats_h[1]) == 0:
-            return DeviceScheme(primes, z, int(stats_h[0]), masks, attempt, 0, prep,
-                                extra=also if isinstance(also, np.ndarray) else None)
-    return DeviceScheme(primes, z, l_max, masks, attempt, int(stats_h[1]), prep,
-                        extra=also if isinstance(also, np.ndarray) else None)
+            return PendingScheme(lambda: run((guess.z, zh, wait)))
+        done = run()
+        return PendingScheme(lambda: done)
+    return run()
+
+
+class PendingScheme:
+    """``build_scheme(defer=True)``: the first attempt's alias kernel is
+    enqueued; ``finish()`` reads its stats back and completes the search
+    (further chunks / attempts) exactly as the undeferred call."""
+
+    def __init__(self, fn):
+        self._fn = fn
+        self._done = None
+
+    def finish(self) -> DeviceScheme:
+        if self._done is None:
+            self._done = self._fn()
+        return self._done
 
 
 def scheme_to_host(dev: Device, cand_rows: np.ndarray, sch: DeviceScheme) -> MultipleRank1Lattice:
@@ -836,6 +878,13 @@ def apply_cap_rows(dev: Device, coef, keep, n: int, counts_h: np.ndarray, cap: i
 def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):
     """Rows of ``cand`` whose flag (OR over ``nrows`` rows) is set, in order;
     optional coefficient gather.  Returns (DeviceFreqs, coef tensor | None)."""
+    return compact_finish(compact_start(dev, cand, flags, nrows, coef))
+
+
+def compact_start(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):
+    """First half of ``compact``: the flag scan and the asynchronous read-back
+    of the survivor count.  The caller may enqueue more device work and do
+    host work before ``compact_finish`` waits for the count."""
     torch = dev.torch
     n = cand.n
     idx = dev.empty((max(n, 1),), torch.int32)
@@ -843,7 +892,19 @@ def compact(dev: Device, cand: DeviceFreqs, flags, nrows: int, coef=None):
     sl = int(_native.query("sfft_scan_scratch_len", n))
     scr = dev.empty((max(sl, 1),), torch.int32)
     dev.call("sfft_flag_indices", dptr(flags), n, nrows, dptr(idx), dptr(total), dptr(scr), ctx="compaction")
-    cnt = int(dev.download_small(total)[0])
+    return dev, cand, idx, total, coef, dev.download_async(total)
+
+
+def compact_count(pending) -> int:
+    """The survivor count of a ``compact_start`` (waits for its read-back)."""
+    return int(pending[5]()[0])
+
+
+def compact_finish(pending):
+    dev, cand, idx, total, coef, wait = pending
+    torch = dev.torch
+    n = cand.n
+    cnt = int(wait()[0])
     out = dev.empty((cand.ncomp, max(cnt, 1)), torch.int32)
     cout = dev.empty((max(cnt, 1), 2), torch.float64) if coef is not None else None
     dev.call("sfft_gather_rows", dptr(cand.data), n, cand.ncomp, dptr(idx), dptr(total), cnt, dptr(out),

@@ -1,0 +1,78 @@
+"""The engine enqueues step t+1 (compaction gather with a guessed count,
+candidate product, first alias kernel, preparation) during step t once the
+prefix counts have settled (engine._start_next_step).  It must change
+nothing: the same report, field by field, as the engine with every step
+run after its predecessor's synchronisation — whether the guessed count
+was right (the enqueued step is used) or wrong (it is discarded)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(a, b):
+    assert np.array_equal(a.detected.freqs, b.detected.freqs)
+    assert np.array_equal(a.detected.coeffs, b.detected.coeffs)
+    for f in ("component_counts", "prefix_counts", "candidate_counts", "scheme_sizes", "lattice_attempts",
+              "detection_calls", "inversion_calls", "warnings"):
+        assert getattr(a, f) == getattr(b, f), f
+    assert a.oracle_calls == b.oracle_calls
+
+
+def _runs(monkeypatch, oracle, cfg):
+    from paper_1711_05152_b200 import engine
+    import paper_1711_05152_b200 as P
+    used, made = [], []
+    real_start = engine._start_next_step
+
+    def spy(*a, **k):
+        nxt = real_start(*a, **k)
+        made.append(nxt is not None)
+        return nxt
+    monkeypatch.setattr(engine, "_start_next_step", spy)
+    got = P.sparse_fft(oracle, cfg)
+    monkeypatch.undo()
+    real_build = engine.build_scheme
+    monkeypatch.setattr(engine, "build_scheme", lambda *a, **k: real_build(*a, **k))  # disables the overlap
+    ref = P.sparse_fft(oracle, cfg)
+    monkeypatch.undo()
+    return got, ref, made
+
+
+def test_overlapped_steps_equal_sequential_config2_shape(monkeypatch):
+    """d = 10, N = 32, s = 200, r = 3: the prefix counts settle at s, so the
+    later steps run enqueued ahead."""
+    import paper_1711_05152_b200 as P
+    truth, oracle = P.gen_random_sparse_poly(10, 32, 200, "box", seed=5, min_magnitude=1e-3)
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(10, 32), delta=1e-12, s=200, r=3, b=10, rng_seed=9)
+    got, ref, made = _runs(monkeypatch, oracle, cfg)
+    _same(got, ref)
+    assert sum(made) >= 4, made
+    assert len(got.detected) == 200
+
+
+def test_overlapped_steps_wrong_guess_discarded(monkeypatch):
+    """Every started step with a wrong count guess (forced off by one) is
+    discarded and the step runs after the synchronisation: same report."""
+    import paper_1711_05152_b200 as P
+    from paper_1711_05152_b200 import engine
+    truth, oracle = P.gen_random_sparse_poly(10, 32, 200, "box", seed=5, min_magnitude=1e-3)
+    cfg = P.DetectionConfig(box=P.SearchBox.centered(10, 32), delta=1e-12, s=200, r=3, b=10, rng_seed=9)
+    real = engine._start_next_step
+    calls = []
+
+    def off_by_one(dev, oracle_, prefixes, pend, cnt, *a):
+        if prefixes is not None:  # step 1: the exact prefix set, nothing to guess
+            return real(dev, oracle_, prefixes, pend, cnt, *a)
+        calls.append(cnt)
+        return real(dev, oracle_, prefixes, pend, cnt + 1, *a)
+    monkeypatch.setattr(engine, "_start_next_step", off_by_one)
+    got = P.sparse_fft(oracle, cfg)
+    monkeypatch.undo()
+    real_build = engine.build_scheme
+    monkeypatch.setattr(engine, "build_scheme", lambda *a, **k: real_build(*a, **k))
+    ref = P.sparse_fft(oracle, cfg)
+    monkeypatch.undo()
+    assert len(calls) >= 4
+    _same(got, ref)
