@@ -552,10 +552,13 @@ def _sample_units(dev: Device, oracle, tabs: LatticeTables, t1: int, d: int,
     tail = d - t1
     anchor = np.ascontiguousarray(np.asarray(tails, dtype=np.float64).reshape(rb, tail)) \
         if tail else np.zeros(1, dtype=np.float64)
-    ulist = list(range(rb * L)) if units is None else [int(u) for u in units]
+    ulist = range(rb * L) if units is None else [int(u) for u in units]
     uarr, nu = _unit_arg(units)
     up = hptr(uarr) if uarr is not None else 0
-    nodes = sum(int(tabs.ms[u % L]) for u in ulist)
+    if units is None:
+        nodes = rb * int(tabs.ms.sum())
+    else:
+        nodes = int(tabs.ms[np.asarray(ulist, dtype=np.int64) % L].sum()) if len(ulist) else 0
     base = oracle.inner if isinstance(oracle, NoisyOracle) else oracle
     device_inner = isinstance(base, (SparsePolynomialOracle, BSplineOracle))
     noisy = isinstance(oracle, NoisyOracle)
@@ -644,7 +647,7 @@ def _add_lattice_noise(dev: Device, oracle: NoisyOracle, tabs: LatticeTables, rb
         dev.call("sfft_finish_devnoise", hptr(tabs.ms), L, rb, dptr(tabs.chirp), dptr(buf), P,
                  dptr(nrm) if nrm is not None else 0, getattr(oracle, "rel", 0.0), oracle.sigma,
                  oracle.device_key, base, 1, up, nuarg, ctx="device noise")
-        oracle.count_samples(sum(int(tabs.ms[u % L]) for u in ulist))
+        oracle.count_samples(int(tabs.ms[np.asarray(list(ulist), dtype=np.int64) % L].sum()) if len(ulist) else 0)
         return
     norms = {}
     if oracle.needs_norm():
