@@ -226,6 +226,12 @@ __device__ __forceinline__ constexpr int out_slot(int r) {
   return (R & (R - 1)) == 0 ? bitrev_small(r, Log2<R>::v) : r;
 }
 
+// Row stride of the mixed-radix column tiles: the padded length made odd, so
+// the rows of consecutive columns start in different 16-byte bank groups (the
+// column-fastest first-pass stores and last-pass loads of C = 8 columns were
+// 2-way bank conflicts with the even stride of N = 200: 226)
+__host__ __device__ constexpr int rstride_x(int n) { return Tile<2048>::rstride(n) | 1; }
+
 // One Stockham pass of radix R (any R <= 8) over ROWS rows of length N in
 // shared memory (E = ROWS * N elements); NS = product of the radices already
 // applied.  All sizes are compile-time (divisions become multiplies); the
@@ -237,7 +243,7 @@ __device__ __forceinline__ void stockham_pass_x(double2* s, const double2* __res
   constexpr int per_row = N / R;
   constexpr int nb = ROWS * per_row;
   constexpr int tstep = N / (NS * R);
-  constexpr int rstride = Tile<2048>::rstride(N);
+  constexpr int rstride = rstride_x(N);
   double2 v[BPT][R];
   int obase[BPT];
 #pragma unroll

@@ -28,7 +28,7 @@ fft_colx_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeo
   constexpr int P2 = 2048;
   constexpr int C = fft_col_ctas_cols(P1, 2048);
   constexpr int E = C * P1;
-  constexpr int rstride = Tile<2048>::rstride(P1);
+  constexpr int rstride = rstride_x(P1);
   const int u = blockIdx.y;
   const int c0 = blockIdx.x * C;
   const int lat = ut.lat[u];
@@ -148,7 +148,7 @@ fft_colx2_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGe
   constexpr int P2 = 2048;
   constexpr int C = fft_col_ctas_cols(P1, 2048);
   constexpr int E = C * P1;
-  constexpr int rstride = Tile<2048>::rstride(P1);
+  constexpr int rstride = rstride_x(P1);
   static_assert(CP::NP >= 2, "hand-off variant needs distinct first and last passes");
   const int u = blockIdx.y;
   const int c0 = blockIdx.x * C;
@@ -247,7 +247,7 @@ template <int A, int F>
 static int launch_colx_t(bool inv, const FftGeom& g, dim3 grid, cudaStream_t st, double2* buf, int64_t us,
                          const UnitTable& ut, int mask, const double2* ftab, const double2* chirp) {
   constexpr int P1 = F << A;
-  const size_t sm = (size_t)fft_col_ctas_cols(P1, 2048) * Tile<2048>::rstride(P1) * sizeof(double2);
+  const size_t sm = (size_t)fft_col_ctas_cols(P1, 2048) * rstride_x(P1) * sizeof(double2);
   if constexpr (ColPasses<F, A>::NP >= 2) {
     if (colx2_enabled()) {
       const void* fn2 = inv ? (const void*)fft_colx2_kernel<A, F, true> : (const void*)fft_colx2_kernel<A, F, false>;

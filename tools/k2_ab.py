@@ -17,10 +17,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-VARIANTS = {
-    "rowp0 (one row per CTA)": {"SFFT_B200_FFT_ROWP": "0"},
-    "rowp1 (persistent, 1 CTA/SM)": {"SFFT_B200_FFT_ROWP": "1"},
-    "rowp2 (persistent, 2 CTA/SM)": {"SFFT_B200_FFT_ROWP": "2"},
+VARIANTS = {  # environment switches of the variants to compare (the first is the reference)
+    "default": {},
 }
 
 
