@@ -315,10 +315,26 @@ def secondary_rooflines(dev, sch, n, d, kernels):
             ("alias", 2 * 4 * d * n, {}),
             ("gather", 4 * d * n + 16 * bins + 17 * n, {"alias_free_bins": bins})):
         ms = kernels[name]
+        if not ms > 0:  # class not launched in the timed steps (e.g. the sharded step's merge kernels instead)
+            out[name] = dict(bound="hbm", algorithmic_bytes=nbytes, ms=None, achieved=None, peak=peak,
+                             unit="GB/s", frac=None, **extra)
+            continue
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = dict(bound="hbm", algorithmic_bytes=nbytes, ms=ms, achieved=gbs, peak=peak, unit="GB/s",
                          frac=gbs / peak, **extra)
     out["peak_source"] = src
+    # K2 against the traffic any three-pass Bluestein FFT of these lengths must
+    # move (P >= 2M - 1 per unit): read the M samples, write P, read P and the
+    # P-point Bhat row, write P, read P, write the M-point spectrum
+    from paper_1711_05152_b200.mr1l import fft_size
+    P_len = fft_size(int(max(sch.primes[:L])))
+    floor_bytes = 16 * (2 * sum_m + 5 * P_len * L)
+    floor_ms = floor_bytes / (peak * 1e9) * 1e3
+    out["bluestein_fft"]["three_pass_floor"] = {
+        "bytes": floor_bytes, "P": P_len, "floor_ms": floor_ms,
+        "frac": floor_ms / kernels["bluestein_fft"] if kernels["bluestein_fft"] > 0 else None,
+        "note": "16 B x (2 sum M + 5 L P): the DRAM traffic of a column / fused-row / column Bluestein pass "
+                "sequence without L2 reuse, against the measured HBM copy peak"}
     # K3's bytes are L2-resident bitmaps: its roofline is random L2 operations.
     # Counted: one atomicOr (first bitmap) and one load (second bitmap) per
     # candidate and lattice of the first chunk; the rarer second-bitmap
@@ -335,7 +351,7 @@ def secondary_rooflines(dev, sch, n, d, kernels):
     floor_ms = (ops / (rates["atomic_or"] * 1e9) + ops / (rates["load"] * 1e9)) * 1e3
     out["alias"]["l2_random"] = {
         "bound": "l2_random_ops", "lattices_evaluated": lhi, "atomic_or_ops": ops, "load_ops": ops,
-        "peak_gops": rates, "floor_ms": floor_ms, "frac": floor_ms / kernels["alias"],
+        "peak_gops": rates, "floor_ms": floor_ms, "frac": floor_ms / kernels["alias"] if kernels["alias"] > 0 else None,
         "peak_source": "measured in this run: random 32-bit atomicOr / loads on an L2-resident bitmap of the "
                        "alias scratch's size (sfft_l2_random_peak)"}
     return out
@@ -489,9 +505,13 @@ def run_ours(args):
     s_terms = wl.oracle.s
     # one (node, term) complex multiply-add = 8 flop; the kernel
     # executes it as 3 real multiply-adds (6 flop, 3-multiplication product)
-    flops = 8.0 * s_terms * sch.total_size
+    # (N > 1: this rank's share, the units it owns, parallel.owned_units)
+    from paper_1711_05152_b200.parallel import owned_units
+    local_nodes = int(sum(int(sch.primes[u % sch.L]) for u in owned_units(sch.L, world, rank))) \
+        if world > 1 else int(sch.total_size)
+    flops = 8.0 * s_terms * local_nodes
     achieved = flops / (kernels["sample_poly"] * 1e-3) / 1e12
-    executed = 6.0 * s_terms * sch.total_size / (kernels["sample_poly"] * 1e-3) / 1e12
+    executed = 6.0 * s_terms * local_nodes / (kernels["sample_poly"] * 1e-3) / 1e12
     traffic = load_traffic()
     others = secondary_rooflines(dev, sch, n, 10, kernels)
 
@@ -604,7 +624,8 @@ def run_ours(args):
                                     f"({peak_dfma:.2f}) and DMMA m8n8k4 loop ({peak_dmma:.2f}) "
                                     "(sfft_fp64_peak / sfft_fp64_mma_peak); MEASURED_PEAKS.json has no FP64 figure",
                      "algorithmic": f"SURVEY §8(d): 8 flop per (node, term) complex multiply-add x {s_terms} "
-                                    f"terms x {sch.total_size} nodes per launch",
+                                    f"terms x {local_nodes} nodes per launch"
+                                    + (f" (this rank's units of the {sch.total_size}-node step)" if world > 1 else ""),
                      "executed": {"achieved": executed, "frac": executed / peak,
                                   "note": "6 flop per (node, term) actually issued: the 3-multiplication complex "
                                           "product (3 real DMMA multiply-adds); frac > 1 above is that saving"},
