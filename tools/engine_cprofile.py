@@ -1,4 +1,4 @@
-"""cProfile one warm config-2 sparse_fft (host hotspots; run on a GPU box)."""
+"""cProfile warm sparse_fft runs of config 2 (default) or 4 (`4`): host hotspots (run on a GPU box)."""
 import cProfile
 import pstats
 import sys
@@ -10,7 +10,7 @@ from paper_1711_05152_b200 import workloads  # noqa: E402
 from paper_1711_05152_b200.device import get_device  # noqa: E402
 
 dev = get_device()
-wl = workloads.config2()
+wl = workloads.config4() if len(sys.argv) > 1 and sys.argv[1] == "4" else workloads.config2()
 P.sparse_fft(wl.oracle, wl.cfg)
 dev.sync()
 pr = cProfile.Profile()
