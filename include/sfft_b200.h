@@ -33,10 +33,10 @@
 extern "C" {
 #endif
 
-/* ABI history: 3 = anchor tables of the sampling entries limited to
+/* ABI history: 4 = sfft_copy_async added (no signature changed).  3 = anchor tables of the sampling entries limited to
  * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
  * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
-#define SFFT_B200_ABI_VERSION 3
+#define SFFT_B200_ABI_VERSION 4
 
 int sfft_abi_version(void);
 /* kernels launched by this library since load (all devices, all streams) */
@@ -51,6 +51,10 @@ int sfft_profile_collect(int cls, double* total_ms, int* count);
 const char* sfft_error_string(int code);
 /* number of SMs and compute capability of the current device */
 int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);
+/* cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, stream): the engine's
+ * read-backs of small results into pinned host buffers (host page-locked
+ * memory for an asynchronous copy), without a framework's stream switch */
+int sfft_copy_async(void* dst, const void* src, int64_t nbytes, void* stream);
 
 /* ---- K3: alias histogram, masks, coverage --------------------------------
  * Replaces construct.py:139-143 (_alias_free_mask) evaluated for every prime

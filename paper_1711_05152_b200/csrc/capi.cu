@@ -444,6 +444,12 @@ int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor) {
   return 0;
 }
 
+int sfft_copy_async(void* dst, const void* src, int64_t nbytes, void* stream) {
+  if (nbytes < 0 || (nbytes > 0 && (!dst || !src))) return E_INVAL;
+  if (nbytes == 0) return 0;
+  return (int)cudaMemcpyAsync(dst, src, (size_t)nbytes, cudaMemcpyDefault, S(stream));
+}
+
 int64_t sfft_alias_scratch_words(const int64_t* h_m, int L) {
   int64_t acc = 0;
   for (int l = 0; l < L; ++l) acc += (h_m[l] + 31) >> 5;

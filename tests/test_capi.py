@@ -45,7 +45,7 @@ def test_sm100a_cubin_embedded():
 def test_size_queries_without_gpu(lib):
     from paper_1711_05152_b200 import _native
     import numpy as np
-    assert _native.query("sfft_abi_version") == 3
+    assert _native.query("sfft_abi_version") == 4
     assert _native.query("sfft_fft_table_len", 3) == -1
     n18 = _native.query("sfft_fft_table_len", 1 << 18)
     # [P1 | P2 | 2^9 | 2^9] with P = 2^18 = 2^7 * 2^11 (2048-point tiles up to 2^22)
