@@ -266,8 +266,9 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
     side = dev.copy_stream()
     side.wait_event(ready)
-    with torch.cuda.stream(side):
-        words_h.copy_(sch.masks.view(torch.uint8), non_blocking=True)
+    from . import _native
+    _native.call("sfft_copy_async", words_h.data_ptr(), sch.masks.data_ptr(), n * 8, side.cuda_stream,
+                 ctx="masks read-back")
     sch.masks.record_stream(side)
     res.finalize()  # cap applied (if binding) before the results are read
     coef, keep = dev.download_many(res.coef[0], res.keep[0])

@@ -31,6 +31,21 @@ def dptr(t) -> int:
     return t.data_ptr()
 
 
+def _torch_dtypes():
+    torch = _torch()
+    return {"i4": torch.int32, "i8": torch.int64, "f8": torch.float64, "f4": torch.float32, "u1": torch.uint8,
+            "i2": torch.int16, "i1": torch.int8, "b1": torch.bool}
+
+
+class _LazyDtypes(dict):
+    def __missing__(self, key):
+        self.update(_torch_dtypes())
+        return dict.__getitem__(self, key)
+
+
+_TORCH_DTYPE = _LazyDtypes()
+
+
 class Device:
     """One CUDA device + stream used by the MR1L engine."""
 
@@ -75,9 +90,11 @@ class Device:
 
     def upload(self, a: np.ndarray, dtype=None, asynchronous: bool = False):
         """Host numpy -> device tensor (ordered on the engine stream).
-        ``asynchronous``: stage through (cached) pinned memory and return
-        without waiting for the copy."""
+        ``asynchronous``: stage through a pinned buffer of the upload ring and
+        return without waiting for the copy."""
         torch = self.torch
+        if asynchronous and dtype is None:
+            return self._upload_async(np.ascontiguousarray(a))
         t = torch.from_numpy(np.ascontiguousarray(a))
         if dtype is not None:
             t = t.to(dtype)
@@ -85,6 +102,37 @@ class Device:
             t = t.pin_memory()
         with torch.cuda.stream(self.stream):
             return t.to(self.device, non_blocking=asynchronous)
+
+    _RING = 16
+
+    def _upload_async(self, a: np.ndarray):
+        """The array through a ring of pinned staging buffers and one
+        cudaMemcpyAsync of the library on the engine stream.  A slot is
+        reused only after the copy that last used it has completed (its
+        event), so the caller may drop ``a`` at once."""
+        torch = self.torch
+        nbytes = a.nbytes
+        ring = self.__dict__.setdefault("_up_ring", [])
+        i = self.__dict__.get("_up_next", 0)
+        self._up_next = (i + 1) % self._RING
+        if i < len(ring):
+            buf, ev = ring[i]
+            if ev is not None:
+                ev.synchronize()
+        else:
+            buf, ev = None, None
+            ring.append((None, None))
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty((max(nbytes, 256),), dtype=torch.uint8, pin_memory=True)
+        buf[:nbytes].numpy()[:] = a.reshape(-1).view(np.uint8)
+        out = torch.empty(a.shape, dtype=_TORCH_DTYPE[a.dtype.str[1:]], device=self.device)
+        if nbytes:
+            _native.call("sfft_copy_async", out.data_ptr(), buf.data_ptr(), nbytes, self.sh, ctx="upload")
+        if ev is None:
+            ev = torch.cuda.Event()
+        ev.record(self.stream)
+        ring[i] = (buf, ev)
+        return out
 
     def download(self, t) -> np.ndarray:
         with self.torch.cuda.stream(self.stream):

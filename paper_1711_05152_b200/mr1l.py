@@ -94,8 +94,15 @@ class DeviceFreqs:
         the extent later with ``extent_of`` (one synchronisation fewer)."""
         torch = dev.torch
         n, d = (int(x) for x in rows.shape)
-        with torch.cuda.stream(dev.stream):
-            d_rows = rows.to(dev.device, non_blocking=bool(rows.is_pinned()))
+        if rows.is_pinned() and rows.is_contiguous() and rows.dtype == torch.int64:
+            # one cudaMemcpyAsync of the library on the engine stream (asynchronous DMA)
+            d_rows = torch.empty((n, d), dtype=torch.int64, device=dev.device)
+            if n * d:
+                _native.call("sfft_copy_async", d_rows.data_ptr(), rows.data_ptr(), n * d * 8, dev.sh,
+                             ctx="row upload")
+        else:
+            with torch.cuda.stream(dev.stream):
+                d_rows = rows.to(dev.device, non_blocking=bool(rows.is_pinned()))
         out = dev.empty((d, n), torch.int32)
         mm = dev.empty((2 * d + 1,), torch.int32)
         dev.call("sfft_pack_rows", dptr(d_rows), n, d, dptr(out), dptr(mm), ctx="pack rows")

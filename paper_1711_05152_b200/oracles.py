@@ -170,8 +170,14 @@ class SparsePolynomialOracle(_DeviceOracle):
                 cf = np.ascontiguousarray(np.stack([self.coeffs.real, self.coeffs.imag], axis=1))
                 host = (torch.from_numpy(hf).pin_memory(), torch.from_numpy(cf).pin_memory())
                 self._pinned_terms = host
-            with torch.cuda.stream(dev.stream):
-                got = tuple(h.to(dev.device, non_blocking=True) for h in host)
+            # asynchronous DMA from the persistent pinned copy (one library
+            # cudaMemcpyAsync each, no framework stream switch)
+            from . import _native
+            got = tuple(torch.empty(h.shape, dtype=h.dtype, device=dev.device) for h in host)
+            for g_, h in zip(got, host):
+                if h.numel():
+                    _native.call("sfft_copy_async", g_.data_ptr(), h.data_ptr(), h.numel() * h.element_size(),
+                                 dev.sh, ctx="oracle terms")
             self._dev_cache[dev.index] = got
         return got
 
