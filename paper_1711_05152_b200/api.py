@@ -147,14 +147,6 @@ def build_multiple_lattice_with_retries(I: FrequencyIndexSet, cfg: MLConfig, b: 
 # one MR1L reconstruction step with a known candidate set (BASELINE config 1)
 
 @dataclass
-class _Shape:
-    """The (n, t+1) of a candidate set before it is on the device (prepare_step
-    needs only the shape)."""
-    n: int
-    ncomp: int
-
-
-@dataclass
 class StepReport:
     coeffs: np.ndarray        # (n,) complex; 0 where uncovered
     covered: np.ndarray       # (n,) bool
@@ -206,10 +198,10 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
 
     def ahead():
         """While the rows are in flight: the first attempt's primes and draw
-        (valid unless the set's spread exceeds lambda; lazy streams only),
-        the alias buffers, and the step preparation for that attempt (its
-        kernels need no candidate data, so they are queued before the
-        read-back of the rows' extent)."""
+        (valid unless the set's spread exceeds lambda; lazy streams only) and
+        the alias buffers.  The step preparation follows the alias kernel
+        (build_scheme's ``prepare``), so the alias kernel runs as soon as the
+        rows have arrived while the host prepares."""
         from . import _native
         g = speculate_scheme(n, t1, seed_seq, b)
         spec.append(g)
@@ -218,11 +210,6 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         early["bufs"] = (dev.empty((max(words, 1),), torch.int32), dev.empty((n,), torch.int64),
                          dev.empty((2,), torch.int32))
         early["words_h"] = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
-        from .mr1l import first_chunk
-        lhi = first_chunk(n, ms)
-        shape = _Shape(n, t1)
-        early["prep"] = prepare_step(dev, oracle, shape, 1, ms[:lhi],
-                                     np.ascontiguousarray(g.z[:lhi].astype(np.int32)), tails=[tail], d=d)
 
     def defer_extent():
         """Skip the read-back of the rows' extent before the alias kernel when
@@ -234,22 +221,19 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None,
                                                 defer=defer_extent)
     guess = spec[0] if spec else None
+    prepare = lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)  # noqa: E731
     if hi is None:  # deferred: alias with the guess, extent read back with the stats
         sch = build_scheme(dev, cand, b, seed_seq, box_extent=0, lazy_streams=fresh, guess=guess,
-                           bufs=early.get("bufs"), also=lo)
+                           bufs=early.get("bufs"), also=lo, prepare=prepare)
         lo, hi, kmax = DeviceFreqs.extent_of(sch.extra.view(np.int32), t1, n)
         cand.kmax = kmax
         if not (sch.attempts == 1 and sch.z is guess.z and guess.primes[0] > int((hi - lo).max())):
             # the guess did not hold (spread >= lambda): the reference's construction
             sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                               prepare=lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d))
+                               prepare=prepare)
     else:
         sch = build_scheme(dev, cand, b, seed_seq, box_extent=int((hi - lo).max()), lazy_streams=fresh,
-                           prepare=None if guess is not None else
-                           (lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)),
-                           guess=guess, bufs=early.get("bufs"))
-    if guess is not None and sch.prep is None and sch.attempts == 1 and sch.z is guess.z:
-        sch.prep = early.get("prep")  # made for exactly this attempt's lattices
+                           prepare=prepare, guess=guess, bufs=early.get("bufs"))
     # the masks are final once the scheme is built: their copy to the host runs
     # on a side stream while the sampling kernel runs (enqueued after the
     # sampling launch, so the launch is not delayed by it)

@@ -329,11 +329,15 @@ def build_scheme(dev: Device, cand: DeviceFreqs, b: int, seed_seq: np.random.See
                 zh = np.ascontiguousarray(z.astype(np.int32))
                 alias(zh, 0, l_hi)
                 if prepare is not None and attempt == 1:
-                    # read the stats back through an event, so the preparation kernels
-                    # queued behind the alias kernel run while the host continues
+                    # read the stats (and ``also``) back through events, so the
+                    # preparation kernels queued behind the alias kernel run while
+                    # the host continues
                     wait = dev.download_async(stats)
+                    wait_x = dev.download_async(extra) if extra is not None else None
                     prep = prepare(ms[:l_hi], zh[:l_hi])
                     stats_h = wait()
+                    if wait_x is not None:
+                        extra = wait_x()  # handed back in DeviceScheme.extra
                 elif extra is not None and attempt == 1:
                     stats_h, extra = dev.download_many(stats, extra)  # extra handed back in DeviceScheme.extra
                     stats_h = stats_h.view(np.int32)
