@@ -33,7 +33,8 @@
 extern "C" {
 #endif
 
-/* ABI history: 4 = sfft_copy_async added (no signature changed).  3 = anchor tables of the sampling entries limited to
+/* ABI history: 4 = sfft_copy_async and sfft_line_sample_poly_all added (no
+ * signature changed).  3 = anchor tables of the sampling entries limited to
  * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
  * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
 #define SFFT_B200_ABI_VERSION 4
@@ -268,6 +269,12 @@ int sfft_residues(const int32_t* d_freqs, int64_t n, int t1, int64_t kmax, const
  * the cap is sfft_select_cap_rows with those counts. */
 int sfft_line_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int t,
                           int K, const double* h_anchors, int r, double* d_values, void* stream);
+/* The r lines of every component t < d in one launch (a centred box: the
+ * same K <= 1024 for all components): line g = t * r + i with anchors
+ * h_anchors[g * d ...] (d * r * d <= 2048 doubles), values row g; the same
+ * samples as d calls of sfft_line_sample_poly. */
+int sfft_line_sample_poly_all(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int K,
+                              const double* h_anchors, int r, double* d_values, void* stream);
 int sfft_line_bins(const double* d_spectra, int64_t P, int r, int K, int64_t lo, double delta,
                    double* d_coefs, uint8_t* d_keep, int32_t* d_counts, void* stream);
 int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, double delta,

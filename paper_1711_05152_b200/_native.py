@@ -68,6 +68,7 @@ _SIGS = {
     "sfft_candidate_product": (_int, [_vp, _i64, _int, _vp, _i64, _vp, _vp]),
     "sfft_residues": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _vp]),
     "sfft_line_sample_poly": (_int, [_vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _vp]),
+    "sfft_line_sample_poly_all": (_int, [_vp, _vp, _int, _int, _int, _vp, _int, _vp, _vp]),
     "sfft_line_select": (_int, [_vp, _int, _int, _i64, _int, _dbl, _vp, _vp, _vp]),
     "sfft_line_bins": (_int, [_vp, _i64, _int, _int, _i64, _dbl, _vp, _vp, _vp, _vp]),
     "sfft_eval_poly_points": (_int, [_vp, _i64, _int, _vp, _vp, _int, _vp, _vp]),

@@ -845,6 +845,15 @@ int sfft_line_sample_poly(const int32_t* d_hfreqs, const double* d_hcoef, int s,
                                  (double2*)d_values, S(stream));
 }
 
+int sfft_line_sample_poly_all(const int32_t* d_hfreqs, const double* d_hcoef, int s, int d, int K,
+                              const double* h_anchors, int r, double* d_values, void* stream) {
+  if (d < 1 || r < 1 || (int64_t)d * r * d > 2048) return E_2BIG;
+  LineAnchors la;
+  for (int i = 0; i < d * r * d; ++i) la.a[i] = h_anchors[i];
+  return launch_line_sample_poly_all(d_hfreqs, (const double2*)d_hcoef, s, d, K, la, r, (double2*)d_values,
+                                     S(stream));
+}
+
 int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, double delta,
                      double* d_coefs, uint8_t* d_keep, void* stream) {
   return launch_line_select((const double2*)d_values, r, K, lo, cap, delta, (double2*)d_coefs,

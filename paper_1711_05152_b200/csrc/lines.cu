@@ -21,14 +21,22 @@ namespace sfft {
 constexpr int LT = 256;
 constexpr int LCH = 512;  // terms per shared-memory chunk
 
+// Grid (line, block of 32 points): each CTA evaluates 32 consecutive points
+// of one line (8 warps split the terms, lane = point), so all lines and
+// point blocks of a launch run side by side.  ``t`` >= 0: every line is of
+// component t; t < 0: line g is of component g / rpc (all components'
+// lines in one launch, anchors la.a + g * d).  Each point's sum runs in the
+// same order whatever the grid: terms in chunks of LCH, warp w taking terms
+// w, w + 8, ..., the 8 warp sums added in warp order.
 __global__ void __launch_bounds__(LT)
 line_sample_poly_kernel(const int32_t* __restrict__ hf, const double2* __restrict__ coef, int s,
-                        int d, int t, int K, LineAnchors la, double2* __restrict__ values) {
+                        int d, int t, int rpc, int K, LineAnchors la, double2* __restrict__ values) {
   __shared__ double2 cs[LCH];
   __shared__ int es[LCH];
   __shared__ double2 wk[1024];
   __shared__ double2 part[8][32];
   const int line = blockIdx.x;
+  const int tc = t >= 0 ? t : line / rpc;
   const double* a = la.a + line * d;
   for (int q = threadIdx.x; q < K; q += LT) {
     double sn, c;
@@ -36,48 +44,46 @@ line_sample_poly_kernel(const int32_t* __restrict__ hf, const double2* __restric
     wk[q] = make_double2(c, sn);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int l0 = 0; l0 < K; l0 += 32) {
-    const int l = l0 + lane;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int h0 = 0; h0 < s; h0 += LCH) {
-      __syncthreads();
-      for (int q = threadIdx.x; q < LCH; q += LT) {
-        const int h = h0 + q;
-        double2 cc = make_double2(0.0, 0.0);
-        int e = 0;
-        if (h < s) {
-          double ph = 0.0;
-          for (int u = 0; u < d; ++u)
-            if (u != t) ph += (double)hf[(int64_t)u * s + h] * a[u];
-          double sn, c;
-          sincospi(2.0 * ph, &sn, &c);
-          cc = cmul(coef[h], make_double2(c, sn));
-          e = (int)mod_slow((int64_t)hf[(int64_t)t * s + h], K);
-        }
-        cs[q] = cc;
-        es[q] = e;
-      }
-      __syncthreads();
-      if (l < K) {
-        for (int q = w; q < LCH && h0 + q < s; q += 8) {
-          const int idx = (int)(((int64_t)es[q] * l) % K);
-          const double2 tw = wk[idx];
-          const double2 cc = cs[q];
-          acc.x = fma(cc.x, tw.x, acc.x);
-          acc.x = fma(-cc.y, tw.y, acc.x);
-          acc.y = fma(cc.x, tw.y, acc.y);
-          acc.y = fma(cc.y, tw.x, acc.y);
-        }
-      }
-    }
-    part[w][lane] = acc;
+  const int l0 = blockIdx.y * 32;
+  const int l = l0 + lane;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int h0 = 0; h0 < s; h0 += LCH) {
     __syncthreads();
-    if (w == 0 && l < K) {
-      double2 t2 = part[0][lane];
-      for (int q = 1; q < 8; ++q) t2 = cadd(t2, part[q][lane]);
-      values[(int64_t)line * K + l] = t2;
+    for (int q = threadIdx.x; q < LCH; q += LT) {
+      const int h = h0 + q;
+      double2 cc = make_double2(0.0, 0.0);
+      int e = 0;
+      if (h < s) {
+        double ph = 0.0;
+        for (int u = 0; u < d; ++u)
+          if (u != tc) ph += (double)hf[(int64_t)u * s + h] * a[u];
+        double sn, c;
+        sincospi(2.0 * ph, &sn, &c);
+        cc = cmul(coef[h], make_double2(c, sn));
+        e = (int)mod_slow((int64_t)hf[(int64_t)tc * s + h], K);
+      }
+      cs[q] = cc;
+      es[q] = e;
     }
     __syncthreads();
+    if (l < K) {
+      for (int q = w; q < LCH && h0 + q < s; q += 8) {
+        const int idx = (int)(((int64_t)es[q] * l) % K);
+        const double2 tw = wk[idx];
+        const double2 cc = cs[q];
+        acc.x = fma(cc.x, tw.x, acc.x);
+        acc.x = fma(-cc.y, tw.y, acc.x);
+        acc.y = fma(cc.x, tw.y, acc.y);
+        acc.y = fma(cc.y, tw.x, acc.y);
+      }
+    }
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && l < K) {
+    double2 t2 = part[0][lane];
+    for (int q = 1; q < 8; ++q) t2 = cadd(t2, part[q][lane]);
+    values[(int64_t)line * K + l] = t2;
   }
 }
 
@@ -207,10 +213,20 @@ line_select_kernel(const double2* __restrict__ values, int K, int64_t lo, int ca
 int launch_line_sample_poly(const int32_t* hf, const double2* coef, int s, int d, int t, int K,
                             const LineAnchors& la, int r, double2* values, cudaStream_t st) {
   if (K < 1 || r <= 0 || r > 65535) return -22;
-  if (K > 1024)
+  if (K > 1024) {
+    if (t < 0) return -22;
     line_sample_poly_big_kernel<<<dim3((K + LT - 1) / LT, r), LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
-  else
-    line_sample_poly_kernel<<<r, LT, 0, st>>>(hf, coef, s, d, t, K, la, values);
+  } else {
+    line_sample_poly_kernel<<<dim3(r, (K + 31) / 32), LT, 0, st>>>(hf, coef, s, d, t, r, K, la, values);
+  }
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
+int launch_line_sample_poly_all(const int32_t* hf, const double2* coef, int s, int d, int K,
+                                const LineAnchors& la, int r, double2* values, cudaStream_t st) {
+  if (K < 1 || K > 1024 || r <= 0 || (int64_t)r * d > 65535) return -22;
+  line_sample_poly_kernel<<<dim3(r * d, (K + 31) / 32), LT, 0, st>>>(hf, coef, s, d, -1, r, K, la, values);
   SFFT_CHECK_LAUNCH();
   return 0;
 }

@@ -312,7 +312,15 @@ def _detect_all_launch(dev: Device, oracle, cfg: DetectionConfig, streams):
     for t in range(d):
         rng = np.random.default_rng(streams[t])
         anchors.append(np.stack([np.zeros(d) if zero else rng.random(d) for _ in range(r)]))
-        if poly:  # launched as soon as the component's anchors exist (the GPU starts early)
+    if poly and d * r * d <= 2048:
+        # every component's r lines in one launch (line g = t r + i)
+        hf, cf = base.device_terms(dev)
+        a_all = np.ascontiguousarray(np.concatenate(anchors))
+        dev.call("sfft_line_sample_poly_all", dptr(hf), dptr(cf), base.s, d, K, hptr(a_all), r, dptr(vals),
+                 ctx="line sampling, all components")
+        base.count_samples(d * r * K)  # the oracle's own call audit, as _line_values
+    elif poly:
+        for t in range(d):
             _line_values(dev, oracle, t, box, anchors[t], t, 0, out=vals[t * r:(t + 1) * r])
     if not poly:
         pts = np.repeat(np.concatenate(anchors), K, axis=0)

@@ -76,3 +76,31 @@ def test_overlapped_steps_wrong_guess_discarded(monkeypatch):
     monkeypatch.undo()
     assert len(calls) >= 4
     _same(got, ref)
+
+
+def test_line_sampling_all_components_bit_identical():
+    """sfft_line_sample_poly_all (every component's lines in one launch) gives
+    the samples of d separate sfft_line_sample_poly calls, bit for bit."""
+    import paper_1711_05152_b200 as P
+    from paper_1711_05152_b200.device import dptr, get_device, hptr
+    dev = get_device()
+    torch = dev.torch
+    truth, oracle = P.gen_random_sparse_poly(6, 20, 300, "box", seed=3, min_magnitude=1e-3)
+    hf, cf = oracle.device_terms(dev)
+    d, r, K = 6, 3, 41
+    anchors = np.random.default_rng(2).random((d, r, d))
+    ref = dev.empty((d * r, K, 2), torch.float64)
+    for t in range(d):
+        a = np.ascontiguousarray(anchors[t])
+        dev.call("sfft_line_sample_poly", dptr(hf), dptr(cf), oracle.s, d, t, K, hptr(a), r, dptr(ref[t * r:]))
+    got = dev.empty((d * r, K, 2), torch.float64)
+    a_all = np.ascontiguousarray(anchors.reshape(d * r, d))
+    dev.call("sfft_line_sample_poly_all", dptr(hf), dptr(cf), oracle.s, d, K, hptr(a_all), r, dptr(got))
+    assert np.array_equal(dev.download(got), dev.download(ref))
+    # and against the oracle itself at the line points
+    pts = np.repeat(anchors.reshape(d * r, d), K, axis=0)
+    for t in range(d):
+        pts[t * r * K:(t + 1) * r * K, t] = np.tile(np.arange(K) / K, r)
+    want = oracle(pts).reshape(d * r, K)
+    g = dev.download(got)
+    assert np.abs(g[..., 0] + 1j * g[..., 1] - want).max() <= 1e-10 * np.abs(want).max()
