@@ -287,7 +287,7 @@ int launch_combine_units(int64_t n, int L, const uint64_t* masks, const double2*
 // length n are OR-ed (union of the kept sets of several iterations).
 
 constexpr int SCAN_T = 256;
-constexpr int SCAN_PER = 8;
+constexpr int SCAN_PER = 1;  // one element per thread: n = 65000 gives 254 CTAs (8 per thread gave 32 CTAs, ~12 us each pass)
 constexpr int SCAN_TILE = SCAN_T * SCAN_PER;
 
 __device__ __forceinline__ int flag_at(const uint8_t* __restrict__ flags, int64_t n, int nrows, int64_t i) {
