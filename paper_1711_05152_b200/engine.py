@@ -366,6 +366,17 @@ def detect_component(oracle, t: int, cfg: DetectionConfig, rng: np.random.Genera
 # ---------------------------------------------------------------------------
 # the engine
 
+def _tables_cached_only() -> bool:
+    """The step preparation builds the per-size tables of the first alias
+    chunk's lattices when they are not cached, behind the alias kernel and
+    off the host's critical path (a few more lattices than the early exit
+    keeps; cold d = 10 runs 0.3 ms faster, `profiles/r02ax_cold_ab.jsonl`).
+    SFFT_B200_PREP_TABLES=0: only cached tables there, run_step builds the
+    L it uses after the alias read-back."""
+    import os
+    return os.environ.get("SFFT_B200_PREP_TABLES", "1") == "0"
+
+
 def _overlap_enabled() -> bool:
     """SFFT_B200_ENGINE_OVERLAP=0 runs every step after its predecessor's
     synchronisation (the A/B of tools/run_configs.py)."""
@@ -418,7 +429,7 @@ def _start_next_step(dev: Device, oracle, prefixes: DeviceFreqs | None, pend, cn
                            lazy_streams=True, guess=g, bufs=bufs, defer=True)
     lhi = first_chunk(n, ms)
     prep = prepare_step(dev, oracle, cand, len(tails), ms[:lhi], np.ascontiguousarray(g.z[:lhi].astype(np.int32)),
-                        cached_tables_only=True, tails=tails, d=d)
+                        cached_tables_only=_tables_cached_only(), tails=tails, d=d)
     return _NextStep(cnt, prefixes, cand, pending, g, prep)
 
 
@@ -541,7 +552,7 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
             # while the alias kernel runs: buffers, the sampling operands
             # (and the tables, when this step's sizes were seen before)
             prepare = lambda ms, z: prepare_step(dev, oracle, cand, r_tilde, ms, z,  # noqa: E731
-                                                 cached_tables_only=True, tails=tails, d=d)
+                                                 cached_tables_only=_tables_cached_only(), tails=tails, d=d)
             if started is not None:
                 sch = started.pending.finish()
                 if sch.prep is None and sch.attempts == 1 and sch.z is started.guess.z:
