@@ -33,8 +33,8 @@
 extern "C" {
 #endif
 
-/* ABI history: 4 = sfft_copy_async and sfft_line_sample_poly_all added (no
- * signature changed).  3 = anchor tables of the sampling entries limited to
+/* ABI history: 4 = sfft_copy_async, sfft_masks_covered and
+ * sfft_line_sample_poly_all added (no signature changed).  3 = anchor tables of the sampling entries limited to
  * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
  * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
 #define SFFT_B200_ABI_VERSION 4
@@ -56,6 +56,10 @@ int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);
  * read-backs of small results into pinned host buffers (host page-locked
  * memory for an asynchronous copy), without a framework's stream switch */
 int sfft_copy_async(void* dst, const void* src, int64_t nbytes, void* stream);
+/* d_out[i] = (d_masks[i] != 0) for i < n: a scheme's coverage of its target
+ * set (MultipleRank1Lattice coverage, lattice.py) as bytes; d_out 8-byte
+ * aligned. */
+int sfft_masks_covered(const uint64_t* d_masks, int64_t n, uint8_t* d_out, void* stream);
 
 /* ---- K3: alias histogram, masks, coverage --------------------------------
  * Replaces construct.py:139-143 (_alias_free_mask) evaluated for every prime

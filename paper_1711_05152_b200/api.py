@@ -209,7 +209,8 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         words = int(_native.query("sfft_alias_scratch_words", hptr(ms), len(ms)))
         early["bufs"] = (dev.empty((max(words, 1),), torch.int32), dev.empty((n,), torch.int64),
                          dev.empty((2,), torch.int32))
-        early["words_h"] = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
+        early["cov_h"] = torch.empty((max(n, 8),), dtype=torch.uint8, pin_memory=True)
+        early["cov_d"] = dev.empty((max(n, 8),), torch.uint8)
 
     def defer_extent():
         """Skip the read-back of the rows' extent before the alias kernel when
@@ -245,22 +246,28 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     else:
         res = run_step(dev, oracle, cand, sch, [tail], d, delta, n if cap is None else int(cap),
                        defer_cap=True, prep=sch.prep)
-    words_h = early.get("words_h")
-    if words_h is None:
-        words_h = torch.empty((n * 8,), dtype=torch.uint8, pin_memory=True)
+    cov_h, cov_d = early.get("cov_h"), early.get("cov_d")
+    if cov_h is None:
+        cov_h = torch.empty((max(n, 8),), dtype=torch.uint8, pin_memory=True)
+        cov_d = dev.empty((max(n, 8),), torch.uint8)
+    # the coverage flags (masks != 0) on the device and their n bytes back, on
+    # a side stream while the sampling kernel runs
     side = dev.copy_stream()
     side.wait_event(ready)
     from . import _native
-    _native.call("sfft_copy_async", words_h.data_ptr(), sch.masks.data_ptr(), n * 8, side.cuda_stream,
-                 ctx="masks read-back")
+    _native.call("sfft_masks_covered", sch.masks.data_ptr(), n, cov_d.data_ptr(), side.cuda_stream,
+                 ctx="coverage flags")
+    _native.call("sfft_copy_async", cov_h.data_ptr(), cov_d.data_ptr(), n, side.cuda_stream,
+                 ctx="coverage read-back")
     sch.masks.record_stream(side)
+    cov_d.record_stream(side)
     res.finalize()  # cap applied (if binding) before the results are read
     coef, keep = dev.download_many(res.coef[0], res.keep[0])
     side.synchronize()
-    words = words_h.numpy()
-    d2h = coef.nbytes + keep.nbytes + words.nbytes
+    covered = cov_h.numpy()[:n].view(bool)
+    d2h = coef.nbytes + keep.nbytes + n
     coef = coef.view(np.complex128).reshape(n)  # views of fresh pinned buffers: no host copy
-    return StepReport(coef, words.view(np.uint64) != 0, keep.view(bool),
+    return StepReport(coef, covered, keep.view(bool),
                       sch.primes[: sch.L], sch.z[: sch.L], sch.attempts, res.nodes, h2d, d2h)
 
 

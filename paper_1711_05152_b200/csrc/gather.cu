@@ -417,6 +417,31 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ in, int64_t n_in,
   }
 }
 
+// covered[i] = (masks[i] != 0): the coverage flags of a scheme (the union of
+// the reconstructing sets, MultipleRank1Lattice coverage) as bytes, 8 per thread
+__global__ void masks_covered_kernel(const uint64_t* __restrict__ masks, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x * 8) {
+    if (i0 + 8 <= n) {
+      uint64_t packed = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) packed |= (uint64_t)(masks[i0 + k] != 0ull ? 1 : 0) << (8 * k);
+      *(uint64_t*)(out + i0) = packed;  // out is 8-byte aligned (caller's buffer start, i0 % 8 == 0)
+    } else {
+      for (int64_t i = i0; i < n; ++i) out[i] = masks[i] != 0ull ? 1 : 0;
+    }
+  }
+}
+
+int launch_masks_covered(const uint64_t* masks, int64_t n, uint8_t* out, int num_sms, cudaStream_t st) {
+  if (n <= 0) return 0;
+  int64_t want = (n + 8 * 256 - 1) / (8 * 256);
+  const int64_t cap = (int64_t)num_sms * 8;
+  masks_covered_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(masks, n, out);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
 int launch_gather_rows(const int32_t* in, int64_t n_in, int ncomp, const int32_t* idx,
                        const int32_t* count, int64_t cap_rows, int32_t* out, int64_t out_stride,
                        const double2* cin, double2* cout, int num_sms, cudaStream_t st) {

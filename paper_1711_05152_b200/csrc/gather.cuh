@@ -19,6 +19,7 @@ int launch_combine_units(int64_t n, int L, const uint64_t* masks, const double2*
 int64_t scan_scratch_len(int64_t n);
 int launch_flag_indices(const uint8_t* flags, int64_t n, int nrows, int32_t* idx_out,
                         int32_t* total, int32_t* scratch, cudaStream_t st);
+int launch_masks_covered(const uint64_t* masks, int64_t n, uint8_t* out, int num_sms, cudaStream_t st);
 int launch_gather_rows(const int32_t* in, int64_t n_in, int ncomp, const int32_t* idx,
                        const int32_t* count, int64_t cap_rows, int32_t* out, int64_t out_stride,
                        const double2* cin, double2* cout, int num_sms, cudaStream_t st);
