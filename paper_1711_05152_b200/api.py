@@ -181,6 +181,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         host_rows = torch.from_numpy(np.ascontiguousarray(np.asarray(candidates, dtype=np.int64)))
     if host_rows.dim() != 2 or not host_rows.shape[0]:
         raise ValueError("candidates must be a nonempty (n, d) integer array")
+    d_rows = DeviceFreqs.upload_rows(dev, host_rows)  # the largest input first: its DMA starts now
     n, t1 = (int(x) for x in host_rows.shape)
     d = oracle.dim
     tail = np.zeros(d - t1) if anchor_tail is None else np.asarray(anchor_tail, dtype=np.float64)
@@ -190,7 +191,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
     h2d = n * t1 * 8
     if hasattr(oracle, "device_terms"):
         # the oracle's terms are inputs of the call too: copied every call
-        # (asynchronously, ahead of the candidate rows)
+        # (asynchronously, behind the candidate rows)
         oracle._dev_cache.pop(dev.index, None)
         hf, cf = oracle.device_terms(dev)
         h2d += hf.numel() * 4 + cf.numel() * 8
@@ -220,7 +221,7 @@ def reconstruct_step(candidates, oracle, *, b: int = 10, seed_seq=None, delta: f
         return bool(spec) and t1 * float(2**31 - 1) * float(max(spec[0].primes)) < 4503599627370496.0
 
     cand, lo, hi = DeviceFreqs.from_rows_tensor(dev, host_rows, before_sync=ahead if fresh else None,
-                                                defer=defer_extent)
+                                                defer=defer_extent, d_rows=d_rows)
     guess = spec[0] if spec else None
     prepare = lambda ms, z: prepare_step(dev, oracle, cand, 1, ms, z, tails=[tail], d=d)  # noqa: E731
     if hi is None:  # deferred: alias with the guess, extent read back with the stats

@@ -83,15 +83,11 @@ class DeviceFreqs:
         t = dev.upload(np.ascontiguousarray(rows.T.astype(np.int32)))
         return cls(t, rows.shape[0], kmax)
 
-    @classmethod
-    def from_rows_tensor(cls, dev: Device, rows, before_sync=None,
-                         defer: bool = False) -> tuple["DeviceFreqs", object, object]:
-        """Upload (n, d) int64 rows (a CPU tensor; pinned memory makes the copy
-        asynchronous DMA) and pack them on the device; also returns the
-        per-component minima and maxima.  ``before_sync()`` runs while the
-        copy is in flight.  ``defer``: no read-back; returns (set with kmax =
-        the int32 bound, the device extent tensor, None) and the caller reads
-        the extent later with ``extent_of`` (one synchronisation fewer)."""
+    @staticmethod
+    def upload_rows(dev: Device, rows):
+        """Start the copy of (n, d) int64 host rows (a CPU tensor) to the
+        device on the engine stream (asynchronous DMA when pinned); the
+        result goes to ``from_rows_tensor(d_rows=...)``."""
         torch = dev.torch
         n, d = (int(x) for x in rows.shape)
         if rows.is_pinned() and rows.is_contiguous() and rows.dtype == torch.int64:
@@ -100,9 +96,24 @@ class DeviceFreqs:
             if n * d:
                 _native.call("sfft_copy_async", d_rows.data_ptr(), rows.data_ptr(), n * d * 8, dev.sh,
                              ctx="row upload")
-        else:
-            with torch.cuda.stream(dev.stream):
-                d_rows = rows.to(dev.device, non_blocking=bool(rows.is_pinned()))
+            return d_rows
+        with torch.cuda.stream(dev.stream):
+            return rows.to(dev.device, non_blocking=bool(rows.is_pinned()))
+
+    @classmethod
+    def from_rows_tensor(cls, dev: Device, rows, before_sync=None,
+                         defer: bool = False, d_rows=None) -> tuple["DeviceFreqs", object, object]:
+        """Upload (n, d) int64 rows (a CPU tensor; pinned memory makes the copy
+        asynchronous DMA) and pack them on the device; also returns the
+        per-component minima and maxima.  ``before_sync()`` runs while the
+        copy is in flight.  ``d_rows``: the copy already started by
+        ``upload_rows``.  ``defer``: no read-back; returns (set with kmax =
+        the int32 bound, the device extent tensor, None) and the caller reads
+        the extent later with ``extent_of`` (one synchronisation fewer)."""
+        torch = dev.torch
+        n, d = (int(x) for x in rows.shape)
+        if d_rows is None:  # (a caller may have started the copy earlier: upload_rows)
+            d_rows = cls.upload_rows(dev, rows)
         out = dev.empty((d, n), torch.int32)
         mm = dev.empty((2 * d + 1,), torch.int32)
         dev.call("sfft_pack_rows", dptr(d_rows), n, d, dptr(out), dptr(mm), ctx="pack rows")
