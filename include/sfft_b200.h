@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-/* ABI history: 4 = sfft_copy_async, sfft_masks_covered and
+/* ABI history: 4 = sfft_copy_async, sfft_zero_async, sfft_masks_covered and
  * sfft_line_sample_poly_all added (no signature changed).  3 = anchor tables of the sampling entries limited to
  * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
  * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
@@ -56,6 +56,8 @@ int sfft_device_info(int* num_sms, int* cc_major, int* cc_minor);
  * read-backs of small results into pinned host buffers (host page-locked
  * memory for an asynchronous copy), without a framework's stream switch */
 int sfft_copy_async(void* dst, const void* src, int64_t nbytes, void* stream);
+/* cudaMemsetAsync(dst, 0, nbytes, stream): zeroed counters of the engine */
+int sfft_zero_async(void* dst, int64_t nbytes, void* stream);
 /* d_out[i] = (d_masks[i] != 0) for i < n: a scheme's coverage of its target
  * set (MultipleRank1Lattice coverage, lattice.py) as bytes; d_out 8-byte
  * aligned. */

@@ -813,6 +813,12 @@ int sfft_flag_indices(const uint8_t* d_flags, int64_t n, int nrows, int32_t* d_i
   return launch_flag_indices(d_flags, n, nrows, d_idx, d_total, d_scratch, S(stream));
 }
 
+int sfft_zero_async(void* dst, int64_t nbytes, void* stream) {
+  if (nbytes < 0 || (nbytes > 0 && !dst)) return E_INVAL;
+  if (nbytes == 0) return 0;
+  return (int)cudaMemsetAsync(dst, 0, (size_t)nbytes, S(stream));
+}
+
 int sfft_masks_covered(const uint64_t* d_masks, int64_t n, uint8_t* d_out, void* stream) {
   if (n < 0 || (n > 0 && (!d_masks || !d_out)) || ((uintptr_t)d_out & 7)) return E_INVAL;
   return launch_masks_covered(d_masks, n, d_out, num_sms_current(), S(stream));

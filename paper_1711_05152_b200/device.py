@@ -88,6 +88,15 @@ class Device:
     def zeros(self, shape, dtype):
         return self.torch.zeros(shape, dtype=dtype, device=self.device)
 
+    def zeros_fast(self, shape, dtype):
+        """A zeroed device tensor through one cudaMemsetAsync of the library on
+        the engine stream (torch.zeros costs a framework fill launch)."""
+        t = self.torch.empty(shape, dtype=dtype, device=self.device)
+        nbytes = t.numel() * t.element_size()
+        if nbytes:
+            _native.call("sfft_zero_async", t.data_ptr(), nbytes, self.sh, ctx="zero fill")
+        return t
+
     def upload(self, a: np.ndarray, dtype=None, asynchronous: bool = False):
         """Host numpy -> device tensor (ordered on the engine stream).
         ``asynchronous``: stage through a pinned buffer of the upload ring and
@@ -237,6 +246,10 @@ _DEVICES: dict[int, Device] = {}
 
 def get_device(index: int | None = None) -> Device:
     torch = _torch()
+    if _DEVICES:  # CUDA is up (a Device exists): skip the availability probe
+        dev = _DEVICES.get(torch.cuda.current_device() if index is None else int(index))
+        if dev is not None:
+            return dev
     if not torch.cuda.is_available():
         raise RuntimeError(
             "paper_1711_05152_b200 requires a CUDA device (B200, sm_100a); there is no CPU fallback"

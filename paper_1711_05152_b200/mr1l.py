@@ -490,6 +490,13 @@ class _TableCache:
 _TABLES: dict[int, _TableCache] = {}
 
 
+def _table_cache(dev: Device) -> _TableCache:
+    tc = _TABLES.get(dev.index)
+    if tc is None:
+        tc = _TABLES[dev.index] = _TableCache()
+    return tc
+
+
 def clear_caches(dev: Device | None = None) -> None:
     """Drop every size-keyed cache (per-size lattice tables, FFT twiddle
     tables, the candidate-prime memo) so the next step pays what a step with
@@ -507,7 +514,7 @@ def lattice_tables(dev: Device, ms: np.ndarray, zs: np.ndarray | None, ctx: str 
     L = len(ms)
     P = fft_size(int(ms.max()))
     key = (P,) + tuple(int(m) for m in ms)
-    tc = _TABLES.setdefault(dev.index, _TableCache())
+    tc = _table_cache(dev)
     got = tc.get(key) if cache else None
     ftab = dev.fft_tables(P)
     if got is not None:
@@ -767,12 +774,12 @@ def prepare_step(dev: Device, oracle, cand: DeviceFreqs, r: int, ms_all, zs_all,
     P_all = fft_size(int(ms_all.max()))
     tabs = None
     if not cached_tables_only or \
-            _TABLES.setdefault(dev.index, _TableCache()).get((P_all,) + tuple(int(m) for m in ms_all)) is not None:
+            _table_cache(dev).get((P_all,) + tuple(int(m) for m in ms_all)) is not None:
         tabs = lattice_tables(dev, ms_all, zs32, ctx="lattice tables (prepared)")
     n = cand.n
     keep = dev.empty((r, n), torch.uint8)
     coef = dev.empty((r, n, 2), torch.float64)
-    counts = dev.zeros((r,), torch.int32)
+    counts = dev.zeros_fast((r,), torch.int32)
     # the transform buffer for all L_max lattices only while that is small
     # (the early-exit L is about half of L_max); otherwise run_step allocates
     buf = dev.empty((r * L_max, P_all, 2), torch.float64) \
@@ -844,7 +851,7 @@ def run_step(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, tails: l
     else:
         keep = dev.empty((r, n), torch.uint8)
         coef = dev.empty((r, n, 2), torch.float64)
-        counts = dev.zeros((r,), torch.int32)
+        counts = dev.zeros_fast((r,), torch.int32)
         buf = dev.empty((rb_alloc * L, P, 2), torch.float64)
         scratch = None
     nodes = 0

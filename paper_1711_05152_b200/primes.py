@@ -10,6 +10,7 @@ histograms over all candidates) runs in the CUDA library (scheme.py).
 from __future__ import annotations
 
 import math
+from functools import lru_cache
 from dataclasses import dataclass
 
 import numpy as np
@@ -43,7 +44,15 @@ _SIEVE = _Sieve()
 
 def primes_above(bound: float, count: int) -> list[int]:
     """The ``count`` smallest primes strictly greater than ``bound``."""
-    start = max(int(math.floor(bound)), 0)
+    return list(_primes_above(max(int(math.floor(bound)), 0), int(count)))
+
+
+@lru_cache(maxsize=1024)
+def _primes_above(start: int, count: int) -> tuple:
+    return tuple(_primes_above_list(start, count))
+
+
+def _primes_above_list(start: int, count: int) -> list[int]:
     out: list[int] = []
     while True:
         _SIEVE.cover(max(2 * (start + 1), 2 * start + 64))
