@@ -33,8 +33,8 @@
 extern "C" {
 #endif
 
-/* ABI history: 4 = sfft_copy_async, sfft_zero_async, sfft_masks_covered and
- * sfft_line_sample_poly_all added (no signature changed).  3 = anchor tables of the sampling entries limited to
+/* ABI history: 4 = sfft_copy_async, sfft_zero_async, sfft_masks_covered,
+ * sfft_line_points and sfft_line_sample_poly_all added (no signature changed).  3 = anchor tables of the sampling entries limited to
  * rb * (d - t1) <= 512 doubles (2 allowed 1024; larger now returns -7, E_2BIG,
  * for every d), sfft_unit_norm2 deterministic (cluster reduction). */
 #define SFFT_B200_ABI_VERSION 4
@@ -289,6 +289,11 @@ int sfft_line_select(const double* d_values, int r, int K, int64_t lo, int cap, 
 /* ---- oracle evaluation at arbitrary points (testbed.py:60-73, 116-127, 232-244)
  * d_pts: n x d row-major float64 in [0,1)^d; d_out: n complex.  These back the
  * device oracles' __call__ and the line samples of non-polynomial oracles. */
+/* The points of r anchored axis lines of every component (K points each):
+ * row g K + l (g = t r + i) = d_anchors[g d ...] with component t = g / r set
+ * to l / K; d_pts is (d r K) x d row-major (line samples of a black-box
+ * oracle at all components' lines, detect.py:175-240). */
+int sfft_line_points(const double* d_anchors, int d, int r, int K, double* d_pts, void* stream);
 int sfft_eval_poly_points(const double* d_pts, int64_t n, int d, const int32_t* d_hfreqs,
                           const double* d_hcoef, int s, double* d_out, void* stream);
 int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,

@@ -26,6 +26,7 @@ _SIGS = {
     "sfft_device_info": (_int, [_vp, _vp, _vp]),
     "sfft_copy_async": (_int, [_vp, _vp, _i64, _vp]),
     "sfft_zero_async": (_int, [_vp, _i64, _vp]),
+    "sfft_line_points": (_int, [_vp, _int, _int, _int, _vp, _vp]),
     "sfft_masks_covered": (_int, [_vp, _i64, _vp, _vp]),
     "sfft_alias_scratch_words": (_i64, [_vp, _int]),
     "sfft_alias_masks": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _int, _vp, _i64, _vp, _vp, _vp]),

@@ -38,6 +38,7 @@ int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* 
                             const double2* coef, int s, double2* out, cudaStream_t st);
 int launch_eval_bspline_points(const double* pts, int64_t n, const BsplineSpec& bs, double2* out,
                                int num_sms, cudaStream_t st);
+int launch_line_points(const double* anchors, int d, int r, int K, double* pts, int num_sms, cudaStream_t st);
 int launch_add_noise(double2* x, const double2* e, int64_t n, double scale, int num_sms,
                      cudaStream_t st);
 }
@@ -882,6 +883,11 @@ int sfft_eval_poly_points(const double* d_pts, int64_t n, int d, const int32_t* 
   if (n < 0 || d < 1 || s < 0) return E_INVAL;
   return launch_eval_poly_points(d_pts, n, d, d_hfreqs, (const double2*)d_hcoef, s,
                                  (double2*)d_out, S(stream));
+}
+
+int sfft_line_points(const double* d_anchors, int d, int r, int K, double* d_pts, void* stream) {
+  if (d < 1 || r < 1 || K < 1) return E_INVAL;
+  return launch_line_points(d_anchors, d, r, K, d_pts, num_sms_current(), S(stream));
 }
 
 int sfft_eval_bspline_points(const double* d_pts, int64_t n, int d, int ngroups,

@@ -87,6 +87,31 @@ int launch_eval_poly_points(const double* pts, int64_t n, int d, const int32_t* 
   return 0;
 }
 
+// The points of r anchored axis lines of every component t < d (K points
+// each, x_t = l / K): row (g K + l), g = t r + i, is anchors[g] with
+// component t = g / r replaced by l / K (the host's np.arange(K) / K).
+__global__ void line_points_kernel(const double* __restrict__ anchors, int d, int r, int K,
+                                   double* __restrict__ pts) {
+  const int64_t total = (int64_t)d * r * K * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / d;
+    const int c = (int)(e - row * d);
+    const int64_t g = row / K;
+    const int l = (int)(row - g * K);
+    pts[e] = c == (int)(g / r) ? (double)l / (double)K : anchors[g * d + c];
+  }
+}
+
+int launch_line_points(const double* anchors, int d, int r, int K, double* pts, int num_sms, cudaStream_t st) {
+  const int64_t total = (int64_t)d * r * K * d;
+  if (total <= 0) return 0;
+  int64_t want = (total + 255) / 256, cap = (int64_t)num_sms * 8;
+  line_points_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(anchors, d, r, K, pts);
+  SFFT_CHECK_LAUNCH();
+  return 0;
+}
+
 int launch_eval_bspline_points(const double* pts, int64_t n, const BsplineSpec& bs, double2* out,
                                int num_sms, cudaStream_t st) {
   if (n == 0) return 0;

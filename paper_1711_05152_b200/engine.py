@@ -323,11 +323,10 @@ def _detect_all_launch(dev: Device, oracle, cfg: DetectionConfig, streams):
         for t in range(d):
             _line_values(dev, oracle, t, box, anchors[t], t, 0, out=vals[t * r:(t + 1) * r])
     if not poly:
-        pts = np.repeat(np.concatenate(anchors), K, axis=0)
-        line = np.tile(np.arange(K) / K, r)
-        for t in range(d):
-            pts[t * r * K:(t + 1) * r * K, t] = line
-        d_pts = dev.upload(np.ascontiguousarray(pts), asynchronous=True)
+        # the d r K line points built on the device from the d r anchors
+        d_anchors = dev.upload(np.ascontiguousarray(np.concatenate(anchors)), asynchronous=True)
+        d_pts = dev.empty((d * r * K, d), torch.float64)
+        dev.call("sfft_line_points", dptr(d_anchors), d, r, K, dptr(d_pts), ctx="line points, all components")
         order, start, comps, scale = base.host_spec()
         dev.call("sfft_eval_bspline_points", dptr(d_pts), d * r * K, d, len(base.groups), hptr(order),
                  hptr(start), hptr(comps), hptr(scale), dptr(vals), ctx="line sampling, all components")
@@ -461,8 +460,6 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
     root = np.random.SeedSequence(cfg.rng_seed)
     detect_parent, anchor_parent, lattice_parent = root.spawn(3)
     detect_streams = detect_parent.spawn(d)
-    anchor_streams = anchor_parent.spawn(d)
-    lattice_streams = lattice_parent.spawn(d)
 
     rep = DetectionReport(detected=SparseSpectrum.from_dict({}, dim=d))
     for name in ("component_counts", "prefix_counts", "candidate_counts", "scheme_sizes",
@@ -477,6 +474,11 @@ def sparse_fft(oracle, cfg: DetectionConfig, *, device: Device | None = None,
     hoisted = None
     if _is_device_oracle(oracle) and not isinstance(oracle, NoisyOracle):
         hoisted = _detect_all_launch(dev, oracle, cfg, detect_streams)
+    # the anchors' and lattice searches' streams after the line detections are
+    # launched (each parent spawns its own children: the order between the
+    # parents does not change any stream)
+    anchor_streams = anchor_parent.spawn(d)
+    lattice_streams = lattice_parent.spawn(d)
     # host work of every step that does not depend on the previous steps,
     # done while the line detections run: the anchors (their own streams) and
     # the first lattice-search attempt's generator of each step

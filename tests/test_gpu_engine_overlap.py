@@ -104,3 +104,20 @@ def test_line_sampling_all_components_bit_identical():
     want = oracle(pts).reshape(d * r, K)
     g = dev.download(got)
     assert np.abs(g[..., 0] + 1j * g[..., 1] - want).max() <= 1e-10 * np.abs(want).max()
+
+
+def test_line_points_bit_exact():
+    """sfft_line_points builds exactly the host's line points (anchor rows,
+    component t of component t's lines set to np.arange(K) / K)."""
+    from paper_1711_05152_b200.device import dptr, get_device
+    dev = get_device()
+    d, r, K = 7, 3, 129
+    anchors = np.random.default_rng(5).random((d * r, d))
+    want = np.repeat(anchors, K, axis=0)
+    line = np.tile(np.arange(K) / K, r)
+    for t in range(d):
+        want[t * r * K:(t + 1) * r * K, t] = line
+    d_a = dev.upload(anchors)
+    pts = dev.empty((d * r * K, d), dev.torch.float64)
+    dev.call("sfft_line_points", dptr(d_a), d, r, K, dptr(pts))
+    assert np.array_equal(dev.download(pts), want)
