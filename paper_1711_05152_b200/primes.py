@@ -4,7 +4,8 @@ Restates reference construct.py:50-136: the L_max smallest primes above
 lambda = c (|I| - 1) that keep the target set distinct componentwise mod p,
 and the MLConfig formulas for L_max and lambda.  These are O(L_max) scalar
 computations per step; the data-parallel part of the construction (alias
-histograms over all candidates) runs in the CUDA library (scheme.py).
+histograms over all candidates) runs in the CUDA library (K3, csrc/alias.cu,
+driven by mr1l.build_scheme).
 """
 
 from __future__ import annotations
