@@ -261,13 +261,14 @@ def measure_fp64_peak(dev, P):
 
 
 def measure_l2_random_peak(dev, P, words: int):
-    """Measured random 32-bit L2 operation rates (G op/s) on a bitmap of the
-    alias scratch's size: atomicOr with the old value used, and loads."""
+    """Measured random 32-bit L2 operation rates (G op/s) on a region of the
+    alias scratch's size: atomicOr with the old value used (bitmap variant),
+    atomicAdd without it (RED, counter variant), and loads."""
     torch = dev.torch
     bits = dev.zeros((max(int(words), 1024),), torch.int32)
     blocks, per = dev.num_sms * 8, 64
     res = {}
-    for mode, name in ((0, "atomic_or"), (1, "load")):
+    for mode, name in ((0, "atomic_or"), (2, "red_add"), (1, "load")):
         dev.call("sfft_l2_random_peak", P.device.dptr(bits), bits.numel(), blocks, per, mode)
         dev.sync()
         best = 0.0
@@ -346,13 +347,17 @@ def secondary_rooflines(dev, sch, n, d, kernels):
     lhi = first_chunk(n, sch.primes)
     ms_np = np.asarray(sch.primes, dtype=np.int64)
     words = int(_native.query("sfft_alias_scratch_words", hptr(ms_np), lhi))
+    bitmap_words = 2 * int(sum((int(m) + 31) // 32 for m in sch.primes[:lhi]))
+    counters = words > bitmap_words  # the 32-bit counter variant (alias.cu) runs at this size
     rates = measure_l2_random_peak(dev, P, words)
     ops = n * lhi
-    floor_ms = (ops / (rates["atomic_or"] * 1e9) + ops / (rates["load"] * 1e9)) * 1e3
+    upd = "red_add" if counters else "atomic_or"
+    floor_ms = (ops / (rates[upd] * 1e9) + ops / (rates["load"] * 1e9)) * 1e3
     out["alias"]["l2_random"] = {
-        "bound": "l2_random_ops", "lattices_evaluated": lhi, "atomic_or_ops": ops, "load_ops": ops,
+        "bound": "l2_random_ops", "variant": "32-bit counters (RED add, load)" if counters else
+        "2-bit bitmaps (atomicOr with return, load)", "lattices_evaluated": lhi, f"{upd}_ops": ops, "load_ops": ops,
         "peak_gops": rates, "floor_ms": floor_ms, "frac": floor_ms / kernels["alias"] if kernels["alias"] > 0 else None,
-        "peak_source": "measured in this run: random 32-bit atomicOr / loads on an L2-resident bitmap of the "
+        "peak_source": "measured in this run: random 32-bit atomics / loads on an L2-resident region of the "
                        "alias scratch's size (sfft_l2_random_peak)"}
     return out
 

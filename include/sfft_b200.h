@@ -329,7 +329,8 @@ int sfft_fp64_peak(double* d_out, int iters, int blocks, void* stream);
 int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream);
 /* K3 roofline probe: blocks x 256 threads x per_thread random 32-bit
  * operations on a bitmap of `words` words (size it like the alias scratch so
- * it is L2-resident): mode 0 atomicOr with the old value used, mode 1 loads. */
+ * it is L2-resident): mode 0 atomicOr with the old value used, mode 1 loads,
+ * mode 2 atomicAdd with the result unused (RED, the alias counter variant). */
 int sfft_l2_random_peak(uint32_t* d_bits, int64_t words, int blocks, int per_thread, int mode, void* stream);
 
 #ifdef __cplusplus

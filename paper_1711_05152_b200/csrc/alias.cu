@@ -403,6 +403,106 @@ static int launch_alias_cluster_t(const int32_t* freqs, int64_t n, const LatTabl
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Counter variant (default when the lattices' 32-bit counters, 4 sum M bytes,
+// stay well inside L2): every (candidate, lattice) adds 1 to its residue's
+// counter with a reduction that returns nothing (RED: the SM does not wait
+// for the L2 round trip, where the bitmap variant needs the old word back to
+// detect a second hit), and a candidate is alias-free on a lattice when its
+// counter is exactly 1.  Same masks as the bitmaps for any multiplicity.
+constexpr int64_t ALIAS_COUNTER_MAX_BYTES = 32ll << 20;
+
+static bool alias_counters_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_B200_ALIAS_COUNTERS");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  return v;
+}
+
+bool alias_counters_for(const int64_t* m, int L) {
+  if (!alias_counters_enabled()) return false;
+  int64_t tot = 0;
+  for (int l = 0; l < L; ++l) tot += m[l];
+  return 4 * tot <= ALIAS_COUNTER_MAX_BYTES;
+}
+
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+alias_count_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int l0, uint32_t* __restrict__ cnt) {
+  __shared__ int64_t co[SFFT_LMAX + 1];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int l = 0; l < lt.nlat; ++l) { co[l] = acc; acc += lt.m[l]; }
+    co[lt.nlat] = acc;
+  }
+  __syncthreads();
+  const int d = lt.d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[DM];
+    load_cand<DM>(k, freqs, n, i, d);
+    for (int lb = l0; lb < lt.nlat; lb += AB) {
+#pragma unroll
+      for (int j = 0; j < AB; ++j) {
+        const int l = lb + j;
+        if (l < lt.nlat) atomicAdd(&cnt[co[l] + SFFT_RES(DM, FAST, k, lt, l)], 1u);  // RED, no return
+      }
+    }
+  }
+}
+
+template <int DM, bool FAST>
+__global__ void __launch_bounds__(256)
+alias_cmask_kernel(const int32_t* __restrict__ freqs, int64_t n, LatTable lt, int l0,
+                   const uint32_t* __restrict__ cnt, uint64_t* __restrict__ masks, int32_t* __restrict__ stats) {
+  __shared__ int64_t co[SFFT_LMAX + 1];
+  __shared__ int red[32];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int l = 0; l < lt.nlat; ++l) { co[l] = acc; acc += lt.m[l]; }
+    co[lt.nlat] = acc;
+  }
+  __syncthreads();
+  const int d = lt.d;
+  int first_max = 0, empty = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[DM];
+    load_cand<DM>(k, freqs, n, i, d);
+    uint64_t mask = l0 > 0 ? masks[i] : 0ull;
+    for (int lb = l0; lb < lt.nlat; lb += AB) {
+      uint32_t c[AB];
+#pragma unroll
+      for (int j = 0; j < AB; ++j) {  // the group's loads in flight together
+        const int l = lb + j;
+        c[j] = 0u;
+        if (l < lt.nlat) c[j] = __ldg(&cnt[co[l] + SFFT_RES(DM, FAST, k, lt, l)]);
+      }
+#pragma unroll
+      for (int j = 0; j < AB; ++j)
+        if (c[j] == 1u) mask |= (1ull << (lb + j));
+    }
+    masks[i] = mask;
+    if (mask) first_max = max(first_max, __ffsll((long long)mask));
+    else empty += 1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    first_max = max(first_max, __shfl_down_sync(0xffffffffu, first_max, o));
+    empty += __shfl_down_sync(0xffffffffu, empty, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[wid] = first_max; red[16 + wid] = empty; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int fm = 0, em = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { fm = max(fm, red[w]); em += red[16 + w]; }
+    if (fm) atomicMax(&stats[0], fm);
+    if (em) atomicAdd(&stats[1], em);
+  }
+}
+
 int64_t alias_scratch_words(const LatTable& lt) {
   int64_t acc = 0;
   for (int l = 0; l < lt.nlat; ++l) acc += (lt.m[l] + 31) >> 5;
@@ -422,7 +522,7 @@ static void launch_alias_t(const int32_t* freqs, int64_t n, const LatTable& lt, 
 // Lattices [l0, lt.nlat) of the table (l0 > 0: the masks of [0, l0) are in
 // `masks` already); `words` = bitmap scratch of all lt.nlat lattices.
 int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
-                 int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
+                 int64_t words, int64_t capacity, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
                  cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(stats, 0, 2 * sizeof(int32_t), st);
   if (e != cudaSuccess) return (int)e;
@@ -450,11 +550,44 @@ int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, ui
     if (rc) return rc;
     if (done) return 0;
   }
-  e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
-  if (e != cudaSuccess) return (int)e;
   int64_t want = (n + 255) / 256;
   int64_t cap = (int64_t)num_sms * 8;
   int blocks = (int)(want < cap ? want : cap);
+  if (alias_counters_for(lt.m, lt.nlat)) {
+    int64_t c0 = 0, c1 = 0;
+    for (int l = 0; l < lt.nlat; ++l) {
+      if (l < l0) c0 += lt.m[l];
+      c1 += lt.m[l];
+    }
+    if (c1 <= capacity) {
+      // counters of lattices [l0, nlat) zeroed; [0, l0) belong to an earlier chunk
+      e = cudaMemsetAsync(bits + c0, 0, (size_t)(c1 - c0) * sizeof(uint32_t), st);
+      if (e != cudaSuccess) return (int)e;
+#define SFFT_ALIASN_CASE(DMV)                                                                                    \
+      if (d <= DMV) {                                                                                            \
+        prof_mark(PROF_ALIAS, true, st);                                                                         \
+        if (fast) {                                                                                              \
+          alias_count_kernel<DMV, true><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits);                         \
+          alias_cmask_kernel<DMV, true><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits, masks, stats);           \
+        } else {                                                                                                 \
+          alias_count_kernel<DMV, false><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits);                        \
+          alias_cmask_kernel<DMV, false><<<blocks, 256, 0, st>>>(freqs, n, lt, l0, bits, masks, stats);          \
+        }                                                                                                        \
+        prof_mark(PROF_ALIAS, false, st);                                                                        \
+        SFFT_CHECK_LAUNCHES(2);                                                                                  \
+        return 0;                                                                                                \
+      }
+      SFFT_ALIASN_CASE(4)
+      SFFT_ALIASN_CASE(8)
+      SFFT_ALIASN_CASE(16)
+      SFFT_ALIASN_CASE(32)
+      SFFT_ALIASN_CASE(64)
+#undef SFFT_ALIASN_CASE
+      return -22;
+    }
+  }
+  e = cudaMemsetAsync(bits, 0, (size_t)words * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return (int)e;
 #define SFFT_ALIAS_CASE(DMV)                                                                 \
   if (d <= DMV) {                                                                            \
     if (fast) launch_alias_t<DMV, true>(freqs, n, lt, l0, bits, words, masks, stats, blocks, st); \

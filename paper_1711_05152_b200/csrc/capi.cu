@@ -452,6 +452,16 @@ int sfft_copy_async(void* dst, const void* src, int64_t nbytes, void* stream) {
 }
 
 int64_t sfft_alias_scratch_words(const int64_t* h_m, int L) {
+  int64_t acc = 0, tot = 0;
+  for (int l = 0; l < L; ++l) {
+    acc += (h_m[l] + 31) >> 5;
+    tot += h_m[l];
+  }
+  // two bitmaps of the lattices, or their 32-bit counters (alias.cu counter variant)
+  return alias_counters_for(h_m, L) && tot > 2 * acc ? tot : 2 * acc;
+}
+
+static int64_t alias_bitmap_words(const int64_t* h_m, int L) {
   int64_t acc = 0;
   for (int l = 0; l < L; ++l) acc += (h_m[l] + 31) >> 5;
   return 2 * acc;
@@ -464,9 +474,9 @@ int sfft_alias_masks_range(const int32_t* d_freqs, int64_t n, int t1, int64_t km
   LatTable lt;
   int rc = fill_lat(lt, h_m, h_z, l1, t1);
   if (rc) return rc;
-  const int64_t need = sfft_alias_scratch_words(h_m, l1);
+  const int64_t need = alias_bitmap_words(h_m, l1);  // the bitmaps always fit; counters when the scratch allows
   if (scratch_words < need) return E_INVAL;
-  return launch_alias(d_freqs, n, lt, l0, d_scratch, need, d_masks, d_stats,
+  return launch_alias(d_freqs, n, lt, l0, d_scratch, need, scratch_words, d_masks, d_stats,
                       fast_i32(lt, t1, kmax, h_m, l1), num_sms_current(), S(stream));
 }
 
@@ -947,7 +957,7 @@ int sfft_fp64_mma_peak(double* d_out, int iters, int blocks, void* stream) {
 }
 
 int sfft_l2_random_peak(uint32_t* d_bits, int64_t words, int blocks, int per_thread, int mode, void* stream) {
-  if (words < 1 || words > 0x7fffffffLL || blocks < 1 || per_thread < 1 || (mode != 0 && mode != 1)) return E_INVAL;
+  if (words < 1 || words > 0x7fffffffLL || blocks < 1 || per_thread < 1 || mode < 0 || mode > 2) return E_INVAL;
   return launch_l2_random_peak(d_bits, (uint32_t)words, blocks, per_thread, mode, S(stream));
 }
 

@@ -3,9 +3,12 @@
 
 namespace sfft {
 
+// words: the two bitmaps' words of lattices [0, nlat) (their layout);
+// capacity: the scratch's words (the 32-bit counter variant when they fit)
 int launch_alias(const int32_t* freqs, int64_t n, const LatTable& lt, int l0, uint32_t* bits,
-                 int64_t words, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
+                 int64_t words, int64_t capacity, uint64_t* masks, int32_t* stats, bool fast, int num_sms,
                  cudaStream_t st);
+bool alias_counters_for(const int64_t* m, int L);
 int64_t alias_scratch_words(const LatTable& lt);
 int launch_gather(const int32_t* freqs, int64_t n, const LatTable& lt, const uint64_t* masks,
                   const double2* buf, int64_t ustride, int rb, int it0, double delta, double2* coef,

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(256) l2_random_peak_kernel(uint32_t* bits, uin
     const uint32_t h = peak_hash32(tid * 131u + (uint32_t)i * 7919u);
     const uint32_t w = h % words;
     if (mode == 0) acc |= atomicOr(&bits[w], 1u << (h >> 27));
+    else if (mode == 2) atomicAdd(&bits[w], 1u);  // result unused: RED (the alias counter variant)
     else acc |= __ldg(&bits[w]);
   }
   if (acc == 0x12345678u) sink[0] = acc;  // keep the results alive

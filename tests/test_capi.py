@@ -69,7 +69,11 @@ def test_size_queries_without_gpu(lib):
         assert 2 * m - 1 <= P <= max(2 * (2 * m - 1), 4096) and _native.query("sfft_fft_table_len", P) > 0
         assert P <= 1.34 * (2 * m - 1) or P <= 4096 or P & (P - 1) == 0
     ms = np.array([7, 64, 65], dtype=np.int64)
-    assert _native.query("sfft_alias_scratch_words", ms.ctypes.data, 3) == 2 * (1 + 2 + 3)
+    # two bitmaps (2 x ceil(M/32) words per lattice) or, while they stay small,
+    # one 32-bit counter per residue: the larger of the two
+    assert _native.query("sfft_alias_scratch_words", ms.ctypes.data, 3) == max(2 * (1 + 2 + 3), 7 + 64 + 65)
+    big = np.full(20, 1_000_003, dtype=np.int64)  # 80 MB of counters: bitmaps only
+    assert _native.query("sfft_alias_scratch_words", big.ctypes.data, 20) == 2 * 20 * ((1_000_003 + 31) // 32)
     assert _native.query("sfft_scan_scratch_len", 0) == 1
     assert _native.query("sfft_scan_scratch_len", 2049) == 10  # 256-element tiles + the total
     assert _native.query("sfft_select_scratch_bytes", 100) > 500

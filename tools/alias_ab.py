@@ -2,8 +2,8 @@
 first chunk of lattices (library CUDA events), at config-1 size (|J| = 1e5,
 d = 10) and config-3 size (|J| = 6.5e5, d = 20).  The path is chosen by
 SFFT_B200_ALIAS_CLUSTER (1: cluster/DSMEM where it fits) and
-SFFT_B200_ALIAS_FUSED (0: the two-kernel L2-atomic path; default: the fused
-cooperative kernel where it fits).  ``call_ms``: CUDA events around the whole
+SFFT_B200_ALIAS_COUNTERS (0: the 2-bit bitmaps everywhere; default: 32-bit
+counters where they fit in 32 MB).  ``call_ms``: CUDA events around the whole
 call (memsets included)."""
 import ctypes
 import json
@@ -25,7 +25,7 @@ def main():
     dev = get_device()
     torch = dev.torch
     out = {"path": "cluster" if os.environ.get("SFFT_B200_ALIAS_CLUSTER") == "1" else
-           ("l2" if os.environ.get("SFFT_B200_ALIAS_FUSED") == "0" else "fused")}
+           ("bitmaps" if os.environ.get("SFFT_B200_ALIAS_COUNTERS") == "0" else "counters where they fit")}
     for name, n, d in (("config1", 100_000, 10), ("config3", 650_000, 20)):
         rows = distinct_rows(np.random.default_rng(1), n, d, 32)
         cand = DeviceFreqs.from_host(dev, rows)
