@@ -584,7 +584,7 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t x, uint64_t M, double invM)
 }
 
 template <int NP>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)  // <= 85 registers: 3 CTAs (24 warps) per SM (88 gave 2)
 sample_bspline_chain_kernel(UnitTable ut, LatTable lt, BsplineSpec bs, AnchorTable at, BsGrid bg,
                             const double2* __restrict__ chirp, double2* __restrict__ buf, int64_t ustride,
                             int apply_chirp) {
