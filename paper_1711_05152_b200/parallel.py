@@ -238,7 +238,15 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
     scd = dev.empty((W * L,), torch.int32)
     dev.call("sfft_mask_tiles", dptr(sch.masks), n, L, dptr(tc), dptr(toff), ts, W, dptr(scd),
              ctx=f"mask tiles, step {step}")
-    sc = dev.download_small(scd).astype(np.int64).reshape(W, L)
+    # read back while the units are sampled and transformed: only the packing
+    # needs the slice counts (the all-to-all's split sizes)
+    sc_wait = dev.download_async(scd)
+    sc_cache = []
+
+    def slice_counts():
+        if not sc_cache:
+            sc_cache.append(sc_wait().astype(np.int64).reshape(W, L))
+        return sc_cache[0]
     nodes = 0
     slices = []  # per chunk: (i0, rb, coef_s [W, rb, S, 2] or None)
     t1 = cand.ncomp
@@ -249,9 +257,7 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
         prepared = (prep is not None and prep.poly_ready and sch.attempts == 1 and i0 == 0 and rb == r)
         sends, plans = [], []
         for g in ranks:
-            mine, soff, ins, outs, roff = exchange_plan(sc, L, U, W, g)
-            plans.append((mine, ins, outs, roff))
-            send = dev.empty((max(int(ins.sum()), 1), 2), torch.float64)
+            mine = owned_units(U, W, g)
             if mine:
                 if prep is not None and prep.buf is not None and prep.buf.shape[1] == tabs.P \
                         and prep.buf.shape[0] >= len(mine):
@@ -264,6 +270,10 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
                 uarr = np.ascontiguousarray(np.asarray(mine, dtype=np.int32))
                 dev.call("sfft_bluestein", hptr(tabs.ms), L, rb, tabs.P, dptr(tabs.ftab), dptr(tabs.bhat),
                          dptr(tabs.chirp), dptr(buf), hptr(uarr), len(mine), ctx=f"Bluestein FFT, step {step}")
+            _, soff, ins, outs, roff = exchange_plan(slice_counts(), L, U, W, g)
+            plans.append((mine, ins, outs, roff))
+            send = dev.empty((max(int(ins.sum()), 1), 2), torch.float64)
+            if mine:
                 d_soff = dev.upload(soff, asynchronous=True)
                 dev.call("sfft_pack_units", dptr(cand.data), n, t1, cand.kmax, hptr(tabs.ms), hptr(tabs.zs), L,
                          dptr(sch.masks), dptr(buf), tabs.P, rb, hptr(uarr), len(mine), dptr(toff), ts,
