@@ -318,8 +318,9 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
             counts[i0:i0 + rb].copy_(ctot)
         dev.call("sfft_unshard_rows", dptr(kg), 1, W, rb, S, n, i0, dptr(keep), ctx=f"unshard, step {step}")
         slices.append((i0, rb, coef_s_all))
-    counts_h = dev.download_small(counts).astype(np.int64)
-    over = counts_h > cap
+    lazy = cap >= n and need_coef  # no cap can bind and every coefficient is gathered: no read-back here
+    counts_h = None if lazy else dev.download_small(counts).astype(np.int64)
+    over = np.zeros(r, dtype=bool) if lazy else counts_h > cap
     for i0, rb, coef_s_all in slices:
         if need_coef or over[i0:i0 + rb].any():
             with torch.cuda.stream(dev.stream):
@@ -329,6 +330,8 @@ def run_step_sharded(dev: Device, oracle, cand: DeviceFreqs, sch: DeviceScheme, 
                     cg = torch.empty((W * rb * S * 2,), dtype=torch.float64, device=dev.device)
                     _all_gather_flat(dev, cg, coef_s_all[0].reshape(-1), shard.group)
             dev.call("sfft_unshard_rows", dptr(cg), 16, W, rb, S, n, i0, dptr(coef), ctx=f"unshard, step {step}")
+    if lazy:
+        return StepResult(keep, coef, None, nodes, _lazy=lambda: dev.download_small(counts).astype(np.int64))
     counts_h = apply_cap_rows(dev, coef, keep, n, counts_h, cap, step)
     return StepResult(keep, coef, counts_h, nodes)
 
