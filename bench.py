@@ -638,6 +638,8 @@ def run_ours(args):
         "kernel_rooflines": others,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_call": {"mean": e2e_step, "median": float(np.median(e2e_ms)), "min": float(np.min(e2e_ms)),
+                                "max": float(np.max(e2e_ms))},
                 "api": "paper_1711_05152_b200.api.reconstruct_step (numpy in/out)",
                 "timing": "CUDA events around each call (host->device copy of the rows and terms, the step, "
                           "device->host copy of the results); L2 flushed before each call, untimed"},
