@@ -260,12 +260,23 @@ void choose_j1_search(int64_t m, int tw2, int& j1, int& nt1, int& nt2) {
   const int64_t amax = (m + 63) / 64;
   const int64_t alim = amax < 4096 ? amax : 4096;
   const double root = sqrt((double)m);
+  // Among the least-padded factorisations the tensor-core kernel (tw2 = 128)
+  // takes the widest J1: its B operand is precomputed per lattice as
+  // ceil(J2 / 128) column tiles x all terms (poly_bpanel_kernel), so fewer
+  // column tiles mean proportionally smaller panels (config 1: 5 -> 1 tiles,
+  // ~25 -> ~5 MB per lattice, L2-resident for the contraction) for the same
+  // padded node count.  The classic kernel keeps J1 near sqrt(M).
+  static const bool wide = [] {
+    const char* e = getenv("SFFT_B200_J1_WIDE");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  const bool prefer_wide = wide && tw2 == 128;
   for (int64_t a = 1; a <= alim; ++a) {
     const int64_t J1 = 64 * a;
     const int64_t J2 = (m + J1 - 1) / J1;
     const int64_t padded = J1 * tw2 * ((J2 + tw2 - 1) / tw2);
     if (best < 0 || padded < best ||
-        (padded == best && fabs((double)J1 - root) < fabs((double)bj - root))) {
+        (padded == best && (prefer_wide ? J1 > bj : fabs((double)J1 - root) < fabs((double)bj - root)))) {
       best = padded;
       bj = (int)J1;
     }
