@@ -64,6 +64,22 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
 // x mod m in [0, m) for |x| < 2^52 and 1 <= m < 2^31 (inv_m = 1.0 / m).
+// Bluestein chirp c_n = e^{-pi i (n^2 mod 2M) / M} (0 <= n < M < 2^31), the
+// value lattice_tables_kernel stores: n^2 mod 2M exactly by a Barrett step
+// (inv2m = floor((2^64 - 1) / 2M): the estimate is at most 2 below the
+// quotient), then the same sincospi call, so table and recomputation agree
+// bit for bit.
+__device__ __forceinline__ double2 chirp_at(int64_t n, int64_t m, uint64_t inv2m) {
+  const uint64_t m2 = 2 * (uint64_t)m;
+  const uint64_t x = (uint64_t)n * (uint64_t)n;
+  uint64_t r = x - __umul64hi(x, inv2m) * m2;
+  if (r >= m2) r -= m2;
+  if (r >= m2) r -= m2;
+  double s, c;
+  sincospi((double)r / (double)m, &s, &c);
+  return make_double2(c, -s);
+}
+
 __device__ __forceinline__ int64_t mod_fast(int64_t x, int64_t m, double inv_m) {
   int64_t q = (int64_t)floor((double)x * inv_m);
   int64_t r = x - q * m;

@@ -38,16 +38,14 @@ __global__ void lattice_tables_kernel(LatTable lt, double2* __restrict__ tw,
   const int l = blockIdx.y;
   const int64_t m = lt.m[l];
   const int64_t off = lt.off[l];
+  const uint64_t inv2m = ~0ull / (2 * (uint64_t)m);
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < m;
        n += (int64_t)gridDim.x * blockDim.x) {
     double s, c;
     // e^{+2 pi i n / M}: argument 2n/M for sincospi
     sincospi(2.0 * (double)n / (double)m, &s, &c);
     tw[off + n] = make_double2(c, s);
-    const int64_t m2 = 2 * m;
-    const int64_t nn = (int64_t)(((uint64_t)n * (uint64_t)n) % (uint64_t)m2);
-    sincospi((double)nn / (double)m, &s, &c);
-    chirp[off + n] = make_double2(c, -s);
+    chirp[off + n] = chirp_at(n, m, inv2m);
   }
 }
 
@@ -143,14 +141,16 @@ fft_col_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeom
   } else {
     // post-chirp: all chirp loads first, then multiply + store (one exposed
     // latency instead of one per group of four)
-    const double2* ch = chirp + ut.off[lat];
+    // (chirp == nullptr: recomputed, not read -- see chirp_at)
+    const double2* ch = chirp ? chirp + ut.off[lat] : nullptr;
+    const uint64_t inv2m = ~0ull / (2 * (uint64_t)m);
     constexpr int Q = TE / FFT_T;
     double2 cv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int f = threadIdx.x + q * FFT_T;
       const int64_t n = (int64_t)(f / C) * P2 + c0 + f % C;
-      cv[q] = n < m ? __ldg(&ch[n]) : make_double2(0.0, 0.0);
+      cv[q] = n < m ? (ch ? __ldg(&ch[n]) : chirp_at(n, m, inv2m)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -520,6 +520,17 @@ __global__ void discard_tails_kernel(double2* __restrict__ buf, int64_t ustride,
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
+// The inverse column pass recomputes the post-chirp (chirp_at, bit-identical
+// to the table) instead of reading 16 B per output point from the lattice
+// table; SFFT_B200_CHIRP_TABLE=1 reads the table (A/B).
+static bool post_chirp_table() {
+  static const bool v = [] {
+    const char* e = getenv("SFFT_B200_CHIRP_TABLE");
+    return e && strcmp(e, "1") == 0;
+  }();
+  return v;
+}
+
 static int bluestein_group(double2* buf, const UnitTable& ut, const FftGeom& g, const double2* ftab,
                            const double2* bhat, const double2* chirp, bool discard, cudaStream_t st) {
   const int64_t P = g.P;
@@ -534,7 +545,7 @@ static int bluestein_group(double2* buf, const UnitTable& ut, const FftGeom& g, 
     rc = launch_row<0>(g.te, g.p2, (total_rows + rows - 1) / rows, sm, st, buf, P, ut, g, total_rows, ftab,
                        bhat, chirp);
   if (rc) return rc;
-  rc = run_cols(true, buf, P, ut, g, 0, ftab, chirp, st);
+  rc = run_cols(true, buf, P, ut, g, 0, ftab, post_chirp_table() ? chirp : nullptr, st);
   if (rc || !discard) return rc;
   discard_tails_kernel<<<dim3(64, ut.nunits), 256, 0, st>>>(buf, P, ut, P);
   SFFT_CHECK_LAUNCH();

@@ -82,13 +82,14 @@ fft_colx_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGeo
       }
     }
   } else {
-    const double2* ch = chirp + ut.off[lat];
+    const double2* ch = chirp ? chirp + ut.off[lat] : nullptr;  // nullptr: recomputed (chirp_at)
+    const uint64_t inv2m = ~0ull / (2 * (uint64_t)m);
     double2 cv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int f = threadIdx.x + q * FFT_T;
       const int64_t n = (int64_t)(f / C) * P2 + c0 + f % C;
-      cv[q] = (f < E && n < m) ? __ldg(&ch[n]) : make_double2(0.0, 0.0);
+      cv[q] = (f < E && n < m) ? (ch ? __ldg(&ch[n]) : chirp_at(n, m, inv2m)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -223,11 +224,14 @@ fft_colx2_kernel(double2* __restrict__ buf, int64_t ustride, UnitTable ut, FftGe
             if (r + 1 < RL) w = cmul(w, step);
           }
         } else {
-          const double2* ch = chirp + ut.off[lat];
+          // post-chirp read from the lattice table, or (chirp == nullptr)
+          // recomputed bit-identically: 16 B per output point less traffic
+          const double2* ch = chirp ? chirp + ut.off[lat] : nullptr;
+          const uint64_t inv2m = ~0ull / (2 * (uint64_t)m);
 #pragma unroll
           for (int r = 0; r < RL; ++r) {
             const int64_t n = (int64_t)(j + r * NSL) * P2 + n2;
-            if (n < m) ub[n] = cmul(v[out_slot<RL>(r)], __ldg(&ch[n]));
+            if (n < m) ub[n] = cmul(v[out_slot<RL>(r)], ch ? __ldg(&ch[n]) : chirp_at(n, m, inv2m));
           }
         }
       }

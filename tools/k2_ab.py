@@ -18,6 +18,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 VARIANTS = {  # environment switches of the variants to compare (the first is the reference)
+    "chirp_table": {"SFFT_B200_CHIRP_TABLE": "1"},
     "default": {},
 }
 
