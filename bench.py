@@ -311,6 +311,22 @@ def secondary_rooflines(dev, sch, n, d, kernels):
     bins = int(np.unpackbits(words.view(np.uint8)).sum())  # sum_l |I_l|
     sum_m = int(sch.total_size)
     out = {}
+    cap = (load_traffic() or {}).get("full_capture", {})
+
+    def class_traffic(prefixes):
+        """DRAM bytes per step of a kernel class from the committed ncu --set
+        full capture (profiles/ncu_summary.json): mean per launch of each of
+        the class's kernels, one launch of each per step."""
+        tot, found = 0.0, False
+        for kname, lst in cap.items():
+            base = kname.replace("sfft::", "")
+            if lst and any(base.startswith(q) for q in prefixes):
+                tot += sum(x["dram_bytes"] for x in lst) / len(lst)
+                found = True
+        return tot if found else None
+    traffic = {"bluestein_fft": class_traffic(("fft_colx", "fft_row2048_kernel<0>")),
+               "alias": class_traffic(("alias_count_kernel<16", "alias_cmask_kernel<16")),
+               "gather": class_traffic(("gather_kernel<16",))}
     for name, nbytes, extra in (
             ("bluestein_fft", 32 * sum_m, {"nominal_gflop": 5e-9 * sum(m * np.log2(m) for m in sch.primes[:L])}),
             ("alias", 2 * 4 * d * n, {}),
@@ -322,7 +338,8 @@ def secondary_rooflines(dev, sch, n, d, kernels):
             continue
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = dict(bound="hbm", algorithmic_bytes=nbytes, ms=ms, achieved=gbs, peak=peak, unit="GB/s",
-                         frac=gbs / peak, **extra)
+                         frac=gbs / peak, traffic=traffic[name],
+                         traffic_over_algorithmic=(traffic[name] / nbytes if traffic[name] else None), **extra)
     out["peak_source"] = src
     # K2 against the traffic any three-pass Bluestein FFT of these lengths must
     # move (P >= 2M - 1 per unit): read the M samples, write P, read P and the

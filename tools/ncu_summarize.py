@@ -33,7 +33,10 @@ def launches(path: Path):
 
 
 def raw_metrics(rep: Path):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.suffix == ".csv":  # `ncu -i rep --page raw --csv` already run on the GPU box (reports can exceed the copy-back limit)
+        txt = rep.read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
